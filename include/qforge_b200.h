@@ -1,0 +1,173 @@
+/*
+ * qforge_b200.h -- C-ABI of the B200 batched state-vector VQE engine.
+ *
+ * Plain C: pointers, sizes, int status codes; no C++/torch types.  Every entry
+ * point replaces one piece of the reference qforge hot path (paths relative to
+ * /root/reference/proj):
+ *
+ *   qf_program_create     <- Circuit / GateInstruction / Circuit::gate validation
+ *                            (include/qforge/circuit.hpp:14-83, src/circuit.cpp:178-200)
+ *                            + gate_matrix (src/circuit.cpp:202-302), compiled once
+ *                            into fused tile sweeps instead of rebuilt per energy call
+ *   qf_observable_create  <- PauliSum::add / compile_term (include/qforge/pauli.hpp:13-30,
+ *                            src/pauli.cpp:12-27, 54-85)
+ *   qf_run_state          <- run(const Circuit&, guard) (src/circuit.cpp:304-317)
+ *   qf_expectation        <- expectation_pauli(psi, obs) (src/circuit.cpp:319-347)
+ *   qf_energy_grad_batch  <- energy() + gradient() for a batch of parameter sets
+ *                            (src/variational.cpp:38-81, batch loop of vqe_run :114-131);
+ *                            gradient by the adjoint method (GradMode::adjoint, new)
+ *   qf_adam_step_device   <- adam_step (src/variational.cpp:83-101) on device-resident
+ *                            theta/m/v for vqe_run (src/variational.cpp:103-143)
+ *   qf_ctx_set_comm       <- parallel_for (include/qforge/parallel.hpp:11-26): batch or
+ *                            term sharding across GPUs, one NCCL all-reduce per call
+ *
+ * Conventions kept from the reference:
+ *   - site 0 is the most significant bit of a basis index (circuit.cpp:87, :329);
+ *   - states are complex amplitudes, interleaved (re, im), like std::complex<double>;
+ *   - precondition failures return QF_EINVAL (the C++ shim maps it to
+ *     std::invalid_argument, common.hpp:24-26); everything else is a runtime
+ *     failure (std::runtime_error).  qf_last_error() has the message.
+ *   - results never depend on the number of GPUs (parallel.hpp:9-10): every batch
+ *     slot has exactly one owner and term chunks are fixed.
+ *
+ * Calls are synchronous (they return after results are on the host) except the
+ * *_device variants, which are stream-ordered on the context's stream.
+ * A context is not thread-safe; one context per GPU per process.
+ */
+#ifndef QFORGE_B200_H
+#define QFORGE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QF_ABI_VERSION 1
+
+enum qf_status {
+    QF_OK = 0,
+    QF_EINVAL = 1,   /* precondition violated (reference: require() -> invalid_argument) */
+    QF_ERUNTIME = 2, /* runtime failure (reference: runtime_error) */
+    QF_ENOMEM = 3,
+    QF_ECUDA = 4,
+    QF_ENCCL = 5
+};
+
+enum qf_precision { QF_C64 = 0, QF_C128 = 1 };
+
+/* Gate kinds: same numbering as qforge::Gate (include/qforge/circuit.hpp:14-23). */
+enum qf_gate {
+    QF_H = 0, QF_X, QF_Y, QF_Z, QF_S,
+    QF_RX, QF_RY, QF_RZ, QF_RZZ,
+    QF_CX, QF_CZ,
+    QF_SU4, QF_CSUM, QF_SUBSPACE_RY, QF_SUBSPACE_RZ,
+    QF_UNITARY
+};
+
+/* One gate of a parameterised circuit template.  The rotation angle is
+ *   param = coef * theta[slot] + offset   (slot >= 0)
+ *   param = offset                        (slot <  0)
+ * This is GateInstruction{name, wires, params} (circuit.hpp:27-32) with the
+ * theta -> params map of AnsatzSpec::builder (variational.hpp:14-21) made
+ * explicit.  q1 = -1 for one-qubit gates.  QF_SU4 / QF_UNITARY take a constant
+ * matrix: mat indexes the `mats` table of qf_program_create (row-major 4x4
+ * complex128, a one-qubit matrix in its top-left 2x2 corner). */
+typedef struct qf_op {
+    int32_t kind;
+    int32_t q0;
+    int32_t q1;
+    int32_t slot;
+    double coef;
+    double offset;
+    int32_t mat;
+    int32_t reserved;
+} qf_op;
+
+typedef struct qf_ctx qf_ctx;
+typedef struct qf_program qf_program;
+typedef struct qf_observable qf_observable;
+
+/* Build / library info. */
+int qf_abi_version(void);
+const char* qf_last_error(void);
+
+/* ---- context: one per GPU ---- */
+int qf_ctx_create(int device, qf_ctx** out);
+int qf_ctx_destroy(qf_ctx* ctx);
+/* Memory budget (bytes) for batch state buffers; 0 = automatic (about 60% of free HBM). */
+int qf_ctx_set_memory_budget(qf_ctx* ctx, size_t bytes);
+/* Multi-GPU: one process per GPU.  Rank 0 calls qf_nccl_unique_id, ships the
+ * 128 bytes to the other ranks (e.g. torch.distributed broadcast), then every
+ * rank calls qf_ctx_set_comm.  world == 1 detaches. */
+int qf_nccl_unique_id(uint8_t out[128]);
+int qf_ctx_set_comm(qf_ctx* ctx, int rank, int world, const uint8_t unique_id[128]);
+/* Stream (cudaStream_t as void*) that *_device calls are ordered on. */
+void* qf_ctx_stream(qf_ctx* ctx);
+
+/* ---- programs (circuit templates) ---- */
+int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops,
+                      const double* mats /* [n_mats][4][4][2] or NULL */, int n_mats,
+                      int n_params, int precision, qf_program** out);
+/* Optional start state (Circuit::initial_state, circuit.hpp:58), 2^n complex128. */
+int qf_program_set_initial_state(qf_program* prog, const double* amps);
+int qf_program_destroy(qf_program* prog);
+/* Schedule introspection: number of fused tile sweeps of the forward and
+ * adjoint passes, and tile bits used. */
+int qf_program_info(const qf_program* prog, int* fwd_sweeps, int* bwd_sweeps,
+                    int* fwd_tile_bits, int* bwd_tile_bits);
+
+/* ---- observables (Pauli sums) ---- */
+/* codes: [n_terms][n_qubits], 0=I 1=X 2=Y 3=Z (pauli.hpp:11-17). */
+int qf_observable_create(qf_ctx* ctx, int n_qubits, int n_terms, const int8_t* codes,
+                         const double* w_re, const double* w_im, qf_observable** out);
+int qf_observable_destroy(qf_observable* obs);
+/* Multi-GPU split of qf_energy_grad_batch: QF_SHARD_BATCH (default) gives each
+ * rank a contiguous block of parameter sets; QF_SHARD_TERMS gives every rank the
+ * whole batch and a contiguous block of Hamiltonian terms (single large state):
+ * energies and gradients are linear in H, so the all-reduce sums the parts. */
+enum qf_shard { QF_SHARD_BATCH = 0, QF_SHARD_TERMS = 1 };
+int qf_observable_set_sharding(qf_observable* obs, int mode);
+
+/* ---- evaluation (host buffers, synchronous) ---- */
+/* run(): amps_out = U(theta)|init>, 2^n complex128 interleaved.
+ * guard_log2 reproduces run()'s memory guard (circuit.cpp:305-307). */
+int qf_run_state(qf_ctx* ctx, const qf_program* prog, const double* theta, int guard_log2,
+                 double* amps_out);
+/* expectation_pauli(run(theta), obs) as complex (re, im). */
+int qf_expectation(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs,
+                   const double* theta, double* out_re_im);
+/* energies[b] = Re<psi(theta_b)|H|psi(theta_b)>, grads[b][p] = dE/dtheta_p by the
+ * adjoint method (grads may be NULL for energies only).  thetas: [batch][n_params].
+ * With a communicator attached, all ranks pass the same full batch; each rank
+ * evaluates its share and every rank receives the full result. */
+int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs,
+                         int batch, const double* thetas, double* energies, double* grads);
+
+/* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
+ * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
+ * float64 device pointers.  Single-GPU semantics (no collective). */
+int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* prog,
+                                const qf_observable* obs, int batch,
+                                const double* d_thetas, double* d_energies,
+                                double* d_grads);
+/* Adam (variational.cpp:83-101) over batch x P device arrays, t = step count after
+ * this update (1-based). */
+int qf_adam_step_device(qf_ctx* ctx, int batch, int n_params, double* d_theta,
+                        double* d_m, double* d_v, const double* d_grad, int t, double lr,
+                        double beta1, double beta2, double eps);
+
+/* ---- instrumentation (bench.py) ---- */
+/* Number of kernel launches made by the last evaluation call, and per-class
+ * device time (ms) when timing is enabled (CUDA events on the context stream):
+ * class 0 = forward sweeps, 1 = H|psi> / energy, 2 = adjoint sweeps, 3 = other. */
+int qf_ctx_set_timing(qf_ctx* ctx, int enabled);
+int qf_ctx_last_stats(qf_ctx* ctx, long long* launches, double* ms_by_class /* [4] */,
+                      double* bytes_by_class /* [4] algorithmic HBM bytes */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QFORGE_B200_H */

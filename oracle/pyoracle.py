@@ -1,0 +1,252 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes wrapper of oracle/liboracle.so, the CPU
+restatement of the reference hot path (see qforge_oracle.h).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module.  The product (paper_2602_14167_b200)
+never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(_HERE, "liboracle.so")
+
+GATES = ["h", "x", "y", "z", "s", "rx", "ry", "rz", "rzz", "cx", "cz", "su4", "csum",
+         "subspace_ry", "subspace_rz", "unitary"]
+GID = {g: i for i, g in enumerate(GATES)}
+
+
+class QoOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("q0", ctypes.c_int32), ("q1", ctypes.c_int32),
+                ("slot", ctypes.c_int32), ("coef", ctypes.c_double), ("offset", ctypes.c_double),
+                ("mat", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class QoRng(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("stream", ctypes.c_uint64), ("counter", ctypes.c_uint64),
+                ("have_spare", ctypes.c_int32), ("pad", ctypes.c_int32), ("spare", ctypes.c_double)]
+
+
+class QoAnsatz(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("n_params", ctypes.c_int), ("n_ops", ctypes.c_int),
+                ("ops", ctypes.POINTER(QoOp)), ("mats", ctypes.c_void_p), ("init", ctypes.c_void_p),
+                ("guard_log2", ctypes.c_int)]
+
+
+class QoHamil(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("n_terms", ctypes.c_int), ("w_re", ctypes.POINTER(ctypes.c_double)),
+                ("w_im", ctypes.POINTER(ctypes.c_double)), ("codes", ctypes.POINTER(ctypes.c_int8))]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"{LIB} missing: run `make -C oracle`")
+        L = ctypes.CDLL(LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        L.qo_last_error.restype = ctypes.c_char_p
+        L.qo_rng_next_u64.restype = ctypes.c_uint64
+        L.qo_rng_uniform.restype = ctypes.c_double
+        L.qo_rng_uniform_below.restype = ctypes.c_uint64
+        L.qo_rng_uniform_below.argtypes = [ctypes.POINTER(QoRng), ctypes.c_uint64]
+        L.qo_rng_normal.restype = ctypes.c_double
+        L.qo_rng_init.argtypes = [ctypes.POINTER(QoRng), ctypes.c_uint64, ctypes.c_uint64]
+        L.qo_rng_split_child.argtypes = [ctypes.POINTER(QoRng), ctypes.c_uint64, ctypes.POINTER(QoRng)]
+        L.qo_energy.argtypes = [ctypes.POINTER(QoAnsatz), D, ctypes.POINTER(QoHamil), D]
+        L.qo_gradient.argtypes = [ctypes.POINTER(QoAnsatz), D, ctypes.POINTER(QoHamil), ctypes.c_int,
+                                  ctypes.c_double, ctypes.c_int, D]
+        L.qo_energy_grad_batch.argtypes = [ctypes.POINTER(QoAnsatz), ctypes.c_int, D, ctypes.POINTER(QoHamil),
+                                           ctypes.c_int, ctypes.c_int, D, D]
+        L.qo_vqe_run.argtypes = [ctypes.POINTER(QoAnsatz), ctypes.c_int, D, ctypes.POINTER(QoHamil),
+                                 ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, D, D, D,
+                                 ctypes.POINTER(ctypes.c_int)]
+        L.qo_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(QoOp), ctypes.c_void_p, D,
+                             ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        L.qo_expectation_pauli.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, D, D,
+                                           ctypes.POINTER(ctypes.c_int8), ctypes.c_void_p]
+        L.qo_tfim_terms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, D, D,
+                                    ctypes.POINTER(ctypes.c_int8)]
+        L.qo_heisenberg_terms.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, D, D, ctypes.POINTER(ctypes.c_int8)]
+        L.qo_random_pauli_sum.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(QoRng), ctypes.c_int,
+                                          D, D, ctypes.POINTER(ctypes.c_int8)]
+        L.qo_chain_edges.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        _lib = L
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _check(rc):
+    if rc != 0:
+        raise ValueError(lib().qo_last_error().decode())
+
+
+class Rng:
+    def __init__(self, seed=0, stream=0):
+        self.s = QoRng()
+        lib().qo_rng_init(ctypes.byref(self.s), seed, stream)
+
+    def next_u64(self):
+        return lib().qo_rng_next_u64(ctypes.byref(self.s))
+
+    def uniform(self):
+        return lib().qo_rng_uniform(ctypes.byref(self.s))
+
+    def uniform_below(self, b):
+        return lib().qo_rng_uniform_below(ctypes.byref(self.s), b)
+
+    def normal(self):
+        return lib().qo_rng_normal(ctypes.byref(self.s))
+
+    def split(self, n):
+        out = []
+        for i in range(n):
+            r = Rng.__new__(Rng)
+            r.s = QoRng()
+            lib().qo_rng_split_child(ctypes.byref(self.s), i, ctypes.byref(r.s))
+            out.append(r)
+        return out
+
+
+# ------------------------------------------------------------------ templates
+def tca_template(n, layers):
+    """tfim_chain_ansatz, variational.cpp:18-36, as an explicit slot template."""
+    ops = [(GID["h"], q, -1, -1, 1.0, 0.0, -1) for q in range(n)]
+    k = 0
+    for _ in range(layers):
+        for i in range(n):
+            ops.append((GID["rx"], i, -1, k, 1.0, 0.0, -1)); k += 1
+        for i in range(n - 1):
+            ops.append((GID["rzz"], i, i + 1, k, 1.0, 0.0, -1)); k += 1
+    return n, ops, k
+
+
+def hea_template(n, layers):
+    """SURVEY.md 8 HEA: ry all, rz all, cx ladder, per layer."""
+    ops, k = [], 0
+    for _ in range(layers):
+        for q in range(n):
+            ops.append((GID["ry"], q, -1, k, 1.0, 0.0, -1)); k += 1
+        for q in range(n):
+            ops.append((GID["rz"], q, -1, k, 1.0, 0.0, -1)); k += 1
+        for q in range(n - 1):
+            ops.append((GID["cx"], q, q + 1, -1, 1.0, 0.0, -1))
+    return n, ops, k
+
+
+class Ansatz:
+    def __init__(self, n, ops, n_params, mats=None, init=None, guard_log2=40):
+        self.n, self.n_params = n, n_params
+        self._ops = (QoOp * max(1, len(ops)))()
+        for i, o in enumerate(ops):
+            self._ops[i] = QoOp(int(o[0]), int(o[1]), int(o[2]), int(o[3]), float(o[4]), float(o[5]), int(o[6]), 0)
+        self._mats = None if mats is None else np.ascontiguousarray(np.asarray(mats, np.complex128).reshape(-1, 16))
+        self._init = None if init is None else np.ascontiguousarray(np.asarray(init, np.complex128))
+        self.s = QoAnsatz(n, n_params, len(ops), self._ops,
+                          self._mats.ctypes.data if self._mats is not None else None,
+                          self._init.ctypes.data if self._init is not None else None, guard_log2)
+
+
+class Hamil:
+    def __init__(self, n, codes, w):
+        self.n = n
+        self.codes = np.ascontiguousarray(np.asarray(codes, np.int8).reshape(-1, n))
+        w = np.asarray(w, np.complex128).reshape(-1)
+        self.wr = np.ascontiguousarray(w.real)
+        self.wi = np.ascontiguousarray(w.imag)
+        self.s = QoHamil(n, len(w), _d(self.wr), _d(self.wi),
+                         self.codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+
+
+def tfim(n, g, pbc=False):
+    T = 3 * n + 2
+    wr, wi = np.zeros(T), np.zeros(T)
+    codes = np.zeros((T, n), np.int8)
+    t = lib().qo_tfim_terms(n, int(pbc), g, _d(wr), _d(wi), codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+    _check(0 if t >= 0 else -1)
+    return Hamil(n, codes[:t], wr[:t] + 1j * wi[:t])
+
+
+def heisenberg(n, jx, jy, jz, pbc=False):
+    T = 3 * (n + 1)
+    wr, wi = np.zeros(T), np.zeros(T)
+    codes = np.zeros((T, n), np.int8)
+    t = lib().qo_heisenberg_terms(n, int(pbc), jx, jy, jz, _d(wr), _d(wi),
+                                  codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+    _check(0 if t >= 0 else -1)
+    return Hamil(n, codes[:t], wr[:t] + 1j * wi[:t])
+
+
+def random_sum(n, terms, rng: Rng, real_weights=True):
+    wr, wi = np.zeros(terms), np.zeros(terms)
+    codes = np.zeros((terms, n), np.int8)
+    lib().qo_random_pauli_sum(n, terms, ctypes.byref(rng.s), int(real_weights), _d(wr), _d(wi),
+                              codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)))
+    return Hamil(n, codes, wr + 1j * wi)
+
+
+# ------------------------------------------------------------------ engine
+def run(n, ops, theta=None, mats=None, init=None, guard_log2=40):
+    a = Ansatz(n, ops, 0 if theta is None else len(theta), mats, init)
+    th = np.ascontiguousarray(np.zeros(1) if theta is None or len(theta) == 0 else np.asarray(theta, np.float64))
+    out = np.zeros(1 << n, np.complex128)
+    _check(lib().qo_run(n, len(ops), a._ops, a.s.mats, _d(th), a.s.init, guard_log2, out.ctypes.data))
+    return out
+
+
+def expectation(n, psi, h: Hamil):
+    psi = np.ascontiguousarray(psi, np.complex128)
+    out = np.zeros(1, np.complex128)
+    _check(lib().qo_expectation_pauli(n, psi.ctypes.data, len(h.wr), _d(h.wr), _d(h.wi),
+                                      h.codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), out.ctypes.data))
+    return complex(out[0])
+
+
+MODES = {"parameter_shift": 0, "finite_diff": 1, "adjoint": 2}
+
+
+def energy(a: Ansatz, theta, h: Hamil):
+    th = np.ascontiguousarray(np.asarray(theta, np.float64).reshape(-1)) if a.n_params else np.zeros(1)
+    e = np.zeros(1)
+    _check(lib().qo_energy(ctypes.byref(a.s), _d(th), ctypes.byref(h.s), _d(e)))
+    return float(e[0])
+
+
+def gradient(a: Ansatz, theta, h: Hamil, mode="parameter_shift", fd_step=1e-5, workers=1):
+    th = np.ascontiguousarray(np.asarray(theta, np.float64).reshape(-1))
+    g = np.zeros(max(1, a.n_params))
+    _check(lib().qo_gradient(ctypes.byref(a.s), _d(th), ctypes.byref(h.s), MODES[mode], fd_step, workers, _d(g)))
+    return g[: a.n_params]
+
+
+def energy_grad_batch(a: Ansatz, thetas, h: Hamil, mode="parameter_shift", workers=1, grads=True):
+    th = np.ascontiguousarray(np.asarray(thetas, np.float64).reshape(-1, a.n_params))
+    B = th.shape[0]
+    E = np.zeros(B)
+    G = np.zeros((B, a.n_params)) if grads else None
+    _check(lib().qo_energy_grad_batch(ctypes.byref(a.s), B, _d(th), ctypes.byref(h.s), MODES[mode], workers,
+                                      _d(E), _d(G) if grads else None))
+    return E, G
+
+
+def vqe_run(a: Ansatz, theta0, h: Hamil, steps, lr, mode="parameter_shift", workers=1):
+    th = np.ascontiguousarray(np.asarray(theta0, np.float64).reshape(-1, a.n_params))
+    B = th.shape[0]
+    traces = np.zeros((B, steps + 1))
+    fin = np.zeros((B, a.n_params))
+    be = np.zeros(1)
+    bi = ctypes.c_int()
+    _check(lib().qo_vqe_run(ctypes.byref(a.s), B, _d(th), ctypes.byref(h.s), steps, lr, MODES[mode], workers,
+                            _d(traces), _d(fin), _d(be), ctypes.byref(bi)))
+    return traces, fin, float(be[0]), bi.value

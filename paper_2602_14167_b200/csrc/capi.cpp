@@ -1,0 +1,810 @@
+// capi.cpp -- the C-ABI (include/qforge_b200.h): contexts, compiled programs and
+// observables, chunked batch evaluation, NCCL sharding.
+//
+// Evaluation of one batch chunk (all on the context stream, no host sync):
+//   forward sweeps (fused tile kernels) -> H|psi> + energy partials ->
+//   adjoint sweeps with gradient taps -> fixed-order reductions.
+// The reference evaluates 1 + 2P full energies per gradient
+// (src/variational.cpp:54-81); this evaluates one forward and one adjoint pass.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qforge_b200.h"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace qfb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define QF_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_err(QF_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                         " at " #call);                                   \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+template <typename T> cudaError_t upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
+    size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+    cudaError_t e = b.reserve(bytes);
+    if (e != cudaSuccess) return e;
+    if (!v.empty()) e = cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    return e;
+}
+
+// ---- NCCL, loaded lazily (torch already ships libnccl.so.2) ----
+typedef struct { char internal[128]; } NcclId;
+typedef void* NcclComm;
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(NcclId*) = nullptr;
+    int (*commInitRank)(NcclComm*, int, NcclId, int) = nullptr;
+    int (*allReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*commDestroy)(NcclComm) = nullptr;
+    const char* (*errStr)(int) = nullptr;
+    bool load(std::string& why) {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so",
+                               "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+        for (const char* nm : names) {
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) {
+            why = "cannot load libnccl.so.2";
+            return false;
+        }
+        getUniqueId = (int (*)(NcclId*))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (int (*)(NcclComm*, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+        allReduce = (int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllReduce");
+        commDestroy = (int (*)(NcclComm))dlsym(h, "ncclCommDestroy");
+        errStr = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !errStr) {
+            why = "libnccl.so.2 lacks required symbols";
+            return false;
+        }
+        return true;
+    }
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+}  // namespace
+
+struct qf_observable;
+
+struct DevPass {
+    DevBuf phases, ops;
+};
+
+struct qf_program {
+    qf_ctx* ctx = nullptr;
+    ProgramPlan plan;
+    DevBuf gates, cmats;
+    DevPass fwd, bwd;
+    DevBuf slot_ptr, slot_taps, slot_coef;
+    DevBuf init;  // optional initial state (RT)
+    bool has_init = false;
+};
+
+struct ObsDev {
+    ObservablePlan plan;
+    DevBuf groups, terms;
+    bool ready = false;
+};
+
+struct qf_observable {
+    qf_ctx* ctx = nullptr;
+    int n = 0;
+    std::vector<int8_t> codes;
+    std::vector<double> w_re, w_im;
+    ObsDev dev[2];         // per precision (tile bits differ)
+    bool term_shard = false;
+    int shard_world = 0;   // term-sharded sub-plan cache key
+    ObsDev shard_dev[2];
+};
+
+struct qf_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    size_t budget = 0;
+    DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init;
+    HostBuf pin;
+    // NCCL
+    NcclComm comm = nullptr;
+    int rank = 0, world = 1;
+    // stats
+    bool timing = false;
+    long long launches = 0;
+    double ms[4] = {0, 0, 0, 0};
+    double bytes[4] = {0, 0, 0, 0};
+    cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+int ensure_obs_dev(qf_observable* o, int prec, int kh, ObsDev& d, int t_begin, int t_end) {
+    if (d.ready && d.plan.kh == kh) return QF_OK;
+    std::string e = build_observable_plan(o->n, t_end - t_begin, o->codes.data() + (size_t)t_begin * o->n,
+                                          o->w_re.data() + t_begin, o->w_im.data() + t_begin, kh, d.plan);
+    if (!e.empty()) return set_err(QF_EINVAL, e);
+    cudaStream_t s = o->ctx->stream;
+    QF_CUDA(upload(d.groups, d.plan.groups, s));
+    QF_CUDA(upload(d.terms, d.plan.terms, s));
+    d.ready = true;
+    (void)prec;
+    return QF_OK;
+}
+
+size_t vsize(int prec) { return prec == QF_C128 ? 16 : 8; }
+
+// one chunk: [b0, b0 + bc) of d_thetas rows
+int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const double* d_thetas,
+               double* d_E, double* d_Eim, double* d_G, ObsDev* od_im) {
+    const ProgramPlan& P = prog->plan;
+    const int n = P.n, prec = P.prec;
+    const size_t N = size_t(1) << n;
+    const size_t vs = vsize(prec);
+    cudaStream_t s = ctx->stream;
+    const bool grads = d_G != nullptr;
+    const int P_ = P.n_params;
+    auto tick = [&](int i) {
+        if (ctx->timing) cudaEventRecord(ctx->ev[i], s);
+    };
+    auto tock = [&](int i, int cls) {
+        if (ctx->timing) {
+            cudaEventRecord(ctx->ev[i + 1], s);
+            cudaEventSynchronize(ctx->ev[i + 1]);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]);
+            ctx->ms[cls] += ms;
+        }
+    };
+
+    // --- forward ---
+    tick(0);
+    SweepArgs sa{};
+    sa.psi = ctx->psi.p;
+    sa.lam = ctx->lam.p;
+    sa.theta = d_thetas;
+    sa.P = P_;
+    sa.n = n;
+    sa.batch_offset = b0;
+    sa.gates = (const DevGate*)prog->gates.p;
+    sa.cmats = (const double*)prog->cmats.p;
+    const bool first_from_zero = !prog->has_init && !P.fwd.sweeps.empty();
+    if (prog->has_init) {
+        QF_CUDA(launch_init_state(prec, ctx->psi.p, prog->init.p, n, bc, s));
+        ctx->launches++;
+    } else if (P.fwd.sweeps.empty()) {
+        QF_CUDA(launch_init_state(prec, ctx->psi.p, ctx->zero_init.p, n, bc, s));
+        ctx->launches++;
+    }
+    sa.phases = (const DevPhase*)prog->fwd.phases.p;
+    sa.ops = (const DevOp*)prog->fwd.ops.p;
+    for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
+        sa.sw = P.fwd.sweeps[i];
+        sa.from_zero = (i == 0 && first_from_zero) ? 1 : 0;
+        QF_CUDA(launch_sweep(prec, false, sa, bc, P.fwd.max_mat, 0, s));
+        ctx->launches++;
+        ctx->bytes[0] += (double)bc * N * vs * (sa.from_zero ? 1 : 2);
+    }
+    if (!prog->has_init && P.fwd.sweeps.empty()) ctx->bytes[0] += (double)bc * N * vs;
+    tock(0, 0);
+
+    // --- H|psi>, energy ---
+    tick(2);
+    const int kh = od->plan.kh;
+    const int tiles_h = 1 << (n - kh);
+    HArgs ha{};
+    ha.psi = ctx->psi.p;
+    ha.lam = ctx->lam.p;
+    ha.n = n;
+    ha.kh = kh;
+    ha.groups = (const DevGroup*)od->groups.p;
+    ha.n_groups = (int)od->plan.groups.size();
+    ha.terms = (const DevTerm*)od->terms.p;
+    ha.write_lam = grads ? 1 : 0;
+    ha.use_imag = 0;
+    ha.epart = (double*)ctx->epart.p;
+    QF_CUDA(launch_hpsi(prec, ha, bc, s));
+    ctx->launches++;
+    ctx->bytes[1] += (double)bc * N * vs * (ha.n_groups + (grads ? 1 : 0));
+    ReduceArgs ra{};
+    ra.part = (const double*)ctx->epart.p;
+    ra.count = 1;
+    ra.tiles = tiles_h;
+    ra.out = d_E + b0;
+    QF_CUDA(launch_reduce(ra, bc, s));
+    ctx->launches++;
+    if (d_Eim && od_im) {
+        HArgs hi = ha;
+        hi.groups = (const DevGroup*)od_im->groups.p;
+        hi.n_groups = (int)od_im->plan.groups.size();
+        hi.terms = (const DevTerm*)od_im->terms.p;
+        hi.write_lam = 0;
+        hi.use_imag = 1;
+        QF_CUDA(launch_hpsi(prec, hi, bc, s));
+        ra.out = d_Eim + b0;
+        QF_CUDA(launch_reduce(ra, bc, s));
+        ctx->launches += 2;
+    }
+    tock(2, 1);
+
+    // --- adjoint ---
+    if (grads) {
+        tick(4);
+        const int nt = P.bwd.n_taps;
+        const int tiles_b = 1 << (n - P.bwd.k);
+        sa.phases = (const DevPhase*)prog->bwd.phases.p;
+        sa.ops = (const DevOp*)prog->bwd.ops.p;
+        sa.from_zero = 0;
+        sa.tap_part = (double*)ctx->tap_part.p;
+        sa.n_taps_total = nt;
+        for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) {
+            sa.sw = P.bwd.sweeps[i];
+            QF_CUDA(launch_sweep(prec, true, sa, bc, P.bwd.max_mat, P.bwd.max_taps, s));
+            ctx->launches++;
+            ctx->bytes[2] += (double)bc * N * vs * 4;
+        }
+        tock(4, 2);
+        tick(6);
+        if (nt > 0) {
+            ReduceArgs rt{};
+            rt.part = (const double*)ctx->tap_part.p;
+            rt.count = nt;
+            rt.tiles = tiles_b;
+            rt.out = (double*)ctx->tapsum.p;
+            QF_CUDA(launch_reduce(rt, bc, s));
+            ctx->launches++;
+        }
+        QF_CUDA(launch_gather_grads((const double*)ctx->tapsum.p, nt, (const int*)prog->slot_ptr.p,
+                                    (const int*)prog->slot_taps.p, (const double*)prog->slot_coef.p,
+                                    P_, bc, d_G + (size_t)b0 * P_, s));
+        ctx->launches++;
+        tock(6, 3);
+    }
+    return QF_OK;
+}
+
+// Evaluate rows [0, batch) of device thetas into device outputs (chunked).
+int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, const double* d_thetas,
+                double* d_E, double* d_Eim, double* d_G, bool term_shard) {
+    const ProgramPlan& P = prog->plan;
+    if (obs->n != P.n) return set_err(QF_EINVAL, "expectation_pauli: size mismatch");
+    if (d_G && !P.adjoint_ok) return set_err(QF_EINVAL, P.adjoint_error);
+    const int prec = P.prec, n = P.n;
+    const Geometry geo = geometry(prec, n);
+    ObsDev* od = &obs->dev[prec];
+    int rc;
+    if (term_shard && ctx->world > 1) {
+        const int T = (int)obs->w_re.size();
+        const int t0 = (int)((long long)T * ctx->rank / ctx->world);
+        const int t1 = (int)((long long)T * (ctx->rank + 1) / ctx->world);
+        if (obs->shard_world != ctx->world) {
+            obs->shard_dev[0].ready = obs->shard_dev[1].ready = false;
+            obs->shard_world = ctx->world;
+        }
+        od = &obs->shard_dev[prec];
+        rc = ensure_obs_dev(obs, prec, geo.kh, *od, t0, t1);
+    } else {
+        rc = ensure_obs_dev(obs, prec, geo.kh, *od, 0, (int)obs->w_re.size());
+    }
+    if (rc) return rc;
+    ObsDev* od_im = (d_Eim && od->plan.has_imag) ? od : nullptr;
+    if (d_Eim && !od_im) QF_CUDA(cudaMemsetAsync(d_Eim, 0, sizeof(double) * batch, ctx->stream));
+
+    const size_t N = size_t(1) << n;
+    const size_t vs = vsize(prec);
+    const bool grads = d_G != nullptr;
+    const int nt = P.bwd.n_taps;
+    const size_t tiles_b = size_t(1) << (n - P.bwd.k);
+    const size_t tiles_h = size_t(1) << (n - geo.kh);
+    const size_t per_entry = N * vs * (grads ? 2 : 1) + (grads ? (size_t)nt * tiles_b * 8 + (size_t)nt * 8 : 0) +
+                             tiles_h * 8;
+    size_t budget = ctx->budget;
+    if (!budget) {
+        size_t fr = 0, tot = 0;
+        QF_CUDA(cudaMemGetInfo(&fr, &tot));
+        budget = (size_t)(0.6 * (double)(fr + ctx->psi.cap + ctx->lam.cap + ctx->tap_part.cap));
+    }
+    long long bc = std::max<long long>(1, (long long)(budget / per_entry));
+    bc = std::min<long long>(bc, batch);
+    bc = std::min<long long>(bc, 65535);
+    // even chunks
+    const long long nchunks = (batch + bc - 1) / bc;
+    bc = (batch + nchunks - 1) / nchunks;
+    QF_CUDA(ctx->psi.reserve(bc * N * vs));
+    if (grads) {
+        QF_CUDA(ctx->lam.reserve(bc * N * vs));
+        QF_CUDA(ctx->tap_part.reserve(std::max<size_t>(16, bc * (size_t)nt * tiles_b * 8)));
+        QF_CUDA(ctx->tapsum.reserve(std::max<size_t>(16, bc * (size_t)nt * 8)));
+    }
+    QF_CUDA(ctx->epart.reserve(bc * tiles_h * 8));
+    if (!prog->has_init && P.fwd.sweeps.empty()) {
+        if (ctx->zero_init.cap < N * vs) {
+            QF_CUDA(ctx->zero_init.reserve(N * vs));
+        }
+        QF_CUDA(cudaMemsetAsync(ctx->zero_init.p, 0, N * vs, ctx->stream));
+        if (prec == QF_C128) {
+            double one[2] = {1.0, 0.0};
+            QF_CUDA(cudaMemcpyAsync(ctx->zero_init.p, one, 16, cudaMemcpyHostToDevice, ctx->stream));
+        } else {
+            float one[2] = {1.0f, 0.0f};
+            QF_CUDA(cudaMemcpyAsync(ctx->zero_init.p, one, 8, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        QF_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    for (long long b0 = 0; b0 < batch; b0 += bc) {
+        const int c = (int)std::min<long long>(bc, batch - b0);
+        rc = eval_chunk(ctx, prog, od, (int)b0, c, d_thetas, d_E, d_Eim, d_G, od_im);
+        if (rc) return rc;
+    }
+    return QF_OK;
+}
+
+int check_thetas(const qf_program* prog, int batch, const double* thetas) {
+    const ProgramPlan& P = prog->plan;
+    for (const auto& gi : P.gates) {
+        if (gi.g.slot < 0) continue;
+        for (int b = 0; b < batch; ++b) {
+            const double p = gi.g.coef * thetas[(size_t)b * P.n_params + gi.g.slot] + gi.g.offset;
+            if (!std::isfinite(p)) return set_err(QF_EINVAL, "Circuit: non-finite parameter");
+        }
+    }
+    return QF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qf_abi_version(void) { return QF_ABI_VERSION; }
+const char* qf_last_error(void) { return g_err.c_str(); }
+
+int qf_ctx_create(int device, qf_ctx** out) {
+    if (!out) return set_err(QF_EINVAL, "qf_ctx_create: null out");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return set_err(QF_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= count) return set_err(QF_EINVAL, "qf_ctx_create: bad device index");
+    QF_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    QF_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return set_err(QF_ECUDA, "qf_ctx_create: this build targets sm_100a (B200)");
+    qf_ctx* c = new qf_ctx();
+    c->device = device;
+    QF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& ev : c->ev) QF_CUDA(cudaEventCreate(&ev));
+    *out = c;
+    return QF_OK;
+}
+
+int qf_ctx_destroy(qf_ctx* c) {
+    if (!c) return QF_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->comm) g_nccl.commDestroy(c->comm);
+    for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init})
+        b->release();
+    c->pin.release();
+    for (auto& ev : c->ev) cudaEventDestroy(ev);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return QF_OK;
+}
+
+int qf_ctx_set_memory_budget(qf_ctx* c, size_t bytes) {
+    if (!c) return set_err(QF_EINVAL, "null context");
+    c->budget = bytes;
+    return QF_OK;
+}
+
+void* qf_ctx_stream(qf_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int qf_nccl_unique_id(uint8_t out[128]) {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    std::string why;
+    if (!g_nccl.load(why)) return set_err(QF_ENCCL, why);
+    NcclId id;
+    int r = g_nccl.getUniqueId(&id);
+    if (r) return set_err(QF_ENCCL, std::string("ncclGetUniqueId: ") + g_nccl.errStr(r));
+    std::memcpy(out, id.internal, 128);
+    return QF_OK;
+}
+
+int qf_ctx_set_comm(qf_ctx* c, int rank, int world, const uint8_t unique_id[128]) {
+    if (!c) return set_err(QF_EINVAL, "null context");
+    if (world < 1 || rank < 0 || rank >= world) return set_err(QF_EINVAL, "qf_ctx_set_comm: bad rank/world");
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (c->comm) {
+        g_nccl.commDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    c->rank = rank;
+    c->world = world;
+    if (world == 1) return QF_OK;
+    std::string why;
+    if (!g_nccl.load(why)) return set_err(QF_ENCCL, why);
+    QF_CUDA(cudaSetDevice(c->device));
+    NcclId id;
+    std::memcpy(id.internal, unique_id, 128);
+    int r = g_nccl.commInitRank(&c->comm, world, id, rank);
+    if (r) return set_err(QF_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.errStr(r));
+    return QF_OK;
+}
+
+int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, const double* mats,
+                      int n_mats, int n_params, int precision, qf_program** out) {
+    if (!ctx || !out) return set_err(QF_EINVAL, "qf_program_create: null argument");
+    if (n_ops < 0 || (n_ops > 0 && !ops)) return set_err(QF_EINVAL, "qf_program_create: bad ops");
+    std::vector<GateSpec> specs(n_ops);
+    for (int i = 0; i < n_ops; ++i)
+        specs[i] = GateSpec{ops[i].kind, ops[i].q0, ops[i].q1, ops[i].slot, ops[i].coef, ops[i].offset, ops[i].mat};
+    qf_program* p = new qf_program();
+    p->ctx = ctx;
+    std::string e = build_program_plan(n_qubits, specs, mats, n_mats, n_params, precision, p->plan);
+    if (!e.empty()) {
+        delete p;
+        return set_err(QF_EINVAL, e);
+    }
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    std::vector<DevGate> dg(p->plan.gates.size());
+    for (size_t i = 0; i < dg.size(); ++i) {
+        const GateSpec& g = p->plan.gates[i].g;
+        dg[i] = DevGate{g.kind, g.slot, g.coef, g.offset, g.mat, g.q0, g.q1};
+    }
+    auto fail = [&](cudaError_t ce) {
+        delete p;
+        return set_err(QF_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(ce));
+    };
+    cudaError_t ce;
+    if ((ce = upload(p->gates, dg, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->cmats, p->plan.mats, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->fwd.phases, p->plan.fwd.phases, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->fwd.ops, p->plan.fwd.ops, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->bwd.phases, p->plan.bwd.phases, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->bwd.ops, p->plan.bwd.ops, s)) != cudaSuccess) return fail(ce);
+    // slot -> taps CSR (taps summed in tap order: deterministic)
+    const int P = n_params;
+    std::vector<int> cnt(P + 1, 0), ptr(P + 1, 0), taps;
+    std::vector<double> coef;
+    for (const auto& t : p->plan.bwd.taps) cnt[t.slot]++;
+    for (int i = 0; i < P; ++i) ptr[i + 1] = ptr[i] + cnt[i];
+    taps.resize(ptr[P]);
+    coef.resize(ptr[P]);
+    std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t t = 0; t < p->plan.bwd.taps.size(); ++t) {
+        const auto& tp = p->plan.bwd.taps[t];
+        taps[fill[tp.slot]] = (int)t;
+        coef[fill[tp.slot]++] = tp.coef;
+    }
+    if ((ce = upload(p->slot_ptr, ptr, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->slot_taps, taps, s)) != cudaSuccess) return fail(ce);
+    if ((ce = upload(p->slot_coef, coef, s)) != cudaSuccess) return fail(ce);
+    if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return fail(ce);
+    *out = p;
+    return QF_OK;
+}
+
+int qf_program_set_initial_state(qf_program* p, const double* amps) {
+    if (!p || !amps) return set_err(QF_EINVAL, "qf_program_set_initial_state: null argument");
+    const size_t N = size_t(1) << p->plan.n;
+    cudaSetDevice(p->ctx->device);
+    if (p->plan.prec == QF_C128) {
+        QF_CUDA(p->init.reserve(N * 16));
+        QF_CUDA(cudaMemcpy(p->init.p, amps, N * 16, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> f(2 * N);
+        for (size_t i = 0; i < 2 * N; ++i) f[i] = (float)amps[i];
+        QF_CUDA(p->init.reserve(N * 8));
+        QF_CUDA(cudaMemcpy(p->init.p, f.data(), N * 8, cudaMemcpyHostToDevice));
+    }
+    p->has_init = true;
+    return QF_OK;
+}
+
+int qf_program_destroy(qf_program* p) {
+    if (!p) return QF_OK;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    for (DevBuf* b : {&p->gates, &p->cmats, &p->fwd.phases, &p->fwd.ops, &p->bwd.phases, &p->bwd.ops,
+                      &p->slot_ptr, &p->slot_taps, &p->slot_coef, &p->init})
+        b->release();
+    delete p;
+    return QF_OK;
+}
+
+int qf_program_info(const qf_program* p, int* fs, int* bs, int* fk, int* bk) {
+    if (!p) return set_err(QF_EINVAL, "null program");
+    if (fs) *fs = (int)p->plan.fwd.sweeps.size();
+    if (bs) *bs = (int)p->plan.bwd.sweeps.size();
+    if (fk) *fk = p->plan.fwd.k;
+    if (bk) *bk = p->plan.bwd.k;
+    return QF_OK;
+}
+
+int qf_observable_create(qf_ctx* ctx, int n, int n_terms, const int8_t* codes, const double* w_re,
+                         const double* w_im, qf_observable** out) {
+    if (!ctx || !out) return set_err(QF_EINVAL, "qf_observable_create: null argument");
+    if (n < 1 || n > 32) return set_err(QF_EINVAL, "observable: qubit count must be in [1, 32]");
+    if (n_terms < 0 || (n_terms > 0 && (!codes || !w_re)))
+        return set_err(QF_EINVAL, "qf_observable_create: bad terms");
+    qf_observable* o = new qf_observable();
+    o->ctx = ctx;
+    o->n = n;
+    o->codes.assign(codes, codes + (size_t)n_terms * n);
+    o->w_re.assign(w_re, w_re + n_terms);
+    o->w_im.assign(n_terms, 0.0);
+    if (w_im) o->w_im.assign(w_im, w_im + n_terms);
+    // validate now (PauliSum::add semantics, pauli.cpp:12-18)
+    ObservablePlan tmp;
+    std::string e = build_observable_plan(n, n_terms, o->codes.data(), o->w_re.data(), o->w_im.data(), n, tmp);
+    if (!e.empty()) {
+        delete o;
+        return set_err(QF_EINVAL, e);
+    }
+    *out = o;
+    return QF_OK;
+}
+
+int qf_observable_set_sharding(qf_observable* o, int mode) {
+    if (!o || (mode != QF_SHARD_BATCH && mode != QF_SHARD_TERMS))
+        return set_err(QF_EINVAL, "qf_observable_set_sharding: bad arguments");
+    o->term_shard = mode == QF_SHARD_TERMS;
+    return QF_OK;
+}
+
+int qf_observable_destroy(qf_observable* o) {
+    if (!o) return QF_OK;
+    cudaSetDevice(o->ctx->device);
+    cudaStreamSynchronize(o->ctx->stream);
+    for (auto* d : {&o->dev[0], &o->dev[1], &o->shard_dev[0], &o->shard_dev[1]}) {
+        d->groups.release();
+        d->terms.release();
+    }
+    delete o;
+    return QF_OK;
+}
+
+static int stage_thetas(qf_ctx* ctx, const qf_program* prog, int batch, const double* thetas) {
+    const size_t bytes = std::max<size_t>(16, (size_t)batch * prog->plan.n_params * sizeof(double));
+    QF_CUDA(ctx->thetas.reserve(bytes));
+    if ((size_t)batch * prog->plan.n_params > 0) {
+        QF_CUDA(ctx->pin.reserve(bytes));
+        std::memcpy(ctx->pin.p, thetas, (size_t)batch * prog->plan.n_params * sizeof(double));
+        QF_CUDA(cudaMemcpyAsync(ctx->thetas.p, ctx->pin.p, (size_t)batch * prog->plan.n_params * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return QF_OK;
+}
+
+static void reset_stats(qf_ctx* ctx) {
+    ctx->launches = 0;
+    for (int i = 0; i < 4; ++i) ctx->ms[i] = ctx->bytes[i] = 0;
+}
+
+int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
+                         const double* thetas, double* energies, double* grads) {
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    qf_observable* obs = const_cast<qf_observable*>(cobs);
+    if (!ctx || !prog || !obs || batch < 0 || (batch > 0 && (!energies || (!thetas && prog->plan.n_params))))
+        return set_err(QF_EINVAL, "qf_energy_grad_batch: bad arguments");
+    if (batch == 0) return QF_OK;
+    if (grads && !prog->plan.adjoint_ok) return set_err(QF_EINVAL, prog->plan.adjoint_error);
+    int rc = check_thetas(prog, batch, thetas);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    reset_stats(ctx);
+    const int P = prog->plan.n_params;
+    rc = stage_thetas(ctx, prog, batch, thetas);
+    if (rc) return rc;
+    // output: [E (batch)] [G (batch x P)]
+    const size_t out_n = (size_t)batch * (1 + (grads ? P : 0));
+    QF_CUDA(ctx->out.reserve(out_n * 8));
+    double* dE = (double*)ctx->out.p;
+    double* dG = grads ? dE + batch : nullptr;
+    const bool sharded = ctx->world > 1 && ctx->comm;
+    const bool term_shard = sharded && obs->term_shard;
+    if (sharded && !term_shard) {
+        // batch sharding: rank r owns rows [b0, b1); zero elsewhere; one all-reduce (exact: x + 0 = x)
+        const int b0 = (int)((long long)batch * ctx->rank / ctx->world);
+        const int b1 = (int)((long long)batch * (ctx->rank + 1) / ctx->world);
+        QF_CUDA(cudaMemsetAsync(ctx->out.p, 0, out_n * 8, ctx->stream));
+        if (b1 > b0) {
+            // evaluate rows b0..b1 into temp area then scatter: reuse thetas offset via pointer arithmetic
+            rc = eval_device(ctx, prog, obs, b1 - b0, (const double*)ctx->thetas.p + (size_t)b0 * P, dE + b0,
+                             nullptr, dG ? dG + (size_t)b0 * P : nullptr, false);
+            if (rc) return rc;
+        }
+    } else {
+        rc = eval_device(ctx, prog, obs, batch, (const double*)ctx->thetas.p, dE, nullptr, dG, term_shard);
+        if (rc) return rc;
+    }
+    if (sharded) {
+        int r = g_nccl.allReduce(ctx->out.p, ctx->out.p, out_n, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream);
+        if (r) return set_err(QF_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(r));
+    }
+    QF_CUDA(ctx->pin.reserve(out_n * 8));
+    QF_CUDA(cudaMemcpyAsync(ctx->pin.p, ctx->out.p, out_n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    QF_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(energies, ctx->pin.p, (size_t)batch * 8);
+    if (grads) std::memcpy(grads, (double*)ctx->pin.p + batch, (size_t)batch * P * 8);
+    return QF_OK;
+}
+
+int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
+                                const double* d_thetas, double* d_energies, double* d_grads) {
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    qf_observable* obs = const_cast<qf_observable*>(cobs);
+    if (!ctx || !prog || !obs || batch < 0 || (batch > 0 && !d_energies))
+        return set_err(QF_EINVAL, "qf_energy_grad_batch_device: bad arguments");
+    if (batch == 0) return QF_OK;
+    cudaSetDevice(ctx->device);
+    reset_stats(ctx);
+    return eval_device(ctx, prog, obs, batch, d_thetas, d_energies, nullptr, d_grads, false);
+}
+
+int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int guard_log2, double* amps_out) {
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    if (!ctx || !prog || !amps_out || (!theta && prog->plan.n_params))
+        return set_err(QF_EINVAL, "qf_run_state: bad arguments");
+    const int n = prog->plan.n;
+    if (!(std::pow(2.0, n) <= std::pow(2.0, (double)guard_log2)))  // circuit.cpp:305-307
+        return set_err(QF_EINVAL, "run: state dimension exceeds memory guard");
+    int rc = check_thetas(prog, 1, theta);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    reset_stats(ctx);
+    rc = stage_thetas(ctx, prog, 1, theta);
+    if (rc) return rc;
+    // forward only: use a trivial observable-free path
+    const ProgramPlan& P = prog->plan;
+    const size_t N = size_t(1) << n;
+    const size_t vs = vsize(P.prec);
+    QF_CUDA(ctx->psi.reserve(N * vs));
+    cudaStream_t s = ctx->stream;
+    if (prog->has_init) {
+        QF_CUDA(launch_init_state(P.prec, ctx->psi.p, prog->init.p, n, 1, s));
+    } else if (P.fwd.sweeps.empty()) {
+        QF_CUDA(cudaMemsetAsync(ctx->psi.p, 0, N * vs, s));
+        if (P.prec == QF_C128) {
+            static const double one[2] = {1.0, 0.0};
+            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 16, cudaMemcpyHostToDevice, s));
+        } else {
+            static const float one[2] = {1.0f, 0.0f};
+            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 8, cudaMemcpyHostToDevice, s));
+        }
+    }
+    SweepArgs sa{};
+    sa.psi = ctx->psi.p;
+    sa.theta = (const double*)ctx->thetas.p;
+    sa.P = P.n_params;
+    sa.n = n;
+    sa.gates = (const DevGate*)prog->gates.p;
+    sa.cmats = (const double*)prog->cmats.p;
+    sa.phases = (const DevPhase*)prog->fwd.phases.p;
+    sa.ops = (const DevOp*)prog->fwd.ops.p;
+    for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
+        sa.sw = P.fwd.sweeps[i];
+        sa.from_zero = (i == 0 && !prog->has_init) ? 1 : 0;
+        QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
+        ctx->launches++;
+    }
+    if (P.prec == QF_C128) {
+        QF_CUDA(cudaMemcpyAsync(amps_out, ctx->psi.p, N * 16, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaStreamSynchronize(s));
+    } else {
+        std::vector<float> f(2 * N);
+        QF_CUDA(cudaMemcpyAsync(f.data(), ctx->psi.p, N * 8, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < 2 * N; ++i) amps_out[i] = f[i];
+    }
+    return QF_OK;
+}
+
+int qf_expectation(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, const double* theta,
+                   double* out_re_im) {
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    qf_observable* obs = const_cast<qf_observable*>(cobs);
+    if (!ctx || !prog || !obs || !out_re_im || (!theta && prog->plan.n_params))
+        return set_err(QF_EINVAL, "qf_expectation: bad arguments");
+    int rc = check_thetas(prog, 1, theta);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    reset_stats(ctx);
+    rc = stage_thetas(ctx, prog, 1, theta);
+    if (rc) return rc;
+    QF_CUDA(ctx->out.reserve(32));
+    double* dE = (double*)ctx->out.p;
+    rc = eval_device(ctx, prog, obs, 1, (const double*)ctx->thetas.p, dE, dE + 1, nullptr, false);
+    if (rc) return rc;
+    QF_CUDA(cudaMemcpyAsync(out_re_im, dE, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    QF_CUDA(cudaStreamSynchronize(ctx->stream));
+    return QF_OK;
+}
+
+int qf_adam_step_device(qf_ctx* ctx, int batch, int P, double* th, double* m, double* v, const double* g,
+                        int t, double lr, double b1, double b2, double eps) {
+    if (!ctx || batch < 0 || P < 0 || t < 1) return set_err(QF_EINVAL, "qf_adam_step_device: bad arguments");
+    cudaSetDevice(ctx->device);
+    const double c1 = 1.0 - std::pow(b1, t);
+    const double c2 = 1.0 - std::pow(b2, t);
+    QF_CUDA(launch_adam(batch * P, th, m, v, g, lr, b1, b2, eps, c1, c2, ctx->stream));
+    return QF_OK;
+}
+
+int qf_ctx_set_timing(qf_ctx* ctx, int enabled) {
+    if (!ctx) return set_err(QF_EINVAL, "null context");
+    ctx->timing = enabled != 0;
+    return QF_OK;
+}
+
+int qf_ctx_last_stats(qf_ctx* ctx, long long* launches, double* ms, double* bytes) {
+    if (!ctx) return set_err(QF_EINVAL, "null context");
+    if (launches) *launches = ctx->launches;
+    for (int i = 0; i < 4; ++i) {
+        if (ms) ms[i] = ctx->ms[i];
+        if (bytes) bytes[i] = ctx->bytes[i];
+    }
+    return QF_OK;
+}
+
+}  // extern "C"

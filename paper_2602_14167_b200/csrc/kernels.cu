@@ -1,0 +1,279 @@
+// kernels.cu -- sm_100a kernels of the batched state-vector VQE engine.
+//
+// HBM-streaming kernels (no tensor-core work): every sweep reads each state
+// tile once from HBM into a swizzled shared-memory tile, applies a fused run of
+// gates in register phases, and writes it back once.  See plan.h and DESIGN.md.
+//
+// Reference behaviour being replaced (paths relative to /root/reference/proj):
+//   sweep_kernel<.., false>  <- run(): apply_local_unitary per gate (src/circuit.cpp:78-176,
+//                               304-317), gate_matrix conventions (:202-302)
+//   hpsi_kernel              <- expectation_pauli (src/circuit.cpp:319-347), extended to
+//                               also produce lambda = H|psi> for the adjoint pass
+//   sweep_kernel<.., true>   <- gradient() (src/variational.cpp:54-81): parameter shift
+//                               replaced by adjoint back-propagation with in-tile taps
+//   reduce_kernel / gather   <- the deterministic per-slot result writes of parallel_for
+//                               (include/qforge/parallel.hpp:9-10): fixed-order sums, no
+//                               float atomics
+//   adam_kernel              <- adam_step (src/variational.cpp:83-101)
+#include <cuda_runtime.h>
+
+#include "sweep_impl.cuh"
+
+namespace qfb {
+
+// ---------------------------------------------------------------------------
+// lambda = H psi and E = Re<psi|lambda>, output-stationary per tile
+// ---------------------------------------------------------------------------
+template <typename RT, int NA>
+__global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
+    using V = typename CxT<RT>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    const uint32_t TS = 1u << a.kh;
+    V* own = reinterpret_cast<V*>(smem_raw);
+    V* part = own + TS;
+    double* red = reinterpret_cast<double*>(part + TS);
+    const uint32_t tile = blockIdx.x;
+    const int b = blockIdx.y;
+    const size_t N = size_t(1) << a.n;
+    const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)b * N;
+    const uint32_t base = tile << a.kh;
+
+    V po[NA], acc[NA];
+    RT dg[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        const uint32_t p = tid + (uint32_t)T * i;
+        po[i] = ps[base + p];
+        own[p] = po[i];
+        acc[i].x = acc[i].y = RT(0);
+        dg[i] = RT(0);
+    }
+    __syncthreads();
+    for (int gi = 0; gi < a.n_groups; ++gi) {
+        const DevGroup g = a.groups[gi];
+        const V* src = own;
+        if (g.f_out) {
+            __syncthreads();
+            const V* pp = ps + (base ^ g.f_out);
+#pragma unroll
+            for (int i = 0; i < NA; ++i) part[tid + T * i] = pp[tid + T * i];
+            __syncthreads();
+            src = part;
+        }
+        for (int t = g.term_begin; t < g.term_end; ++t) {
+            const DevTerm d = a.terms[t];
+            const RT cr = (RT)(a.use_imag ? d.ci_re : d.c_re);
+            const RT ci = (RT)(a.use_imag ? d.ci_im : d.c_im);
+            const uint32_t zlo = d.z & (TS - 1);
+            const uint32_t cpar = (__popc(base & d.z) ^ d.fz_par) & 1;
+            if (d.kind == TK_DIAG) {
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const uint32_t p = tid + (uint32_t)T * i;
+                    const uint32_t par = (__popc(p & zlo) ^ cpar) & 1;
+                    dg[i] += par ? -cr : cr;
+                }
+            } else if (d.kind == TK_FLIP) {
+                V c;
+                c.x = cr;
+                c.y = ci;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const uint32_t p = tid + (uint32_t)T * i;
+                    acc[i] = cfma(c, src[p ^ d.f_in], acc[i]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const uint32_t p = tid + (uint32_t)T * i;
+                    const uint32_t par = (__popc(p & zlo) ^ cpar) & 1;
+                    V c;
+                    c.x = par ? -cr : cr;
+                    c.y = par ? -ci : ci;
+                    acc[i] = cfma(c, src[p ^ d.f_in], acc[i]);
+                }
+            }
+        }
+    }
+    double e = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        acc[i].x = fma(dg[i], po[i].x, acc[i].x);
+        acc[i].y = fma(dg[i], po[i].y, acc[i].y);
+        e += (double)po[i].x * (double)acc[i].x + (double)po[i].y * (double)acc[i].y;
+    }
+    if (a.write_lam) {
+        V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * N;
+#pragma unroll
+        for (int i = 0; i < NA; ++i) lm[base + tid + T * i] = acc[i];
+    }
+    const unsigned m = lane_mask(T);
+    for (int o = (T >= 32 ? 16 : T / 2); o > 0; o >>= 1) e += __shfl_xor_sync(m, e, o);
+    const int nwarps = (T + 31) >> 5;
+    if ((tid & 31) == 0) red[tid >> 5] = e;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0;
+        for (int w = 0; w < nwarps; ++w) s += red[w];
+        a.epart[(size_t)b * gridDim.x + tile] = s;
+    }
+}
+
+template <typename RT>
+__global__ void init_state_kernel(typename CxT<RT>::T* psi, const typename CxT<RT>::T* init, size_t N) {
+    const size_t b = blockIdx.y;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
+        psi[b * N + i] = init[i];
+}
+
+// warp per (b, item): fixed-order sum over tiles (deterministic)
+__global__ void reduce_kernel(const ReduceArgs a) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int item = blockIdx.x * (blockDim.x >> 5) + w;
+    const int b = blockIdx.y;
+    if (item >= a.count) return;
+    const double* p = a.part + ((size_t)b * a.count + item) * a.tiles;
+    double s = 0;
+    for (int t = lane; t < a.tiles; t += 32) s += p[t];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.out[(size_t)b * a.count + item] = s;
+}
+
+__global__ void gather_grads_kernel(const double* tapsum, int n_taps, const int* slot_ptr,
+                                    const int* slot_taps, const double* slot_coef, int P,
+                                    double* grads) {
+    const int b = blockIdx.y;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= P) return;
+    double g = 0;
+    for (int k = slot_ptr[s]; k < slot_ptr[s + 1]; ++k)
+        g += slot_coef[k] * tapsum[(size_t)b * n_taps + slot_taps[k]];
+    grads[(size_t)b * P + s] = g;
+}
+
+// adam_step, variational.cpp:83-101 (c1 = 1 - beta1^t, c2 = 1 - beta2^t from the host)
+__global__ void adam_kernel(int count, double* theta, double* m, double* v, const double* g,
+                            double lr, double b1, double b2, double eps, double c1, double c2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double gi = g[i];
+    const double mi = b1 * m[i] + (1.0 - b1) * gi;
+    const double vi = b2 * v[i] + (1.0 - b2) * (gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    const double mhat = mi / c1;
+    const double vhat = vi / c2;
+    theta[i] -= lr * mhat / (sqrt(vhat) + eps);
+}
+
+__global__ void convert_kernel(const float2* src, double2* dst, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = make_double2(src[i].x, src[i].y);
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+size_t sweep_smem_bytes(int prec, bool bwd, const DevSweep& sw, int max_mat, int max_taps) {
+    const size_t vs = prec == QF_C128 ? 16 : 8;
+    const size_t TS = size_t(1) << sw.k;
+    const int T = 1 << (sw.k - sw.R);
+    const int nwarps = (T + 31) / 32;
+    size_t bytes = TS * vs * (bwd ? 2 : 1);
+    bytes += (size_t)((max_mat + 1) & ~1) * vs;
+    bytes += (size_t)max_taps * nwarps * 8;
+    bytes += (size_t)(1 << sw.R) * 4;
+    return bytes;
+}
+
+cudaError_t launch_sweep_f32_fwd(const SweepArgs&, int, size_t, cudaStream_t);
+cudaError_t launch_sweep_f32_bwd(const SweepArgs&, int, size_t, cudaStream_t);
+cudaError_t launch_sweep_f64_fwd(const SweepArgs&, int, size_t, cudaStream_t);
+cudaError_t launch_sweep_f64_bwd(const SweepArgs&, int, size_t, cudaStream_t);
+
+cudaError_t launch_sweep(int prec, bool bwd, const SweepArgs& a, int batch, int max_mat,
+                         int max_taps, cudaStream_t s) {
+    const size_t smem = sweep_smem_bytes(prec, bwd, a.sw, max_mat, max_taps);
+    if (prec == QF_C128)
+        return bwd ? launch_sweep_f64_bwd(a, batch, smem, s) : launch_sweep_f64_fwd(a, batch, smem, s);
+    return bwd ? launch_sweep_f32_bwd(a, batch, smem, s) : launch_sweep_f32_fwd(a, batch, smem, s);
+}
+
+template <typename RT, int NA>
+static cudaError_t launch_hpsi_t(const HArgs& a, int batch, int T, cudaStream_t s) {
+    const size_t vs = sizeof(RT) * 2;
+    const size_t smem = ((size_t)2 << a.kh) * vs + 8 * 8;
+    auto kern = hpsi_kernel<RT, NA>;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    dim3 grid(1u << (a.n - a.kh), batch);
+    kern<<<grid, T, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename RT>
+static cudaError_t dispatch_hpsi(const HArgs& a, int batch, cudaStream_t s) {
+    const int TS = 1 << a.kh;
+    const int T = TS < 256 ? TS : 256;
+    switch (TS / T) {
+        case 1: return launch_hpsi_t<RT, 1>(a, batch, T, s);
+        case 2: return launch_hpsi_t<RT, 2>(a, batch, T, s);
+        case 4: return launch_hpsi_t<RT, 4>(a, batch, T, s);
+        case 8: return launch_hpsi_t<RT, 8>(a, batch, T, s);
+        case 16: return launch_hpsi_t<RT, 16>(a, batch, T, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_hpsi(int prec, const HArgs& a, int batch, cudaStream_t s) {
+    return prec == QF_C128 ? dispatch_hpsi<double>(a, batch, s) : dispatch_hpsi<float>(a, batch, s);
+}
+
+cudaError_t launch_init_state(int prec, void* psi, const void* init, int n, int batch, cudaStream_t s) {
+    const size_t N = size_t(1) << n;
+    dim3 grid((unsigned)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024), batch);
+    if (prec == QF_C128)
+        init_state_kernel<double><<<grid, 256, 0, s>>>((double2*)psi, (const double2*)init, N);
+    else
+        init_state_kernel<float><<<grid, 256, 0, s>>>((float2*)psi, (const float2*)init, N);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const ReduceArgs& a, int batch, cudaStream_t s) {
+    if (a.count == 0) return cudaSuccess;
+    dim3 grid((a.count + 7) / 8, batch);
+    reduce_kernel<<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_grads(const double* tapsum, int n_taps, const int* slot_ptr,
+                                const int* slot_taps, const double* slot_coef, int P, int batch,
+                                double* grads, cudaStream_t s) {
+    if (P == 0) return cudaSuccess;
+    dim3 grid((P + 127) / 128, batch);
+    gather_grads_kernel<<<grid, 128, 0, s>>>(tapsum, n_taps, slot_ptr, slot_taps, slot_coef, P, grads);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adam(int count, double* theta, double* m, double* v, const double* g, double lr,
+                        double b1, double b2, double eps, double c1, double c2, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    adam_kernel<<<(count + 255) / 256, 256, 0, s>>>(count, theta, m, v, g, lr, b1, b2, eps, c1, c2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert_state(int prec, const void* src, double* dst, int64_t count, cudaStream_t s) {
+    if (prec == QF_C128)
+        return cudaMemcpyAsync(dst, src, (size_t)count * 16, cudaMemcpyDeviceToDevice, s);
+    convert_kernel<<<1024, 256, 0, s>>>((const float2*)src, (double2*)dst, count);
+    return cudaGetLastError();
+}
+
+}  // namespace qfb

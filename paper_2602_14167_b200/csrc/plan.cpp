@@ -1,0 +1,461 @@
+// plan.cpp -- circuit template -> fused tile sweeps (see plan.h for the model).
+//
+// Replaces the reference's per-energy-call rebuild of the op list
+// (variational.cpp:41 -> builder -> Circuit::gate, circuit.cpp:178-186) and the
+// one-sweep-per-gate loop of run() (circuit.cpp:313-315): the template is
+// validated and scheduled once, then executed for every parameter set.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <map>
+#include <set>
+
+#include "../../include/qforge_b200.h"
+
+namespace qfb {
+
+Geometry geometry(int prec, int n) {
+    Geometry g;
+    if (prec == QF_C128) {
+        g.kf = 12; g.Rf = 4; g.kb = 11; g.Rb = 3; g.kh = 11; g.c = 3; g.W = 3;
+    } else {
+        g.kf = 13; g.Rf = 5; g.kb = 12; g.Rb = 4; g.kh = 12; g.c = 4; g.W = 4;
+    }
+    g.kf = std::min(g.kf, n);
+    g.kb = std::min(g.kb, n);
+    g.kh = std::min(g.kh, n);
+    g.Rf = std::min(g.Rf, g.kf);
+    g.Rb = std::min(g.Rb, g.kb);
+    g.c = std::min(g.c, n);
+    return g;
+}
+
+static int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
+                                   const std::vector<std::vector<int>>& preds,
+                                   uint64_t fixed_bits, int budget) {
+    const int n = (int)need.size();
+    std::vector<int> indeg(n, 0);
+    std::vector<std::vector<int>> succ(n);
+    for (int j = 0; j < n; ++j) {
+        indeg[j] = (int)preds[j].size();
+        for (int p : preds[j]) succ[p].push_back(j);
+    }
+    std::set<int> ready;
+    for (int j = 0; j < n; ++j)
+        if (indeg[j] == 0) ready.insert(j);
+    std::vector<Group> out;
+    int remaining = n;
+    while (remaining > 0) {
+        Group g;
+        g.bits = fixed_bits;
+        for (;;) {
+            bool progress = true;
+            while (progress) {
+                progress = false;
+                for (int it : ready) {
+                    if ((need[it] & ~g.bits) == 0) {
+                        ready.erase(it);
+                        g.items.push_back(it);
+                        --remaining;
+                        for (int s : succ[it])
+                            if (--indeg[s] == 0) ready.insert(s);
+                        progress = true;
+                        break;
+                    }
+                }
+            }
+            int best = -1, best_cost = 1 << 30;
+            for (int it : ready) {
+                int extra = popc(need[it] & ~g.bits);
+                if (popc(g.bits) + extra <= budget && extra < best_cost) {
+                    best = it;
+                    best_cost = extra;
+                }
+            }
+            if (best < 0) break;
+            g.bits |= need[best];
+        }
+        if (g.items.empty()) return {};  // an item needs more bits than the budget
+        out.push_back(std::move(g));
+    }
+    return out;
+}
+
+static bool commute(const GateInfo& a, const GateInfo& b) {
+    for (int i = 0; i < a.nw; ++i)
+        for (int j = 0; j < b.nw; ++j)
+            if (a.wires[i] == b.wires[j]) {
+                char ta = a.wtype[i], tb = b.wtype[j];
+                if (ta != tb || ta == 'G') return false;
+            }
+    return true;
+}
+
+static bool is_diag_matrix(const double* m, int d) {  // exact-zero test, circuit.cpp:90-95
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c)
+            if (r != c && (m[2 * (r * 4 + c)] != 0.0 || m[2 * (r * 4 + c) + 1] != 0.0)) return false;
+    return true;
+}
+
+static bool is_unitary(const double* m, int d) {  // Circuit::unitary check, circuit.cpp:193-196
+    using cd = std::complex<double>;
+    double worst = 0.0;
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            cd acc = 0.0;
+            for (int k = 0; k < d; ++k)
+                acc += std::conj(cd(m[2 * (k * 4 + r)], m[2 * (k * 4 + r) + 1])) *
+                       cd(m[2 * (k * 4 + c)], m[2 * (k * 4 + c) + 1]);
+            worst = std::max(worst, std::abs(acc - cd(r == c ? 1.0 : 0.0, 0.0)));
+        }
+    return worst < 1e-10;
+}
+
+static std::string classify(int n, const GateSpec& s, const double* mats, int n_mats,
+                            int n_params, GateInfo& gi) {
+    gi.g = s;
+    auto inr = [n](int q) { return q >= 0 && q < n; };
+    const bool two = s.kind == QF_RZZ || s.kind == QF_CX || s.kind == QF_CZ ||
+                     s.kind == QF_SU4 || (s.kind == QF_UNITARY && s.q1 >= 0);
+    switch (s.kind) {
+        case QF_H: case QF_X: case QF_Y: case QF_Z: case QF_S:
+        case QF_RX: case QF_RY: case QF_RZ: case QF_RZZ:
+        case QF_CX: case QF_CZ: case QF_SU4: case QF_UNITARY:
+            break;
+        case QF_CSUM: case QF_SUBSPACE_RY: case QF_SUBSPACE_RZ:
+            return "gate_matrix: qudit gates are not supported on the qubit device path";
+        default:
+            return "gate_matrix: unknown gate kind";
+    }
+    if (!inr(s.q0)) return "Circuit: wire out of range";
+    if (two) {
+        if (!inr(s.q1)) return "Circuit: wire out of range";
+        if (s.q0 == s.q1) return "Circuit: duplicate wires";
+    }
+    gi.nw = two ? 2 : 1;
+    gi.wires[0] = s.q0;
+    gi.wires[1] = two ? s.q1 : -1;
+    if (s.slot >= n_params) return "program: parameter slot out of range";
+    if (s.slot < 0 && !std::isfinite(s.offset)) return "Circuit: non-finite parameter";
+    if (s.slot >= 0 && (!std::isfinite(s.coef) || !std::isfinite(s.offset)))
+        return "Circuit: non-finite parameter";
+    if (s.kind == QF_SU4 || s.kind == QF_UNITARY) {
+        if (s.slot >= 0)
+            return "program: parameterised su4/unitary gates are not supported on the device path";
+        if (s.mat < 0 || s.mat >= n_mats || !mats) return "program: missing gate matrix";
+        const double* m = mats + 32 * (size_t)s.mat;
+        if (!is_unitary(m, two ? 4 : 2)) return "unitary: matrix is not unitary";
+        gi.diag = is_diag_matrix(m, two ? 4 : 2);
+    }
+    auto pos = [n](int q) { return n - 1 - q; };
+    switch (s.kind) {
+        case QF_Z: case QF_S: case QF_RZ: case QF_RZZ: case QF_CZ:
+            gi.diag = true;
+            break;
+        default:
+            break;
+    }
+    if (gi.diag) {
+        gi.wtype[0] = gi.wtype[1] = 'D';
+        gi.need = 0;
+    } else if (s.kind == QF_X || s.kind == QF_RX) {
+        gi.wtype[0] = 'X';
+        gi.need = 1ull << pos(s.q0);
+    } else if (s.kind == QF_Y || s.kind == QF_RY) {
+        gi.wtype[0] = 'Y';
+        gi.need = 1ull << pos(s.q0);
+    } else if (s.kind == QF_CX) {
+        gi.wtype[0] = 'D';
+        gi.wtype[1] = 'X';
+        gi.need = 1ull << pos(s.q1);
+    } else {
+        gi.wtype[0] = gi.wtype[1] = 'G';
+        gi.need = 1ull << pos(s.q0);
+        if (two) gi.need |= 1ull << pos(s.q1);
+    }
+    if (s.slot >= 0) {
+        switch (s.kind) {
+            case QF_RX: gi.gen = 1; break;
+            case QF_RY: gi.gen = 2; break;
+            case QF_RZ: gi.gen = 3; break;
+            case QF_RZZ: gi.gen = 4; break;
+            default: gi.gen = 0; break;  // slot feeds a parameter-free gate: zero derivative
+        }
+    }
+    return "";
+}
+
+static int mat_size(uint8_t kind) {
+    switch (kind) {
+        case DK_G1: case DK_R1: case DK_RX: return 4;
+        case DK_D1: return 2;
+        case DK_D2: return 4;
+        case DK_G2: return 16;
+        default: return 0;
+    }
+}
+
+// Lower one pass (forward or adjoint) of an ordered gate list.
+static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
+                       const std::vector<std::vector<int>>& preds_in_order, int k, int R,
+                       int c, int W, bool adjoint, PassPlan& out) {
+    const int n = P.n;
+    out.k = k;
+    out.R = R;
+    std::vector<uint64_t> need(order.size());
+    for (size_t i = 0; i < order.size(); ++i) need[i] = P.gates[order[i]].need;
+    const uint64_t all = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+    const uint64_t fixed = (n <= k) ? all : ((1ull << c) - 1);
+    auto sweeps = schedule_groups(need, preds_in_order, fixed, k);
+
+    for (auto& sw : sweeps) {
+        // pad the tile to exactly k bits with the lowest free positions
+        uint64_t bits = sw.bits;
+        for (int p = 0; p < n && popc(bits) < k; ++p) bits |= 1ull << p;
+        DevSweep ds{};
+        ds.k = k;
+        ds.R = R;
+        int tl_of_pos[64];
+        for (int p = 0; p < 64; ++p) tl_of_pos[p] = -1;
+        int t = 0;
+        for (int p = 0; p < n; ++p)
+            if (bits >> p & 1) {
+                ds.tb[t] = (int8_t)p;
+                tl_of_pos[p] = t++;
+            }
+        ds.out_mask = (uint32_t)(all & ~bits);
+        ds.phase_begin = (int)out.phases.size();
+        ds.op_begin = (int)out.ops.size();
+        ds.tap_begin = out.n_taps;
+
+        // phases: schedule the sweep's gates over tile-local bits with budget R
+        std::map<int, int> local;  // index in `order` -> index in sweep
+        for (size_t i = 0; i < sw.items.size(); ++i) local[sw.items[i]] = (int)i;
+        std::vector<uint64_t> lneed(sw.items.size());
+        std::vector<std::vector<int>> lpreds(sw.items.size());
+        for (size_t i = 0; i < sw.items.size(); ++i) {
+            int it = sw.items[i];
+            uint64_t m = 0;
+            for (int p = 0; p < n; ++p)
+                if (need[it] >> p & 1) m |= 1ull << tl_of_pos[p];
+            lneed[i] = m;
+            for (int pr : preds_in_order[it]) {
+                auto f = local.find(pr);
+                if (f != local.end()) lpreds[i].push_back(f->second);
+            }
+        }
+        auto phases = schedule_groups(lneed, lpreds, 0, R);
+        int moff = 0, ntap = 0;
+        for (auto& ph : phases) {
+            DevPhase dp{};
+            for (int i = 0; i < kMaxReg; ++i) dp.reg_tl[i] = -1;
+            for (int i = 0; i < kMaxThreadBits; ++i) dp.thr_tl[i] = -1;
+            // register bits: the needed ones, padded with the highest free tile bits
+            uint64_t rbits = ph.bits;
+            for (int b = k - 1; b >= 0 && popc(rbits) < R; --b) rbits |= 1ull << b;
+            int r = 0;
+            int rb_of_tl[kMaxTileBits];
+            for (int b = 0; b < kMaxTileBits; ++b) rb_of_tl[b] = -1;
+            for (int b = 0; b < k; ++b)
+                if (rbits >> b & 1) {
+                    dp.reg_tl[r] = (int8_t)b;
+                    rb_of_tl[b] = r++;
+                }
+            // thread bits: lanes first, covering distinct residues mod W (bank spread)
+            std::vector<int> free_bits;
+            for (int b = 0; b < k; ++b)
+                if (!(rbits >> b & 1)) free_bits.push_back(b);
+            std::vector<int> lanes, rest;
+            std::vector<bool> used(free_bits.size(), false);
+            const int nl = std::min<int>(5, (int)free_bits.size());
+            for (int pass = 0; pass < 2 && (int)lanes.size() < nl; ++pass) {
+                uint32_t seen = 0;
+                for (int l : lanes) seen |= 1u << (l % W);
+                for (size_t i = 0; i < free_bits.size() && (int)lanes.size() < nl; ++i) {
+                    if (used[i]) continue;
+                    int res = free_bits[i] % W;
+                    if (pass == 0 && (seen >> res & 1)) continue;
+                    used[i] = true;
+                    seen |= 1u << res;
+                    lanes.push_back(free_bits[i]);
+                }
+            }
+            for (size_t i = 0; i < free_bits.size(); ++i)
+                if (!used[i]) rest.push_back(free_bits[i]);
+            std::sort(lanes.begin(), lanes.end());
+            int ti = 0;
+            for (int l : lanes) dp.thr_tl[ti++] = (int8_t)l;
+            for (int l : rest) dp.thr_tl[ti++] = (int8_t)l;
+
+            dp.op_begin = (int)out.ops.size();
+            auto rb_of_pos = [&](int p) { return rb_of_tl[tl_of_pos[p]]; };
+            for (int li : ph.items) {
+                const int gidx = order[sw.items[li]];
+                const GateInfo& gi = P.gates[gidx];
+                const GateSpec& s = gi.g;
+                const int p0 = n - 1 - s.q0;
+                const int p1 = gi.nw == 2 ? n - 1 - s.q1 : -1;
+                if (adjoint && gi.gen) {
+                    DevOp tp{};
+                    tp.gate = gidx;
+                    tp.moff = -1;
+                    tp.tap = ntap++;
+                    tp.pos0 = (int8_t)p0;
+                    tp.pos1 = (int8_t)p1;
+                    tp.rb0 = (int8_t)(tl_of_pos[p0] >= 0 ? rb_of_pos(p0) : -1);
+                    tp.rb1 = (int8_t)(p1 >= 0 && tl_of_pos[p1] >= 0 ? rb_of_pos(p1) : -1);
+                    tp.kind = gi.gen == 1 ? DK_TX : gi.gen == 2 ? DK_TY : gi.gen == 3 ? DK_TZ : DK_TZZ;
+                    out.ops.push_back(tp);
+                    out.taps.push_back(DevTap{s.slot, 0, s.coef});
+                }
+                DevOp op{};
+                op.gate = gidx;
+                op.tap = -1;
+                op.pos0 = (int8_t)p0;
+                op.pos1 = (int8_t)p1;
+                op.rb0 = (int8_t)(tl_of_pos[p0] >= 0 ? rb_of_pos(p0) : -1);
+                op.rb1 = (int8_t)(p1 >= 0 && tl_of_pos[p1] >= 0 ? rb_of_pos(p1) : -1);
+                if (gi.diag) {
+                    op.kind = gi.nw == 2 ? DK_D2 : DK_D1;
+                } else {
+                    switch (s.kind) {
+                        case QF_H: case QF_RY: op.kind = DK_R1; break;
+                        case QF_RX: op.kind = DK_RX; break;
+                        case QF_X: op.kind = DK_X1; break;
+                        case QF_CX:
+                            op.kind = DK_CX;
+                            // target (wire 1) is the register bit, control is pos0
+                            op.rb0 = (int8_t)rb_of_pos(p1);
+                            op.rb1 = (int8_t)(tl_of_pos[p0] >= 0 ? rb_of_pos(p0) : -1);
+                            break;
+                        default: op.kind = gi.nw == 2 ? DK_G2 : DK_G1; break;
+                    }
+                }
+                int ms = mat_size(op.kind);
+                op.moff = (int16_t)(ms ? moff : -1);
+                moff += ms;
+                out.ops.push_back(op);
+            }
+            dp.op_end = (int)out.ops.size();
+            out.phases.push_back(dp);
+        }
+        ds.n_phases = (int)phases.size();
+        ds.op_end = (int)out.ops.size();
+        ds.n_mat = moff;
+        ds.n_taps = ntap;
+        out.n_taps += ntap;
+        out.max_mat = std::max(out.max_mat, moff);
+        out.max_ops = std::max(out.max_ops, ds.op_end - ds.op_begin);
+        out.max_taps = std::max(out.max_taps, ntap);
+        out.sweeps.push_back(ds);
+    }
+}
+
+std::string build_program_plan(int n, const std::vector<GateSpec>& ops, const double* mats,
+                               int n_mats, int n_params, int prec, ProgramPlan& P) {
+    if (n < 1 || n > 32) return "program: qubit count must be in [1, 32] on the device path";
+    if (n_params < 0) return "AnsatzSpec: negative parameter count";
+    if (prec != QF_C64 && prec != QF_C128) return "program: precision must be QF_C64 or QF_C128";
+    P = ProgramPlan{};
+    P.n = n;
+    P.prec = prec;
+    P.n_params = n_params;
+    if (mats && n_mats > 0) P.mats.assign(mats, mats + 32 * (size_t)n_mats);
+    P.gates.resize(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) {
+        std::string e = classify(n, ops[i], mats, n_mats, n_params, P.gates[i]);
+        if (!e.empty()) return e;
+        if (ops[i].slot >= 0 && !P.gates[i].gen &&
+            (ops[i].kind == QF_SU4 || ops[i].kind == QF_UNITARY)) {
+            P.adjoint_ok = false;
+            P.adjoint_error = "gradient: parameter feeds a gate without a Pauli generator";
+        }
+    }
+    // commutation DAG (program order among non-commuting gates sharing a wire)
+    const int G = (int)ops.size();
+    std::vector<std::vector<int>> on_wire(n);
+    std::vector<std::vector<int>> preds(G), succs(G);
+    for (int j = 0; j < G; ++j) {
+        std::set<int> ps;
+        for (int w = 0; w < P.gates[j].nw; ++w)
+            for (int i : on_wire[P.gates[j].wires[w]])
+                if (!commute(P.gates[i], P.gates[j])) ps.insert(i);
+        preds[j].assign(ps.begin(), ps.end());
+        for (int i : preds[j]) succs[i].push_back(j);
+        for (int w = 0; w < P.gates[j].nw; ++w) on_wire[P.gates[j].wires[w]].push_back(j);
+    }
+    Geometry geo = geometry(prec, n);
+    std::vector<int> order(G);
+    for (int i = 0; i < G; ++i) order[i] = i;
+    lower_pass(P, order, preds, geo.kf, geo.Rf, geo.c, geo.W, false, P.fwd);
+    // adjoint: reversed order, reversed DAG
+    std::vector<int> rorder(G);
+    std::vector<std::vector<int>> rpreds(G);
+    for (int i = 0; i < G; ++i) rorder[i] = G - 1 - i;
+    for (int i = 0; i < G; ++i) {
+        int g = G - 1 - i;
+        for (int s : succs[g]) rpreds[i].push_back(G - 1 - s);
+    }
+    lower_pass(P, rorder, rpreds, geo.kb, geo.Rb, geo.c, geo.W, true, P.bwd);
+    if (G > 0 && (P.fwd.sweeps.empty() || P.bwd.sweeps.empty()))
+        return "program: scheduling failed";
+    return "";
+}
+
+std::string build_observable_plan(int n, int n_terms, const int8_t* codes, const double* w_re,
+                                  const double* w_im, int kh, ObservablePlan& O) {
+    if (n < 1 || n > 32) return "observable: qubit count must be in [1, 32] on the device path";
+    if (n_terms < 0) return "observable: negative term count";
+    O = ObservablePlan{};
+    O.n = n;
+    O.kh = kh;
+    const uint32_t lo = (kh >= 32) ? 0xffffffffu : ((1u << kh) - 1);
+    std::map<uint32_t, std::vector<DevTerm>> groups;
+    groups[0];  // own tile always first (energy needs it)
+    for (int t = 0; t < n_terms; ++t) {
+        uint32_t flip = 0, z = 0;
+        int y = 0;
+        for (int i = 0; i < n; ++i) {  // compile_term, pauli.cpp:61-74
+            int c = codes[(size_t)t * n + i];
+            if (c < 0 || c > 3) return "PauliSum::add: code out of range";
+            uint32_t bit = 1u << (n - 1 - i);
+            if (c == 1) flip |= bit;
+            if (c == 2) { flip |= bit; z |= bit; ++y; }
+            if (c == 3) z |= bit;
+        }
+        if (!std::isfinite(w_re[t]) || !std::isfinite(w_im ? w_im[t] : 0.0))
+            return "PauliSum::add: non-finite weight";
+        static const double ip[4][2] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+        DevTerm d{};
+        const double wr = w_re[t], wi = w_im ? w_im[t] : 0.0;
+        d.c_re = wr * ip[y & 3][0];
+        d.c_im = wr * ip[y & 3][1];
+        d.ci_re = wi * ip[y & 3][0];
+        d.ci_im = wi * ip[y & 3][1];
+        if (wi != 0.0) O.has_imag = true;
+        d.f_in = flip & lo;
+        d.z = z;
+        d.fz_par = (uint32_t)(__builtin_popcount(flip & z) & 1);
+        d.kind = flip == 0 ? TK_DIAG : (z == 0 ? TK_FLIP : TK_GEN);
+        groups[flip & ~lo].push_back(d);
+    }
+    for (auto& [fo, ts] : groups) {
+        DevGroup g{};
+        g.f_out = fo;
+        g.term_begin = (int)O.terms.size();
+        // diagonal terms first, then pure flips, then general (kernel loops per kind)
+        for (int kind = 0; kind < 3; ++kind)
+            for (auto& d : ts)
+                if (d.kind == kind) O.terms.push_back(d);
+        g.term_end = (int)O.terms.size();
+        O.groups.push_back(g);
+    }
+    return "";
+}
+
+}  // namespace qfb

@@ -1,0 +1,17 @@
+// sweep_f32_fwd.cu -- explicit instantiation of the fused sweep (float, forward).
+#include "sweep_impl.cuh"
+
+namespace qfb {
+
+cudaError_t launch_sweep_f32_fwd(const SweepArgs& a, int batch, size_t smem, cudaStream_t s) {
+    switch (a.sw.R) {
+        case 1: return launch_sweep_t<float, 1, false>(a, batch, smem, s);
+        case 2: return launch_sweep_t<float, 2, false>(a, batch, smem, s);
+        case 3: return launch_sweep_t<float, 3, false>(a, batch, smem, s);
+        case 4: return launch_sweep_t<float, 4, false>(a, batch, smem, s);
+        case 5: return launch_sweep_t<float, 5, false>(a, batch, smem, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace qfb

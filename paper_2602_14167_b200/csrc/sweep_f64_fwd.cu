@@ -1,0 +1,16 @@
+// sweep_f64_fwd.cu -- explicit instantiation of the fused sweep (double, forward).
+#include "sweep_impl.cuh"
+
+namespace qfb {
+
+cudaError_t launch_sweep_f64_fwd(const SweepArgs& a, int batch, size_t smem, cudaStream_t s) {
+    switch (a.sw.R) {
+        case 1: return launch_sweep_t<double, 1, false>(a, batch, smem, s);
+        case 2: return launch_sweep_t<double, 2, false>(a, batch, smem, s);
+        case 3: return launch_sweep_t<double, 3, false>(a, batch, smem, s);
+        case 4: return launch_sweep_t<double, 4, false>(a, batch, smem, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace qfb

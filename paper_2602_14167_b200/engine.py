@@ -1,0 +1,216 @@
+"""Thin Python handles over the C-ABI objects (qf_ctx, qf_program, qf_observable).
+
+The numerics live in libqforge_b200.so (sm_100a kernels + C++ scheduler); this
+module only moves host buffers in and out.  Nothing here computes amplitudes.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import QfOp, check, dptr
+
+PRECISIONS = {"c64": _lib.QF_C64, "c128": _lib.QF_C128, _lib.QF_C64: _lib.QF_C64,
+              _lib.QF_C128: _lib.QF_C128}
+
+
+class Context:
+    """One GPU (qf_ctx): stream, scratch buffers, optional NCCL communicator."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        self.device = device
+        h = ctypes.c_void_p()
+        check(self.lib.qf_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.rank, self.world = 0, 1
+
+    @property
+    def stream(self) -> int:
+        return self.lib.qf_ctx_stream(self.handle) or 0
+
+    def set_memory_budget(self, nbytes: int) -> None:
+        check(self.lib.qf_ctx_set_memory_budget(self.handle, int(nbytes)))
+
+    def set_timing(self, on: bool) -> None:
+        check(self.lib.qf_ctx_set_timing(self.handle, 1 if on else 0))
+
+    def last_stats(self):
+        launches = ctypes.c_longlong()
+        ms = (ctypes.c_double * 4)()
+        by = (ctypes.c_double * 4)()
+        check(self.lib.qf_ctx_last_stats(self.handle, ctypes.byref(launches), ms, by))
+        return int(launches.value), list(ms), list(by)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = _lib.load()
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib.qf_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def set_comm(self, rank: int, world: int, uid: Optional[bytes]) -> None:
+        buf = (ctypes.c_uint8 * 128)(*(uid or bytes(128)))
+        check(self.lib.qf_ctx_set_comm(self.handle, rank, world, buf))
+        self.rank, self.world = rank, world
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.qf_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: Optional[int] = None) -> Context:
+    if device is None:
+        try:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        except Exception:
+            device = 0
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+class Program:
+    """A compiled circuit template (qf_program).
+
+    ops: sequence of (kind, q0, q1, slot, coef, offset, mat) with kind a gate
+    name or qforge::Gate number; mats: [M, 4, 4] complex constant matrices.
+    """
+
+    def __init__(self, ctx: Context, n: int, ops: Sequence, n_params: int, precision="c128",
+                 mats: Optional[np.ndarray] = None):
+        self.ctx, self.n, self.n_params = ctx, n, n_params
+        self.precision = PRECISIONS[precision]
+        arr = (QfOp * max(1, len(ops)))()
+        for i, op in enumerate(ops):
+            kind, q0, q1, slot, coef, offset, mat = op
+            if isinstance(kind, str):
+                kind = _lib.GATE_ID[kind]
+            arr[i] = QfOp(int(kind), int(q0), int(q1), int(slot), float(coef), float(offset), int(mat), 0)
+        if mats is not None and len(mats):
+            m = np.ascontiguousarray(np.asarray(mats, dtype=np.complex128).reshape(-1, 4, 4))
+            mv = m.view(np.float64).reshape(-1)
+            nm = m.shape[0]
+        else:
+            mv, nm = None, 0
+        self._mats_keepalive = mv
+        h = ctypes.c_void_p()
+        check(ctx.lib.qf_program_create(ctx.handle, n, len(ops), arr, dptr(mv), nm, n_params,
+                                        self.precision, ctypes.byref(h)))
+        self.handle = h
+
+    def set_initial_state(self, amps: np.ndarray) -> None:
+        a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128).reshape(-1))
+        if a.size != (1 << self.n):
+            raise ValueError("run: initial state size mismatch")
+        check(self.ctx.lib.qf_program_set_initial_state(self.handle, dptr(a.view(np.float64))))
+
+    def info(self) -> dict:
+        v = [ctypes.c_int() for _ in range(4)]
+        check(self.ctx.lib.qf_program_info(self.handle, *[ctypes.byref(x) for x in v]))
+        return {"fwd_sweeps": v[0].value, "bwd_sweeps": v[1].value, "fwd_tile_bits": v[2].value,
+                "bwd_tile_bits": v[3].value}
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.qf_program_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Observable:
+    """A Pauli sum on the device (qf_observable). codes [T, n] int8, weights complex [T]."""
+
+    def __init__(self, ctx: Context, n: int, codes: np.ndarray, weights: np.ndarray):
+        self.ctx, self.n = ctx, n
+        codes = np.ascontiguousarray(np.asarray(codes, dtype=np.int8).reshape(-1, n) if n else codes)
+        w = np.asarray(weights, dtype=np.complex128).reshape(-1)
+        self.n_terms = int(w.size)
+        wr = np.ascontiguousarray(w.real)
+        wi = np.ascontiguousarray(w.imag)
+        h = ctypes.c_void_p()
+        check(ctx.lib.qf_observable_create(ctx.handle, n, self.n_terms,
+                                           codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
+                                           dptr(wr), dptr(wi), ctypes.byref(h)))
+        self.handle = h
+
+    def set_sharding(self, mode: int) -> None:
+        check(self.ctx.lib.qf_observable_set_sharding(self.handle, int(mode)))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.qf_observable_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def energy_grad_batch(ctx: Context, prog: Program, obs: Observable, thetas: np.ndarray,
+                      grads: bool = True):
+    """Host-buffer evaluation (qf_energy_grad_batch): returns (E[B], G[B, P] or None)."""
+    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(-1, prog.n_params)
+                              if prog.n_params else np.zeros((len(thetas), 0)))
+    B = th.shape[0]
+    E = np.empty(B, dtype=np.float64)
+    G = np.empty((B, prog.n_params), dtype=np.float64) if grads else None
+    check(ctx.lib.qf_energy_grad_batch(ctx.handle, prog.handle, obs.handle, B, dptr(th), dptr(E),
+                                       dptr(G) if grads else None))
+    return E, G
+
+
+def energy_grad_batch_device(ctx: Context, prog: Program, obs: Observable, d_thetas, d_energies,
+                             d_grads=None) -> None:
+    """Device-buffer evaluation (torch CUDA float64 tensors), ordered on ctx.stream."""
+    B = int(d_energies.shape[0])
+    check(ctx.lib.qf_energy_grad_batch_device(
+        ctx.handle, prog.handle, obs.handle, B, ctypes.c_void_p(d_thetas.data_ptr()),
+        ctypes.c_void_p(d_energies.data_ptr()),
+        ctypes.c_void_p(d_grads.data_ptr()) if d_grads is not None else None))
+
+
+def run_state(ctx: Context, prog: Program, theta: np.ndarray, guard_log2: int = 24) -> np.ndarray:
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64).reshape(-1))
+    out = np.empty(1 << prog.n, dtype=np.complex128)
+    check(ctx.lib.qf_run_state(ctx.handle, prog.handle, dptr(th) if th.size else None, int(guard_log2),
+                               dptr(out.view(np.float64))))
+    return out
+
+
+def expectation(ctx: Context, prog: Program, obs: Observable, theta: np.ndarray) -> complex:
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64).reshape(-1))
+    out = np.empty(2, dtype=np.float64)
+    check(ctx.lib.qf_expectation(ctx.handle, prog.handle, obs.handle, dptr(th) if th.size else None,
+                                 dptr(out)))
+    return complex(out[0], out[1])
+
+
+def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
+                     eps=1e-8) -> None:
+    B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))
+    check(ctx.lib.qf_adam_step_device(ctx.handle, B, P, ctypes.c_void_p(theta.data_ptr()),
+                                      ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(v.data_ptr()),
+                                      ctypes.c_void_p(g.data_ptr()), int(t), float(lr), float(beta1),
+                                      float(beta2), float(eps)))
