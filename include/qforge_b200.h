@@ -159,12 +159,15 @@ int qf_adam_step_device(qf_ctx* ctx, int batch, int n_params, double* d_theta,
                         double beta1, double beta2, double eps);
 
 /* ---- instrumentation (bench.py) ---- */
-/* Number of kernel launches made by the last evaluation call, and per-class
- * device time (ms) when timing is enabled (CUDA events on the context stream):
- * class 0 = forward sweeps, 1 = H|psi> / energy, 2 = adjoint sweeps, 3 = other. */
+/* Counters accumulated since the last qf_ctx_reset_stats: kernel launches (total
+ * and per class), algorithmic HBM bytes per class and, when timing is enabled,
+ * device time per class from CUDA events recorded on the context stream
+ * (resolved lazily, no syncs inside evaluation calls).  Classes: 0 = forward
+ * sweeps, 1 = H|psi> / energy, 2 = adjoint sweeps, 3 = reductions. */
 int qf_ctx_set_timing(qf_ctx* ctx, int enabled);
-int qf_ctx_last_stats(qf_ctx* ctx, long long* launches, double* ms_by_class /* [4] */,
-                      double* bytes_by_class /* [4] algorithmic HBM bytes */);
+int qf_ctx_reset_stats(qf_ctx* ctx);
+int qf_ctx_stats(qf_ctx* ctx, long long* launches, long long* launches_by_class /* [4] */,
+                 double* ms_by_class /* [4] */, double* bytes_by_class /* [4] */);
 
 #ifdef __cplusplus
 }

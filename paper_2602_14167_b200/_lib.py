@@ -55,7 +55,8 @@ SIGNATURES = {
     "qf_adam_step_device": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double]),
     "qf_ctx_set_timing": (_I, [_P, _I]),
-    "qf_ctx_last_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), _D, _D]),
+    "qf_ctx_reset_stats": (_I, [_P]),
+    "qf_ctx_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _D, _D]),
 }
 
 _lib = None

@@ -168,12 +168,16 @@ struct qf_ctx {
     // NCCL
     NcclComm comm = nullptr;
     int rank = 0, world = 1;
-    // stats
+    // stats (accumulated until qf_ctx_reset_stats); timing uses event pairs
+    // recorded on the context stream and resolved lazily (no mid-call syncs)
     bool timing = false;
     long long launches = 0;
+    long long class_launches[4] = {0, 0, 0, 0};
     double ms[4] = {0, 0, 0, 0};
     double bytes[4] = {0, 0, 0, 0};
-    cudaEvent_t ev[8] = {};
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<size_t, int>> pending;  // (start event index, class); end = start + 1
 };
 
 namespace {
@@ -193,6 +197,33 @@ int ensure_obs_dev(qf_observable* o, int prec, int kh, ObsDev& d, int t_begin, i
 
 size_t vsize(int prec) { return prec == QF_C128 ? 16 : 8; }
 
+void resolve_events(qf_ctx* ctx) {
+    if (ctx->pending.empty()) {
+        ctx->ev_used = 0;
+        return;
+    }
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& pr : ctx->pending) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev_pool[pr.first], ctx->ev_pool[pr.first + 1]);
+        ctx->ms[pr.second] += ms;
+    }
+    ctx->pending.clear();
+    ctx->ev_used = 0;
+}
+
+// records an event on s; start/end pairs are consecutive in the pool
+size_t record_event(qf_ctx* ctx, cudaStream_t s) {
+    if (ctx->ev_used >= 4096 && ctx->ev_used % 2 == 0) resolve_events(ctx);
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->ev_pool.push_back(e);
+    }
+    cudaEventRecord(ctx->ev_pool[ctx->ev_used], s);
+    return ctx->ev_used++;
+}
+
 // one chunk: [b0, b0 + bc) of d_thetas rows
 int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const double* d_thetas,
                double* d_E, double* d_Eim, double* d_G, ObsDev* od_im) {
@@ -203,16 +234,14 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     cudaStream_t s = ctx->stream;
     const bool grads = d_G != nullptr;
     const int P_ = P.n_params;
+    size_t ev_start[4] = {0, 0, 0, 0};
     auto tick = [&](int i) {
-        if (ctx->timing) cudaEventRecord(ctx->ev[i], s);
+        if (ctx->timing) ev_start[i / 2] = record_event(ctx, s);
     };
     auto tock = [&](int i, int cls) {
         if (ctx->timing) {
-            cudaEventRecord(ctx->ev[i + 1], s);
-            cudaEventSynchronize(ctx->ev[i + 1]);
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]);
-            ctx->ms[cls] += ms;
+            record_event(ctx, s);
+            ctx->pending.push_back({ev_start[i / 2], cls});
         }
     };
 
@@ -242,6 +271,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         sa.from_zero = (i == 0 && first_from_zero) ? 1 : 0;
         QF_CUDA(launch_sweep(prec, false, sa, bc, P.fwd.max_mat, 0, s));
         ctx->launches++;
+        ctx->class_launches[0]++;
         ctx->bytes[0] += (double)bc * N * vs * (sa.from_zero ? 1 : 2);
     }
     if (!prog->has_init && P.fwd.sweeps.empty()) ctx->bytes[0] += (double)bc * N * vs;
@@ -264,6 +294,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.epart = (double*)ctx->epart.p;
     QF_CUDA(launch_hpsi(prec, ha, bc, s));
     ctx->launches++;
+    ctx->class_launches[1]++;
     ctx->bytes[1] += (double)bc * N * vs * (ha.n_groups + (grads ? 1 : 0));
     ReduceArgs ra{};
     ra.part = (const double*)ctx->epart.p;
@@ -300,6 +331,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
             sa.sw = P.bwd.sweeps[i];
             QF_CUDA(launch_sweep(prec, true, sa, bc, P.bwd.max_mat, P.bwd.max_taps, s));
             ctx->launches++;
+            ctx->class_launches[2]++;
             ctx->bytes[2] += (double)bc * N * vs * 4;
         }
         tock(4, 2);
@@ -431,7 +463,6 @@ int qf_ctx_create(int device, qf_ctx** out) {
     qf_ctx* c = new qf_ctx();
     c->device = device;
     QF_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    for (auto& ev : c->ev) QF_CUDA(cudaEventCreate(&ev));
     *out = c;
     return QF_OK;
 }
@@ -444,7 +475,7 @@ int qf_ctx_destroy(qf_ctx* c) {
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init})
         b->release();
     c->pin.release();
-    for (auto& ev : c->ev) cudaEventDestroy(ev);
+    for (auto& ev : c->ev_pool) cudaEventDestroy(ev);
     cudaStreamDestroy(c->stream);
     delete c;
     return QF_OK;
@@ -637,8 +668,12 @@ static int stage_thetas(qf_ctx* ctx, const qf_program* prog, int batch, const do
 }
 
 static void reset_stats(qf_ctx* ctx) {
+    resolve_events(ctx);
     ctx->launches = 0;
-    for (int i = 0; i < 4; ++i) ctx->ms[i] = ctx->bytes[i] = 0;
+    for (int i = 0; i < 4; ++i) {
+        ctx->ms[i] = ctx->bytes[i] = 0;
+        ctx->class_launches[i] = 0;
+    }
 }
 
 int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
@@ -652,7 +687,6 @@ int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observab
     int rc = check_thetas(prog, batch, thetas);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
-    reset_stats(ctx);
     const int P = prog->plan.n_params;
     rc = stage_thetas(ctx, prog, batch, thetas);
     if (rc) return rc;
@@ -698,7 +732,6 @@ int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* cprog, const qf_o
         return set_err(QF_EINVAL, "qf_energy_grad_batch_device: bad arguments");
     if (batch == 0) return QF_OK;
     cudaSetDevice(ctx->device);
-    reset_stats(ctx);
     return eval_device(ctx, prog, obs, batch, d_thetas, d_energies, nullptr, d_grads, false);
 }
 
@@ -712,7 +745,6 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
     int rc = check_thetas(prog, 1, theta);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
-    reset_stats(ctx);
     rc = stage_thetas(ctx, prog, 1, theta);
     if (rc) return rc;
     // forward only: use a trivial observable-free path
@@ -769,7 +801,6 @@ int qf_expectation(qf_ctx* ctx, const qf_program* cprog, const qf_observable* co
     int rc = check_thetas(prog, 1, theta);
     if (rc) return rc;
     cudaSetDevice(ctx->device);
-    reset_stats(ctx);
     rc = stage_thetas(ctx, prog, 1, theta);
     if (rc) return rc;
     QF_CUDA(ctx->out.reserve(32));
@@ -797,9 +828,18 @@ int qf_ctx_set_timing(qf_ctx* ctx, int enabled) {
     return QF_OK;
 }
 
-int qf_ctx_last_stats(qf_ctx* ctx, long long* launches, double* ms, double* bytes) {
+int qf_ctx_reset_stats(qf_ctx* ctx) {
     if (!ctx) return set_err(QF_EINVAL, "null context");
+    reset_stats(ctx);
+    return QF_OK;
+}
+
+int qf_ctx_stats(qf_ctx* ctx, long long* launches, long long* class_launches, double* ms, double* bytes) {
+    if (!ctx) return set_err(QF_EINVAL, "null context");
+    resolve_events(ctx);
     if (launches) *launches = ctx->launches;
+    for (int i = 0; i < 4; ++i)
+        if (class_launches) class_launches[i] = ctx->class_launches[i];
     for (int i = 0; i < 4; ++i) {
         if (ms) ms[i] = ctx->ms[i];
         if (bytes) bytes[i] = ctx->bytes[i];

@@ -38,12 +38,18 @@ class Context:
     def set_timing(self, on: bool) -> None:
         check(self.lib.qf_ctx_set_timing(self.handle, 1 if on else 0))
 
-    def last_stats(self):
+    def reset_stats(self) -> None:
+        check(self.lib.qf_ctx_reset_stats(self.handle))
+
+    def stats(self):
+        """(launches, launches per class, ms per class, algorithmic bytes per class);
+        classes: forward sweeps, H|psi>, adjoint sweeps, reductions."""
         launches = ctypes.c_longlong()
+        cl = (ctypes.c_longlong * 4)()
         ms = (ctypes.c_double * 4)()
         by = (ctypes.c_double * 4)()
-        check(self.lib.qf_ctx_last_stats(self.handle, ctypes.byref(launches), ms, by))
-        return int(launches.value), list(ms), list(by)
+        check(self.lib.qf_ctx_stats(self.handle, ctypes.byref(launches), cl, ms, by))
+        return int(launches.value), list(cl), list(ms), list(by)
 
     @staticmethod
     def nccl_unique_id() -> bytes:
