@@ -372,7 +372,7 @@ def main():
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * P * 8,
                         "d2h_bytes_per_step": B * (1 + P) * 8},
                 "gpu_launches": launches, "clocks": clocks,
-                "program": prog.info(), "e2e_vs_device_max_abs_dE": agree}
+                "program": dict(prog.info(), jit=prog.jit_status()), "e2e_vs_device_max_abs_dE": agree}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

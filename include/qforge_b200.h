@@ -118,6 +118,13 @@ int qf_program_destroy(qf_program* prog);
 int qf_program_info(const qf_program* prog, int* fwd_sweeps, int* bwd_sweeps,
                     int* fwd_tile_bits, int* bwd_tile_bits);
 
+/* Specialised-kernel status: by default every program's sweeps are compiled
+ * into straight-line sm_100a kernels (NVRTC, cached on disk under
+ * $QF_JIT_CACHE or ~/.cache/qforge_b200); QF_JIT=0 selects the generic AOT
+ * kernels, QF_JIT=2 makes a failed specialisation an error. */
+int qf_program_jit_status(const qf_program* prog, int* active, int* compiled, int* cached,
+                          double* seconds, const char** error);
+
 /* ---- observables (Pauli sums) ---- */
 /* codes: [n_terms][n_qubits], 0=I 1=X 2=Y 3=Z (pauli.hpp:11-17). */
 int qf_observable_create(qf_ctx* ctx, int n_qubits, int n_terms, const int8_t* codes,

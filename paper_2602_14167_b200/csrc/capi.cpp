@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,7 @@
 
 #include "../../include/qforge_b200.h"
 #include "kernels.cuh"
+#include "jit.hpp"
 #include "plan.hpp"
 
 using namespace qfb;
@@ -140,6 +142,10 @@ struct qf_program {
     DevBuf slot_ptr, slot_taps, slot_coef;
     DevBuf init;  // optional initial state (RT)
     bool has_init = false;
+    // NVRTC-specialised sweep kernels (jit.hpp); the AOT interpreter is the fallback
+    bool use_jit = false;
+    JitPass jf, jb;
+    JitStats jst;
 };
 
 struct ObsDev {
@@ -269,7 +275,10 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
         sa.sw = P.fwd.sweeps[i];
         sa.from_zero = (i == 0 && first_from_zero) ? 1 : 0;
-        QF_CUDA(launch_sweep(prec, false, sa, bc, P.fwd.max_mat, 0, s));
+        if (prog->use_jit)
+            QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), bc, s));
+        else
+            QF_CUDA(launch_sweep(prec, false, sa, bc, P.fwd.max_mat, 0, s));
         ctx->launches++;
         ctx->class_launches[0]++;
         ctx->bytes[0] += (double)bc * N * vs * (sa.from_zero ? 1 : 2);
@@ -329,7 +338,10 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         sa.n_taps_total = nt;
         for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) {
             sa.sw = P.bwd.sweeps[i];
-            QF_CUDA(launch_sweep(prec, true, sa, bc, P.bwd.max_mat, P.bwd.max_taps, s));
+            if (prog->use_jit)
+                QF_CUDA((cudaError_t)jit_launch(prog->jb.sweeps[i], sa, 1 << (n - sa.sw.k), bc, s));
+            else
+                QF_CUDA(launch_sweep(prec, true, sa, bc, P.bwd.max_mat, P.bwd.max_taps, s));
             ctx->launches++;
             ctx->class_launches[2]++;
             ctx->bytes[2] += (double)bc * N * vs * 4;
@@ -571,7 +583,27 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
     if ((ce = upload(p->slot_taps, taps, s)) != cudaSuccess) return fail(ce);
     if ((ce = upload(p->slot_coef, coef, s)) != cudaSuccess) return fail(ce);
     if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return fail(ce);
+    const char* jit_env = std::getenv("QF_JIT");
+    if (!(jit_env && jit_env[0] == '0') && !p->plan.gates.empty()) {
+        p->use_jit = jit_build(p->plan, p->jf, p->jb, p->jst);
+        if (!p->use_jit && jit_env && jit_env[0] == '2') {  // QF_JIT=2: specialised kernels required
+            std::string why = p->jst.error;
+            delete p;
+            return set_err(QF_ERUNTIME, "JIT required but unavailable: " + why);
+        }
+    }
     *out = p;
+    return QF_OK;
+}
+
+int qf_program_jit_status(const qf_program* p, int* active, int* compiled, int* cached, double* seconds,
+                          const char** error) {
+    if (!p) return set_err(QF_EINVAL, "null program");
+    if (active) *active = p->use_jit ? 1 : 0;
+    if (compiled) *compiled = p->jst.compiled;
+    if (cached) *cached = p->jst.cached;
+    if (seconds) *seconds = p->jst.seconds;
+    if (error) *error = p->jst.error.c_str();
     return QF_OK;
 }
 
@@ -777,7 +809,10 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
     for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
         sa.sw = P.fwd.sweeps[i];
         sa.from_zero = (i == 0 && !prog->has_init) ? 1 : 0;
-        QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
+        if (prog->use_jit)
+            QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), 1, s));
+        else
+            QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
         ctx->launches++;
     }
     if (P.prec == QF_C128) {

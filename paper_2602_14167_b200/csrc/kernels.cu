@@ -184,8 +184,9 @@ size_t sweep_smem_bytes(int prec, bool bwd, const DevSweep& sw, int max_mat, int
     const int nwarps = (T + 31) / 32;
     size_t bytes = TS * vs * (bwd ? 2 : 1);
     bytes += (size_t)((max_mat + 1) & ~1) * vs;
-    bytes += (size_t)max_taps * nwarps * 8;
-    bytes += (size_t)(1 << sw.R) * 4;
+    bytes += (size_t)((max_taps * nwarps + 1) & ~1) * 8;
+    bytes += (size_t)(sw.op_end - sw.op_begin) * sizeof(DevOp);
+    bytes += (size_t)sw.n_phases * sizeof(DevPhase);
     return bytes;
 }
 

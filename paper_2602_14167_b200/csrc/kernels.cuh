@@ -8,23 +8,6 @@
 
 namespace qfb {
 
-struct SweepArgs {
-    void* psi;                 // [B][N] complex (float2 / double2)
-    void* lam;                 // adjoint state (backward only)
-    const double* theta;       // [B_total][P]
-    int P;
-    int n;
-    int batch_offset;          // global index of blockIdx.y == 0 (theta rows)
-    int from_zero;             // forward sweep 0 builds |0..0> in-tile
-    DevSweep sw;               // this sweep (by value)
-    const DevPhase* phases;
-    const DevOp* ops;
-    const DevGate* gates;
-    const double* cmats;       // constant matrices [n][16][2]
-    double* tap_part;          // [B][n_taps_total][tiles]
-    int n_taps_total;
-};
-
 struct HArgs {
     const void* psi;
     void* lam;

@@ -7,6 +7,8 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <complex>
 #include <map>
@@ -16,12 +18,23 @@
 
 namespace qfb {
 
+static_assert((int)GK_H == (int)QF_H && (int)GK_RX == (int)QF_RX && (int)GK_RZZ == (int)QF_RZZ && (int)GK_CX == (int)QF_CX &&
+                  (int)GK_SU4 == (int)QF_SU4 && (int)GK_UNITARY == (int)QF_UNITARY,
+              "GateKind must mirror qf_gate");
+
 Geometry geometry(int prec, int n) {
     Geometry g;
     if (prec == QF_C128) {
         g.kf = 12; g.Rf = 4; g.kb = 11; g.Rb = 3; g.kh = 11; g.c = 3; g.W = 3;
     } else {
         g.kf = 13; g.Rf = 5; g.kb = 12; g.Rb = 4; g.kh = 12; g.c = 4; g.W = 4;
+    }
+    // development override: QF_GEOM_C64 / QF_GEOM_C128 = "kf,Rf,kb,Rb"
+    if (const char* e = std::getenv(prec == QF_C128 ? "QF_GEOM_C128" : "QF_GEOM_C64")) {
+        int a, b, c, d;
+        if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
+            g.kf = a; g.Rf = b; g.kb = c; g.Rb = d;
+        }
     }
     g.kf = std::min(g.kf, n);
     g.kb = std::min(g.kb, n);

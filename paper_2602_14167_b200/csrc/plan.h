@@ -16,9 +16,26 @@
 // bit n-1-q of the basis index (site 0 = most significant, circuit.cpp:87).
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#else
+typedef unsigned char uint8_t;
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
+#endif
 
 namespace qfb {
+
+// Gate kinds: mirror of qf_gate (include/qforge_b200.h, = qforge::Gate,
+// reference include/qforge/circuit.hpp:14-23); static_assert'ed in plan.cpp.
+enum GateKind : int32_t {
+    GK_H = 0, GK_X, GK_Y, GK_Z, GK_S, GK_RX, GK_RY, GK_RZ, GK_RZZ, GK_CX, GK_CZ,
+    GK_SU4, GK_CSUM, GK_SUBSPACE_RY, GK_SUBSPACE_RZ, GK_UNITARY
+};
 
 constexpr int kMaxTileBits = 14;
 constexpr int kMaxReg = 5;
@@ -106,6 +123,24 @@ struct DevGroup {
     uint32_t f_out;    // flip bits above the tile
     int32_t term_begin, term_end;
     int32_t pad;
+};
+
+// Kernel arguments of one sweep launch (AOT interpreter and NVRTC kernels).
+struct SweepArgs {
+    void* psi;                 // [B][N] complex (float2 / double2)
+    void* lam;                 // adjoint state (backward only)
+    const double* theta;       // [B_total][P]
+    int P;
+    int n;
+    int batch_offset;          // global index of blockIdx.y == 0 (theta rows)
+    int from_zero;             // forward sweep 0 builds |0..0> in-tile
+    DevSweep sw;               // this sweep (by value)
+    const DevPhase* phases;
+    const DevOp* ops;
+    const DevGate* gates;
+    const double* cmats;       // constant matrices [n][16][2]
+    double* tap_part;          // [B][n_taps_total][tiles]
+    int n_taps_total;
 };
 
 }  // namespace qfb

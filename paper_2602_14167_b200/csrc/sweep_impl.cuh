@@ -1,50 +1,16 @@
-// sweep_impl.cuh -- device code of the fused tile sweep (included by the
-// per-precision/direction translation units so they compile in parallel).
+// sweep_impl.cuh -- device code of the AOT (interpreter) fused tile sweep
+// (included by the per-precision/direction translation units so they compile
+// in parallel).  The NVRTC-specialised variant lives in jit.cpp.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <type_traits>
 
 #include "../../include/qforge_b200.h"
+#include "device_common.cuh"
 #include "kernels.cuh"
 
 namespace qfb {
-
-template <typename RT> struct CxT;
-template <> struct CxT<float> { using T = float2; };
-template <> struct CxT<double> { using T = double2; };
-
-// a*b + acc (complex), FMA chains
-template <typename V> __device__ __forceinline__ V cfma(V a, V b, V acc) {
-    acc.x = fma(a.x, b.x, acc.x);
-    acc.x = fma(-a.y, b.y, acc.x);
-    acc.y = fma(a.x, b.y, acc.y);
-    acc.y = fma(a.y, b.x, acc.y);
-    return acc;
-}
-template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
-    V r;
-    r.x = a.x * b.x;
-    r.x = fma(-a.y, b.y, r.x);
-    r.y = a.x * b.y;
-    r.y = fma(a.y, b.x, r.y);
-    return r;
-}
-// Im(conj(u) v), Re(conj(u) v)
-template <typename V> __device__ __forceinline__ auto imcv(V u, V v) { return fma(u.x, v.y, -u.y * v.x); }
-template <typename V> __device__ __forceinline__ auto recv(V u, V v) { return fma(u.x, v.x, u.y * v.y); }
-
-// XOR-fold swizzle of a tile-local amplitude index (linear over GF(2)); W bits
-// select the shared-memory bank group (16 x 8B for c64, 8 x 16B for c128).
-template <int W> __device__ __forceinline__ uint32_t swz(uint32_t p) {
-    uint32_t x = p >> W, f = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        f ^= x;
-        x >>= W;
-    }
-    return p ^ (f & ((1u << W) - 1));
-}
 
 template <int V_> using IC = std::integral_constant<int, V_>;
 
@@ -214,94 +180,6 @@ template <int NR, typename V> __device__ __forceinline__ auto t_sum(const V* x, 
     return s;
 }
 
-__device__ __forceinline__ unsigned lane_mask(int T) { return T >= 32 ? 0xffffffffu : ((1u << T) - 1); }
-
-__device__ __forceinline__ void tap_store(double v, double* stap, int tap, int nwarps, int T) {
-    const unsigned m = lane_mask(T);
-    for (int o = (T >= 32 ? 16 : T / 2); o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
-    if ((threadIdx.x & 31) == 0) stap[tap * nwarps + (threadIdx.x >> 5)] = v;
-}
-
-// ---------------------------------------------------------------------------
-// gate matrices (computed per CTA from theta in double, circuit.cpp:202-302)
-// ---------------------------------------------------------------------------
-template <typename V, bool ADJ>
-__device__ __forceinline__ void put_c(V* out, int o, double re, double im) {
-    V r;
-    r.x = re;
-    r.y = ADJ ? -im : im;
-    out[o] = r;
-}
-
-// Writes the op's matrix block (the adjoint for the backward pass).  Layouts:
-// G1/R1: m00 m01 m10 m11; RX: (c, s) of [[c, -i s], [-i s, c]]; D1: d0 d1;
-// D2: d00 d01 d10 d11; G2: row-major 4x4.
-template <typename V, bool ADJ>
-__device__ void build_matrix(const DevOp& op, const DevGate& g, const double* th,
-                             const double* cmats, V* out) {
-    const double p = g.slot >= 0 ? g.coef * th[g.slot] + g.offset : g.offset;
-    double s, c;
-    sincos(0.5 * p, &s, &c);
-    const double isq = 0.70710678118654752440;  // 1/sqrt(2), circuit.cpp:205
-    switch (g.kind) {
-        case QF_H:  // self-adjoint
-            put_c<V, false>(out, 0, isq, 0); put_c<V, false>(out, 1, isq, 0);
-            put_c<V, false>(out, 2, isq, 0); put_c<V, false>(out, 3, -isq, 0);
-            return;
-        case QF_RY:  // [[c, -s], [s, c]]; adjoint = transpose
-            put_c<V, false>(out, 0, c, 0); put_c<V, false>(out, 1, ADJ ? s : -s, 0);
-            put_c<V, false>(out, 2, ADJ ? -s : s, 0); put_c<V, false>(out, 3, c, 0);
-            return;
-        case QF_RX:
-            put_c<V, false>(out, 0, c, ADJ ? -s : s);
-            return;
-        case QF_Y:  // [[0, -i], [i, 0]], self-adjoint
-            put_c<V, false>(out, 0, 0, 0); put_c<V, false>(out, 1, 0, -1);
-            put_c<V, false>(out, 2, 0, 1); put_c<V, false>(out, 3, 0, 0);
-            return;
-        case QF_Z: put_c<V, ADJ>(out, 0, 1, 0); put_c<V, ADJ>(out, 1, -1, 0); return;
-        case QF_S: put_c<V, ADJ>(out, 0, 1, 0); put_c<V, ADJ>(out, 1, 0, 1); return;
-        case QF_RZ: put_c<V, ADJ>(out, 0, c, -s); put_c<V, ADJ>(out, 1, c, s); return;
-        case QF_RZZ:
-            put_c<V, ADJ>(out, 0, c, -s); put_c<V, ADJ>(out, 1, c, s);
-            put_c<V, ADJ>(out, 2, c, s); put_c<V, ADJ>(out, 3, c, -s);
-            return;
-        case QF_CZ:
-            put_c<V, ADJ>(out, 0, 1, 0); put_c<V, ADJ>(out, 1, 1, 0);
-            put_c<V, ADJ>(out, 2, 1, 0); put_c<V, ADJ>(out, 3, -1, 0);
-            return;
-        case QF_SU4:
-        case QF_UNITARY: {
-            const double* m = cmats + 32 * (size_t)g.mat;  // row-major 4x4 complex
-#define QF_M(r, cc) m[2 * ((r) * 4 + (cc))], m[2 * ((r) * 4 + (cc)) + 1]
-            switch (op.kind) {
-                case DK_G1: case DK_R1:
-                    put_c<V, ADJ>(out, 0, QF_M(0, 0));
-                    put_c<V, ADJ>(out, 1, ADJ ? m[2 * 4] : m[2], ADJ ? m[2 * 4 + 1] : m[3]);
-                    put_c<V, ADJ>(out, 2, ADJ ? m[2] : m[2 * 4], ADJ ? m[3] : m[2 * 4 + 1]);
-                    put_c<V, ADJ>(out, 3, QF_M(1, 1));
-                    return;
-                case DK_D1:
-                    put_c<V, ADJ>(out, 0, QF_M(0, 0)); put_c<V, ADJ>(out, 1, QF_M(1, 1));
-                    return;
-                case DK_D2:
-                    put_c<V, ADJ>(out, 0, QF_M(0, 0)); put_c<V, ADJ>(out, 1, QF_M(1, 1));
-                    put_c<V, ADJ>(out, 2, QF_M(2, 2)); put_c<V, ADJ>(out, 3, QF_M(3, 3));
-                    return;
-                case DK_G2:
-                    for (int r = 0; r < 4; ++r)
-                        for (int cc = 0; cc < 4; ++cc) {
-                            const int sr = ADJ ? cc : r, sc = ADJ ? r : cc;
-                            put_c<V, ADJ>(out, r * 4 + cc, QF_M(sr, sc));
-                        }
-                    return;
-                default: return;
-            }
-#undef QF_M
-        }
-        default: return;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // one op inside a phase
@@ -420,19 +298,19 @@ __device__ __forceinline__ void apply_op(const DevOp& op, V* x, V* y, uint32_t g
         }
         default:
             if constexpr (BWD) {
-                double v = 0;
+                RT v = 0;
                 switch (op.kind) {
                     case DK_TX:
-                        with_rb<R>(op.rb0, [&](auto B) { v = (double)t_x<decltype(B)::value, NR>(x, y); });
+                        with_rb<R>(op.rb0, [&](auto B) { v = t_x<decltype(B)::value, NR>(x, y); });
                         break;
                     case DK_TY:
-                        with_rb<R>(op.rb0, [&](auto B) { v = (double)t_y<decltype(B)::value, NR>(x, y); });
+                        with_rb<R>(op.rb0, [&](auto B) { v = t_y<decltype(B)::value, NR>(x, y); });
                         break;
                     case DK_TZ:
                         if (op.rb0 >= 0) {
-                            with_rb<R>(op.rb0, [&](auto B) { v = (double)t_z<decltype(B)::value, NR>(x, y); });
+                            with_rb<R>(op.rb0, [&](auto B) { v = t_z<decltype(B)::value, NR>(x, y); });
                         } else {
-                            v = (double)t_sum<NR>(x, y);
+                            v = t_sum<NR>(x, y);
                             if ((g_t >> op.pos0) & 1) v = -v;
                         }
                         break;
@@ -441,22 +319,22 @@ __device__ __forceinline__ void apply_op(const DevOp& op, V* x, V* y, uint32_t g
                             with_rb<R>(op.rb0, [&](auto B) {
                                 with_rb<R>(op.rb1, [&](auto C) {
                                     if constexpr (decltype(B)::value != decltype(C)::value)
-                                        v = (double)t_zz<decltype(B)::value, decltype(C)::value, NR>(x, y);
+                                        v = t_zz<decltype(B)::value, decltype(C)::value, NR>(x, y);
                                 });
                             });
                         } else if (op.rb0 >= 0 || op.rb1 >= 0) {
                             const int rb = op.rb0 >= 0 ? op.rb0 : op.rb1;
                             const int cp = op.rb0 >= 0 ? op.pos1 : op.pos0;
-                            with_rb<R>(rb, [&](auto B) { v = (double)t_z<decltype(B)::value, NR>(x, y); });
+                            with_rb<R>(rb, [&](auto B) { v = t_z<decltype(B)::value, NR>(x, y); });
                             if ((g_t >> cp) & 1) v = -v;
                         } else {
-                            v = (double)t_sum<NR>(x, y);
+                            v = t_sum<NR>(x, y);
                             if (((g_t >> op.pos0) ^ (g_t >> op.pos1)) & 1) v = -v;
                         }
                         break;
                     default: break;
                 }
-                tap_store(v, stap, op.tap, nwarps, T);
+                tap_store<RT>(v, stap, op.tap, nwarps, T);
             }
             break;
     }
@@ -466,7 +344,7 @@ __device__ __forceinline__ void apply_op(const DevOp& op, V* x, V* y, uint32_t g
 // fused tile sweep
 // ---------------------------------------------------------------------------
 template <typename RT, int R, bool BWD>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
     using V = typename CxT<RT>::T;
     constexpr int NR = 1 << R;
     constexpr int W = sizeof(RT) == 4 ? 4 : 3;
@@ -482,7 +360,9 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
     V* tile2 = tile + (BWD ? TS : 0);
     V* smat = tile2 + TS;
     double* stap = reinterpret_cast<double*>(smat + ((sw.n_mat + 1) & ~1));
-    uint32_t* jtab = reinterpret_cast<uint32_t*>(stap + sw.n_taps * nwarps);
+    const int n_ops = sw.op_end - sw.op_begin;
+    DevOp* sops = reinterpret_cast<DevOp*>(stap + ((sw.n_taps * nwarps + 1) & ~1));
+    DevPhase* sph = reinterpret_cast<DevPhase*>(sops + n_ops);
 
     const uint32_t tile_id = blockIdx.x;
     const int b = blockIdx.y;
@@ -500,42 +380,50 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
             m ^= low;
         }
     }
-    for (int j = tid; j < NR; j += T) {
-        uint32_t v = 0;
-        for (int r = 0; r < R; ++r)
-            if ((j >> r) & 1) v |= 1u << sw.tb[k - R + r];
-        jtab[j] = v;
-    }
+    // memory offsets of the load/store loop index j (tile bits k-R .. k-1), in registers
+    uint32_t jb[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) jb[r] = 1u << sw.tb[k - R + r];
     uint32_t g_ld = tile_base;
     for (int j = 0; j < k - R; ++j)
         if ((tid >> j) & 1) g_ld |= 1u << sw.tb[j];
 
+    // HBM -> registers: every load in flight before the first shared-memory store
+    V v0[NR];
+    V v1[BWD ? NR : 1];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        uint32_t g = g_ld;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if ((j >> r) & 1) g |= jb[r];
+        if (!BWD && a.from_zero) {
+            v0[j].x = (g == 0) ? RT(1) : RT(0);
+            v0[j].y = RT(0);
+        } else {
+            v0[j] = st[g];
+        }
+        if constexpr (BWD) v1[j] = lm[g];
+    }
+
+    // op list, phases and gate matrices of this sweep -> shared memory
+    for (int o = tid; o < n_ops; o += T) sops[o] = a.ops[sw.op_begin + o];
+    for (int f = tid; f < sw.n_phases; f += T) sph[f] = a.phases[sw.phase_begin + f];
     const double* th = a.theta + (size_t)(b + a.batch_offset) * a.P;
     for (int o = sw.op_begin + tid; o < sw.op_end; o += T) {
         const DevOp op = a.ops[o];
         if (op.moff >= 0) build_matrix<V, BWD>(op, a.gates[op.gate], th, a.cmats, smat + op.moff);
     }
-    __syncthreads();
-
-    // HBM -> shared tile (coalesced: lanes walk tile bits 0..4, the low ones contiguous)
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         const uint32_t p = tid + (uint32_t)T * j;
-        const uint32_t g = g_ld | jtab[j];
-        V v;
-        if (!BWD && a.from_zero) {
-            v.x = (g == 0) ? RT(1) : RT(0);
-            v.y = RT(0);
-        } else {
-            v = st[g];
-        }
-        tile[swz<W>(p)] = v;
-        if constexpr (BWD) tile2[swz<W>(p)] = lm[g];
+        tile[swz<W>(p)] = v0[j];
+        if constexpr (BWD) tile2[swz<W>(p)] = v1[j];
     }
     __syncthreads();
 
     for (int f = 0; f < sw.n_phases; ++f) {
-        const DevPhase* ph = a.phases + sw.phase_begin + f;
+        const DevPhase* ph = sph + f;
         uint32_t p_t = 0, g_t = tile_base;
         for (int j = 0; j < k - R; ++j) {
             const int tl = ph->thr_tl[j];
@@ -561,10 +449,14 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         }
         uint32_t s_st = s_t;
         asm volatile("" : "+r"(s_st));
-        const int ob = ph->op_begin, oe = ph->op_end;
-        for (int o = ob; o < oe; ++o) {
-            const DevOp op = a.ops[o];
-            apply_op<RT, R, BWD>(op, x, y, g_t, smat, stap, nwarps, T);
+        const int ob = ph->op_begin - sw.op_begin, oe = ph->op_end - sw.op_begin;
+        if (ob < oe) {
+            DevOp nxt = sops[ob];
+            for (int o = ob; o < oe; ++o) {
+                const DevOp op = nxt;
+                if (o + 1 < oe) nxt = sops[o + 1];  // prefetch: hides the shared-memory latency
+                apply_op<RT, R, BWD>(op, x, y, g_t, smat, stap, nwarps, T);
+            }
         }
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
@@ -578,13 +470,21 @@ __global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
         __syncthreads();
     }
 
-    // shared tile -> HBM
+    // shared tile -> registers -> HBM
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         const uint32_t p = tid + (uint32_t)T * j;
-        const uint32_t g = g_ld | jtab[j];
-        st[g] = tile[swz<W>(p)];
-        if constexpr (BWD) lm[g] = tile2[swz<W>(p)];
+        v0[j] = tile[swz<W>(p)];
+        if constexpr (BWD) v1[j] = tile2[swz<W>(p)];
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+        uint32_t g = g_ld;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if ((j >> r) & 1) g |= jb[r];
+        st[g] = v0[j];
+        if constexpr (BWD) lm[g] = v1[j];
     }
     if constexpr (BWD) {
         const int tiles = gridDim.x;

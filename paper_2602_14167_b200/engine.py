@@ -131,6 +131,16 @@ class Program:
         return {"fwd_sweeps": v[0].value, "bwd_sweeps": v[1].value, "fwd_tile_bits": v[2].value,
                 "bwd_tile_bits": v[3].value}
 
+    def jit_status(self) -> dict:
+        """Specialised-kernel status (NVRTC): active, kernels compiled / loaded from cache, seconds."""
+        a, c, k = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        sec = ctypes.c_double()
+        err = ctypes.c_char_p()
+        check(self.ctx.lib.qf_program_jit_status(self.handle, ctypes.byref(a), ctypes.byref(c), ctypes.byref(k),
+                                                 ctypes.byref(sec), ctypes.byref(err)))
+        return {"active": bool(a.value), "compiled": c.value, "cached": k.value, "seconds": sec.value,
+                "error": (err.value or b"").decode()}
+
     def close(self) -> None:
         if getattr(self, "handle", None):
             self.ctx.lib.qf_program_destroy(self.handle)

@@ -25,12 +25,12 @@ def check(name, n, ops, P, h, B=3, precs=("c128", "c64"), seed=1, mats=None):
             scale = max(np.abs(E_ref).max(), np.abs(G_ref).max() if P else 0, 1e-300)
             eE = np.abs(E - E_ref).max() / scale
             eG = np.abs(G - G_ref).max() / max(np.abs(G_ref).max(), 1e-300) if P else 0
-            print(f"{name:28s} {prec}: dE={eE:.2e} dG={eG:.2e} info={prog.info()} t_ref={tr:.2f}s t_gpu={tg:.3f}s E0={E[0]:.6f}/{E_ref[0]:.6f}", flush=True)
+            print(f"{name:28s} {prec}: dE={eE:.2e} dG={eG:.2e} info={prog.info()} jit={prog.jit_status()['active']} t_ref={tr:.2f}s t_gpu={tg:.3f}s E0={E[0]:.6f}/{E_ref[0]:.6f}", flush=True)
         except Exception as e:
             print(f"{name:28s} {prec}: EXC {e}", flush=True)
             traceback.print_exc()
 
-for n in (1, 2, 3, 5, 6, 8, 10, 11, 12, 13, 14, 16):
+for n in (1, 2, 3, 5, 8, 10, 13, 14, 16):
     if n >= 2:
         _, ops, P = po.hea_template(n, 2)
         check(f"hea n={n}", n, ops, P, po.tfim(n, 1.0))
