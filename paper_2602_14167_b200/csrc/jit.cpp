@@ -9,6 +9,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
@@ -82,7 +83,15 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const char* RTt = dbl ? "double" : "float";
     const int minb = [] {
         const char* e = std::getenv("QF_JIT_MINB");
-        return e ? std::max(1, atoi(e)) : 1;
+        return e ? std::max(1, atoi(e)) : 2;
+    }();
+    const bool allow_direct = [] {
+        const char* e = std::getenv("QF_JIT_DIRECT");
+        return !(e && e[0] == '0');
+    }();
+    const bool allow_fuse = [] {
+        const char* e = std::getenv("QF_JIT_FUSE");
+        return !(e && e[0] == '0');
     }();
     Out o;
     o.s += kPrelude;
@@ -95,13 +104,41 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     o("  V* tile2 = tile + %u;", bwd ? (1u << k) : 0u);
     o("  V* smat = tile2 + %u;", 1u << k);
     o("  double* stap = reinterpret_cast<double*>(smat + %d);", (sw.n_mat + 1) & ~1);
-    o("  (void)tile2; (void)stap;");
+    o("  (void)tile; (void)tile2; (void)stap;");
     o("  const uint32_t tid = threadIdx.x, tile_id = blockIdx.x; const int b = blockIdx.y;");
     o("  V* st = reinterpret_cast<V*>(a.psi) + (size_t)b * %zuull;", (size_t)1 << P.n);
     if (bwd) o("  V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", (size_t)1 << P.n);
     o("  const uint32_t tile_base = pdep_u32(tile_id, %uu);", sw.out_mask);
-    o("  uint32_t g_ld = tile_base;");
-    for (int j = 0; j < k - R; ++j) o("  g_ld |= ((tid >> %d) & 1u) << %d;", j, sw.tb[j]);
+
+    int tl_of_pos[64];
+    for (int p = 0; p < 64; ++p) tl_of_pos[p] = -1;
+    for (int t = 0; t < k; ++t) tl_of_pos[(int)sw.tb[t]] = t;
+    const int nph = sw.n_phases;
+    auto phase = [&](int f) -> const DevPhase& { return pass.phases[sw.phase_begin + f]; };
+    // A phase can move its registers straight to/from HBM when its lanes cover the
+    // lowest tile bits (>= 32-byte contiguous runs per lane group: full sectors).
+    auto lanes_cover_low = [&](const DevPhase& ph) {
+        if (T < 32) return true;
+        const int need = dbl ? 1 : 2;
+        int have = 0;
+        for (int j = 0; j < 5 && j < k - R; ++j)
+            if (ph.thr_tl[j] < need) ++have;
+        return have == need;
+    };
+    const bool direct_first = allow_direct && nph > 0 && lanes_cover_low(phase(0));
+    const bool direct_last = allow_direct && nph > 0 && lanes_cover_low(phase(nph - 1));
+    // memory offset of register index l in phase f, and of the phase's thread base
+    auto reg_goff = [&](const DevPhase& ph, int l) {
+        uint32_t off = 0;
+        for (int r = 0; r < R; ++r)
+            if ((l >> r) & 1) off |= 1u << sw.tb[(int)ph.reg_tl[r]];
+        return off;
+    };
+    auto emit_gbase = [&](const DevPhase& ph, const char* name) {
+        o("  uint32_t %s = tile_base;", name);
+        for (int j = 0; j < k - R; ++j) o("  %s |= ((tid >> %d) & 1u) << %d;", name, j, sw.tb[(int)ph.thr_tl[j]]);
+    };
+
     std::vector<uint32_t> joff(NR);
     for (int j = 0; j < NR; ++j) {
         uint32_t off = 0;
@@ -109,12 +146,26 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if ((j >> r) & 1) off |= 1u << sw.tb[k - R + r];
         joff[j] = off;
     }
-    // HBM -> registers (all loads in flight), then prologue, then registers -> shared
-    for (int j = 0; j < NR; ++j) {
-        if (!bwd)
-            o("  V v%d = a.from_zero ? mk_basis<V>((g_ld | %uu) == 0u) : st[g_ld | %uu];", j, joff[j], joff[j]);
-        else
-            o("  V v%d = st[g_ld | %uu]; V w%d = lm[g_ld | %uu];", j, joff[j], j, joff[j]);
+    if (!direct_first || !direct_last) {
+        o("  uint32_t g_ld = tile_base;");
+        for (int j = 0; j < k - R; ++j) o("  g_ld |= ((tid >> %d) & 1u) << %d;", j, sw.tb[j]);
+    }
+    if (direct_first) {
+        emit_gbase(phase(0), "g_p0");
+        for (int l = 0; l < NR; ++l) {
+            const uint32_t off = reg_goff(phase(0), l);
+            if (!bwd)
+                o("  V x%d = a.from_zero ? mk_basis<V>((g_p0 | %uu) == 0u) : st[g_p0 | %uu];", l, off, off);
+            else
+                o("  V x%d = st[g_p0 | %uu]; V y%d = lm[g_p0 | %uu];", l, off, l, off);
+        }
+    } else {
+        for (int j = 0; j < NR; ++j) {
+            if (!bwd)
+                o("  V v%d = a.from_zero ? mk_basis<V>((g_ld | %uu) == 0u) : st[g_ld | %uu];", j, joff[j], joff[j]);
+            else
+                o("  V v%d = st[g_ld | %uu]; V w%d = lm[g_ld | %uu];", j, joff[j], j, joff[j]);
+        }
     }
     o("  {");
     o("    const double* th = a.theta + (size_t)(b + a.batch_offset) * a.P;");
@@ -124,20 +175,23 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
       bwd ? "true" : "false");
     o("    }");
     o("  }");
-    for (int j = 0; j < NR; ++j) {
-        o("  tile[swz<%d>(tid + %uu)] = v%d;%s", W, (unsigned)(T * j), j,
-          bwd ? (" tile2[swz<" + std::to_string(W) + ">(tid + " + std::to_string(T * j) + "u)] = w" +
-                 std::to_string(j) + ";").c_str()
-              : "");
+    if (!direct_first) {
+        for (int j = 0; j < NR; ++j) {
+            if (bwd)
+                o("  tile[swz<%d>(tid + %uu)] = v%d; tile2[swz<%d>(tid + %uu)] = w%d;", W, (unsigned)(T * j), j, W,
+                  (unsigned)(T * j), j);
+            else
+                o("  tile[swz<%d>(tid + %uu)] = v%d;", W, (unsigned)(T * j), j);
+        }
     }
     o("  __syncthreads();");
 
-    int tl_of_pos[64];
-    for (int p = 0; p < 64; ++p) tl_of_pos[p] = -1;
-    for (int t = 0; t < k; ++t) tl_of_pos[(int)sw.tb[t]] = t;
+    std::vector<const char*> arrs = {"x"};
+    if (bwd) arrs.push_back("y");
+    int uid = 0;  // unique names inside fused blocks
 
-    for (int f = 0; f < sw.n_phases; ++f) {
-        const DevPhase& ph = pass.phases[sw.phase_begin + f];
+    for (int f = 0; f < nph; ++f) {
+        const DevPhase& ph = phase(f);
         int thr_of_tl[kMaxTileBits];
         for (int t = 0; t < kMaxTileBits; ++t) thr_of_tl[t] = -1;
         for (int j = 0; j < k - R; ++j) thr_of_tl[(int)ph.thr_tl[j]] = j;
@@ -157,27 +211,31 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             }
             return s;
         };
-        o("  { // phase %d", f);
-        o("    uint32_t s_t = 0;");
-        for (int j = 0; j < k - R; ++j)
-            o("    s_t ^= (0u - ((tid >> %d) & 1u)) & %uu;", j, swz_host(1u << ph.thr_tl[j], W));
+        const bool dfirst = (f == 0 && direct_first);
+        const bool dlast = (f == nph - 1 && direct_last);
+        o("  { // phase %d%s%s", f, dfirst ? " (registers from HBM)" : "", dlast ? " (registers to HBM)" : "");
         std::vector<uint32_t> offs(NR);
-        for (int l = 0; l < NR; ++l) {
-            uint32_t off = 0;
-            for (int r = 0; r < R; ++r)
-                if ((l >> r) & 1) off |= 1u << ph.reg_tl[r];
-            offs[l] = swz_host(off, W);
+        if (!dfirst || !dlast) {
+            o("    uint32_t s_t = 0;");
+            for (int j = 0; j < k - R; ++j)
+                o("    s_t ^= (0u - ((tid >> %d) & 1u)) & %uu;", j, swz_host(1u << ph.thr_tl[j], W));
+            for (int l = 0; l < NR; ++l) {
+                uint32_t off = 0;
+                for (int r = 0; r < R; ++r)
+                    if ((l >> r) & 1) off |= 1u << ph.reg_tl[r];
+                offs[l] = swz_host(off, W);
+            }
         }
-        for (int l = 0; l < NR; ++l) {
-            if (bwd)
-                o("    V x%d = tile[s_t ^ %uu]; V y%d = tile2[s_t ^ %uu];", l, offs[l], l, offs[l]);
-            else
-                o("    V x%d = tile[s_t ^ %uu];", l, offs[l]);
+        if (!dfirst) {
+            for (int l = 0; l < NR; ++l) {
+                if (bwd)
+                    o("    V x%d = tile[s_t ^ %uu]; V y%d = tile2[s_t ^ %uu];", l, offs[l], l, offs[l]);
+                else
+                    o("    V x%d = tile[s_t ^ %uu];", l, offs[l]);
+            }
         }
         std::vector<int> phys(NR);
         for (int l = 0; l < NR; ++l) phys[l] = l;
-        std::vector<const char*> arrs = {"x"};
-        if (bwd) arrs.push_back("y");
         auto pairs = [&](int bit) {
             std::vector<std::pair<int, int>> v;
             for (int l = 0; l < NR; ++l)
@@ -188,8 +246,163 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             for (int l = 0; l < NR; ++l)
                 if (!((l >> tbit) & 1) && (cbit < 0 || ((l >> cbit) & 1))) std::swap(phys[l], phys[l | (1 << tbit)]);
         };
-        for (int oi = ph.op_begin; oi < ph.op_end; ++oi) {
+        auto is_diagish = [&](uint8_t kd) { return kd == DK_D1 || kd == DK_D2 || kd == DK_TZ || kd == DK_TZZ; };
+
+        // ---- fused run of diagonal gates and Z-type taps (they all commute) ----
+        auto flush_diag_run = [&](int ob, int oe) {
+            const int id = uid++;
+            o("    { // fused diagonal run (%d ops)", oe - ob);
+            // taps first: v_l = Im(conj(lambda_l) psi_l) is invariant under diagonal
+            // unitaries applied to both states, so every tap of the run shares it
+            bool any_tap = false;
+            for (int oi = ob; oi < oe; ++oi) any_tap |= pass.ops[oi].kind == DK_TZ || pass.ops[oi].kind == DK_TZZ;
+            if (any_tap)
+                for (int l = 0; l < NR; ++l) o("      const RT v%d_%d = imcv(y%d, x%d);", id, l, phys[l], phys[l]);
+            std::vector<std::string> rt_factors;                   // per-thread scalars
+            std::vector<std::vector<std::pair<std::string, std::string>>> perbit(R);  // (f0, f1) per register bit
+            struct D2s { int r0, r1; std::string d[4]; };
+            std::vector<D2s> d2s;
+            for (int oi = ob; oi < oe; ++oi) {
+                const DevOp& op = pass.ops[oi];
+                const std::string nm = "f" + std::to_string(id) + "_" + std::to_string(oi - ob);
+                if (op.kind == DK_TZ || op.kind == DK_TZZ) {
+                    BitSrc s0 = src(op.pos0);
+                    BitSrc s1 = op.kind == DK_TZZ ? src(op.pos1) : BitSrc{};
+                    std::string sum;
+                    o("      { RT s = 0;");
+                    for (int l = 0; l < NR; ++l) {
+                        int sg = 0;
+                        if (s0.rb >= 0) sg ^= (l >> s0.rb) & 1;
+                        if (op.kind == DK_TZZ && s1.rb >= 0) sg ^= (l >> s1.rb) & 1;
+                        o("        s %s= v%d_%d;", sg ? "-" : "+", id, l);
+                    }
+                    std::string rt;
+                    if (s0.rb < 0) rt = s0.expr;
+                    if (op.kind == DK_TZZ && s1.rb < 0) rt = rt.empty() ? s1.expr : "(" + rt + " ^ " + s1.expr + ")";
+                    if (!rt.empty()) o("        if (%s) s = -s;", rt.c_str());
+                    o("        tap_store<RT>(s, stap, %d, %d, %d); }", op.tap, nwarps, T);
+                    continue;
+                }
+                if (op.kind == DK_D1) {
+                    o("      const V %s_0 = smat[%d], %s_1 = smat[%d];", nm.c_str(), op.moff, nm.c_str(), op.moff + 1);
+                    BitSrc s0 = src(op.pos0);
+                    if (s0.rb >= 0)
+                        perbit[s0.rb].push_back({nm + "_0", nm + "_1"});
+                    else
+                        rt_factors.push_back("(" + s0.expr + " ? " + nm + "_1 : " + nm + "_0)");
+                } else {  // DK_D2
+                    o("      const V %s_0 = smat[%d], %s_1 = smat[%d], %s_2 = smat[%d], %s_3 = smat[%d];", nm.c_str(),
+                      op.moff, nm.c_str(), op.moff + 1, nm.c_str(), op.moff + 2, nm.c_str(), op.moff + 3);
+                    BitSrc s0 = src(op.pos0), s1 = src(op.pos1);
+                    if (s0.rb < 0 && s1.rb < 0) {
+                        rt_factors.push_back("(" + s0.expr + " ? (" + s1.expr + " ? " + nm + "_3 : " + nm + "_2) : (" +
+                                             s1.expr + " ? " + nm + "_1 : " + nm + "_0))");
+                    } else if (s0.rb >= 0 && s1.rb < 0) {
+                        o("      const V %s_e0 = %s ? %s_1 : %s_0, %s_e1 = %s ? %s_3 : %s_2;", nm.c_str(), s1.expr.c_str(),
+                          nm.c_str(), nm.c_str(), nm.c_str(), s1.expr.c_str(), nm.c_str(), nm.c_str());
+                        perbit[s0.rb].push_back({nm + "_e0", nm + "_e1"});
+                    } else if (s0.rb < 0 && s1.rb >= 0) {
+                        o("      const V %s_e0 = %s ? %s_2 : %s_0, %s_e1 = %s ? %s_3 : %s_1;", nm.c_str(), s0.expr.c_str(),
+                          nm.c_str(), nm.c_str(), nm.c_str(), s0.expr.c_str(), nm.c_str(), nm.c_str());
+                        perbit[s1.rb].push_back({nm + "_e0", nm + "_e1"});
+                    } else {
+                        D2s d;
+                        d.r0 = s0.rb;
+                        d.r1 = s1.rb;
+                        for (int q = 0; q < 4; ++q) d.d[q] = nm + "_" + std::to_string(q);
+                        d2s.push_back(d);
+                    }
+                }
+            }
+            // combine per-thread scalars
+            const bool have_c = !rt_factors.empty();
+            if (have_c) {
+                o("      V c%d = %s;", id, rt_factors[0].c_str());
+                for (size_t q = 1; q < rt_factors.size(); ++q) o("      c%d = cmul(c%d, %s);", id, id, rt_factors[q].c_str());
+            }
+            // combine factors per register bit
+            std::vector<int> bits;
+            std::vector<std::pair<std::string, std::string>> pb(R);
+            std::vector<bool> ident(R, true);
+            for (int r = 0; r < R; ++r) {
+                bool used = !perbit[r].empty();
+                for (auto& d : d2s) used |= d.r0 == r || d.r1 == r;
+                if (!used) continue;
+                bits.push_back(r);
+                if (perbit[r].empty()) continue;
+                ident[r] = false;
+                std::string a0 = perbit[r][0].first, a1 = perbit[r][0].second;
+                for (size_t q = 1; q < perbit[r].size(); ++q) {
+                    const std::string n0 = "p" + std::to_string(id) + "_" + std::to_string(r) + "_" + std::to_string(q);
+                    o("      const V %s_0 = cmul(%s, %s), %s_1 = cmul(%s, %s);", n0.c_str(), a0.c_str(),
+                      perbit[r][q].first.c_str(), n0.c_str(), a1.c_str(), perbit[r][q].second.c_str());
+                    a0 = n0 + "_0";
+                    a1 = n0 + "_1";
+                }
+                pb[r] = {a0, a1};
+            }
+            if (!have_c && bits.empty()) {
+                o("    }");
+                return;
+            }
+            // table over the factor bits: entry index = bits of l restricted to `bits`
+            std::vector<std::string> tab = {have_c ? ("c" + std::to_string(id)) : std::string()};
+            int tcount = 0;
+            for (size_t bi = 0; bi < bits.size(); ++bi) {
+                const int r = bits[bi];
+                std::vector<std::string> nt(tab.size() * 2);
+                for (size_t e = 0; e < tab.size(); ++e) {
+                    for (int v = 0; v < 2; ++v) {
+                        const std::string fac = ident[r] ? std::string() : (v ? pb[r].second : pb[r].first);
+                        std::string res;
+                        if (tab[e].empty()) res = fac;
+                        else if (fac.empty()) res = tab[e];
+                        else {
+                            res = "t" + std::to_string(id) + "_" + std::to_string(tcount++);
+                            o("      const V %s = cmul(%s, %s);", res.c_str(), tab[e].c_str(), fac.c_str());
+                        }
+                        nt[e | (size_t(v) << bi)] = res;
+                    }
+                }
+                tab.swap(nt);
+            }
+            auto tidx = [&](int l) {
+                size_t e = 0;
+                for (size_t bi = 0; bi < bits.size(); ++bi)
+                    if ((l >> bits[bi]) & 1) e |= size_t(1) << bi;
+                return e;
+            };
+            for (auto& d : d2s) {  // both bits in registers: multiply the table entries
+                auto pos_in = [&](int r) { return (int)(std::find(bits.begin(), bits.end(), r) - bits.begin()); };
+                const int i0 = pos_in(d.r0), i1 = pos_in(d.r1);
+                for (size_t e = 0; e < tab.size(); ++e) {
+                    const int q = (int)(((e >> i0) & 1) << 1 | ((e >> i1) & 1));
+                    const std::string res = "t" + std::to_string(id) + "_" + std::to_string(tcount++);
+                    if (tab[e].empty())
+                        o("      const V %s = %s;", res.c_str(), d.d[q].c_str());
+                    else
+                        o("      const V %s = cmul(%s, %s);", res.c_str(), tab[e].c_str(), d.d[q].c_str());
+                    tab[e] = res;
+                }
+            }
+            for (const char* A : arrs)
+                for (int l = 0; l < NR; ++l) {
+                    const std::string& fac = tab[tidx(l)];
+                    if (!fac.empty()) o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l], fac.c_str());
+                }
+            o("    }");
+        };
+
+        int oi = ph.op_begin;
+        while (oi < ph.op_end) {
             const DevOp& op = pass.ops[oi];
+            if (allow_fuse && is_diagish(op.kind)) {
+                int oe = oi;
+                while (oe < ph.op_end && is_diagish(pass.ops[oe].kind)) ++oe;
+                flush_diag_run(oi, oe);
+                oi = oe;
+                continue;
+            }
             switch (op.kind) {
                 case DK_G1: case DK_R1: case DK_RX: {
                     o("    { const V m0 = smat[%d], m1 = smat[%d], m2 = smat[%d], m3 = smat[%d]; (void)m1; (void)m2; (void)m3;",
@@ -219,50 +432,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         o("    }");
                     }
                     break;
-                case DK_D1: {
-                    o("    { const V d0 = smat[%d], d1 = smat[%d];", op.moff, op.moff + 1);
-                    BitSrc s0 = src(op.pos0);
-                    if (s0.rb >= 0) {
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l)
-                                o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l], ((l >> s0.rb) & 1) ? "d1" : "d0");
-                    } else {
-                        o("      const V d = %s ? d1 : d0;", s0.expr.c_str());
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l) o("      %s%d = cmul(%s%d, d);", A, phys[l], A, phys[l]);
-                    }
-                    o("    }");
+                case DK_D1: case DK_D2: case DK_TZ: case DK_TZZ:
+                    flush_diag_run(oi, oi + 1);
                     break;
-                }
-                case DK_D2: {
-                    o("    { const V d00 = smat[%d], d01 = smat[%d], d10 = smat[%d], d11 = smat[%d];", op.moff,
-                      op.moff + 1, op.moff + 2, op.moff + 3);
-                    BitSrc s0 = src(op.pos0), s1 = src(op.pos1);
-                    if (s0.rb < 0 && s1.rb < 0) {
-                        o("      const V d = %s ? (%s ? d11 : d10) : (%s ? d01 : d00);", s0.expr.c_str(),
-                          s1.expr.c_str(), s1.expr.c_str());
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l) o("      %s%d = cmul(%s%d, d);", A, phys[l], A, phys[l]);
-                    } else if (s0.rb >= 0 && s1.rb >= 0) {
-                        const char* dn[4] = {"d00", "d01", "d10", "d11"};
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l)
-                                o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l],
-                                  dn[(((l >> s0.rb) & 1) << 1) | ((l >> s1.rb) & 1)]);
-                    } else if (s0.rb >= 0) {  // wire 1 runtime
-                        o("      const V e0 = %s ? d01 : d00, e1 = %s ? d11 : d10;", s1.expr.c_str(), s1.expr.c_str());
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l)
-                                o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l], ((l >> s0.rb) & 1) ? "e1" : "e0");
-                    } else {  // wire 0 runtime
-                        o("      const V e0 = %s ? d10 : d00, e1 = %s ? d11 : d01;", s0.expr.c_str(), s0.expr.c_str());
-                        for (const char* A : arrs)
-                            for (int l = 0; l < NR; ++l)
-                                o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l], ((l >> s1.rb) & 1) ? "e1" : "e0");
-                    }
-                    o("    }");
-                    break;
-                }
                 case DK_G2: {
                     o("    { const V* m = smat + %d;", op.moff);
                     const int e0 = 1 << op.rb0, e1 = 1 << op.rb1;
@@ -275,27 +447,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     o("    }");
                     break;
                 }
-                case DK_TX: case DK_TY: case DK_TZ: case DK_TZZ: {
+                case DK_TX: case DK_TY: {
                     o("    { RT s = 0;");
                     if (op.kind == DK_TX) {
                         for (auto pr : pairs(op.rb0))
                             o("      s += imcv(y%d, x%d) + imcv(y%d, x%d);", pr.first, pr.second, pr.second, pr.first);
-                    } else if (op.kind == DK_TY) {
+                    } else {
                         for (auto pr : pairs(op.rb0))
                             o("      s += recv(y%d, x%d) - recv(y%d, x%d);", pr.second, pr.first, pr.first, pr.second);
-                    } else {
-                        BitSrc s0 = src(op.pos0);
-                        BitSrc s1 = op.kind == DK_TZZ ? src(op.pos1) : BitSrc{};
-                        for (int l = 0; l < NR; ++l) {
-                            int sg = 0;
-                            if (s0.rb >= 0) sg ^= (l >> s0.rb) & 1;
-                            if (op.kind == DK_TZZ && s1.rb >= 0) sg ^= (l >> s1.rb) & 1;
-                            o("      s %s= imcv(y%d, x%d);", sg ? "-" : "+", phys[l], phys[l]);
-                        }
-                        std::string rt;
-                        if (s0.rb < 0) rt = s0.expr;
-                        if (op.kind == DK_TZZ && s1.rb < 0) rt = rt.empty() ? s1.expr : "(" + rt + " ^ " + s1.expr + ")";
-                        if (!rt.empty()) o("      if (%s) s = -s;", rt.c_str());
                     }
                     o("      tap_store<RT>(s, stap, %d, %d, %d); }", op.tap, nwarps, T);
                     break;
@@ -303,28 +462,44 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 default:
                     break;
             }
+            ++oi;
         }
-        for (int l = 0; l < NR; ++l) {
+        if (dlast) {
+            emit_gbase(ph, "g_pl");
+            for (int l = 0; l < NR; ++l) {
+                const uint32_t off = reg_goff(ph, l);
+                if (bwd)
+                    o("    st[g_pl | %uu] = x%d; lm[g_pl | %uu] = y%d;", off, phys[l], off, phys[l]);
+                else
+                    o("    st[g_pl | %uu] = x%d;", off, phys[l]);
+            }
+            o("  }");
+            if (bwd && sw.n_taps > 0) o("  __syncthreads();");
+        } else {
+            for (int l = 0; l < NR; ++l) {
+                if (bwd)
+                    o("    tile[s_t ^ %uu] = x%d; tile2[s_t ^ %uu] = y%d;", offs[l], phys[l], offs[l], phys[l]);
+                else
+                    o("    tile[s_t ^ %uu] = x%d;", offs[l], phys[l]);
+            }
+            o("    __syncthreads();");
+            o("  }");
+        }
+    }
+    if (!direct_last) {
+        for (int j = 0; j < NR; ++j) {
             if (bwd)
-                o("    tile[s_t ^ %uu] = x%d; tile2[s_t ^ %uu] = y%d;", offs[l], phys[l], offs[l], phys[l]);
+                o("  const V v%d_o = tile[swz<%d>(tid + %uu)]; const V w%d_o = tile2[swz<%d>(tid + %uu)];", j, W,
+                  (unsigned)(T * j), j, W, (unsigned)(T * j));
             else
-                o("    tile[s_t ^ %uu] = x%d;", offs[l], phys[l]);
+                o("  const V v%d_o = tile[swz<%d>(tid + %uu)];", j, W, (unsigned)(T * j));
         }
-        o("    __syncthreads();");
-        o("  }");
-    }
-    for (int j = 0; j < NR; ++j) {
-        if (bwd)
-            o("  v%d = tile[swz<%d>(tid + %uu)]; w%d = tile2[swz<%d>(tid + %uu)];", j, W, (unsigned)(T * j), j, W,
-              (unsigned)(T * j));
-        else
-            o("  v%d = tile[swz<%d>(tid + %uu)];", j, W, (unsigned)(T * j));
-    }
-    for (int j = 0; j < NR; ++j) {
-        if (bwd)
-            o("  st[g_ld | %uu] = v%d; lm[g_ld | %uu] = w%d;", joff[j], j, joff[j], j);
-        else
-            o("  st[g_ld | %uu] = v%d;", joff[j], j);
+        for (int j = 0; j < NR; ++j) {
+            if (bwd)
+                o("  st[g_ld | %uu] = v%d_o; lm[g_ld | %uu] = w%d_o;", joff[j], j, joff[j], j);
+            else
+                o("  st[g_ld | %uu] = v%d_o;", joff[j], j);
+        }
     }
     if (bwd && sw.n_taps > 0) {
         o("  for (int t = (int)tid; t < %d; t += %d) {", sw.n_taps, T);
