@@ -125,6 +125,16 @@ int qf_program_info(const qf_program* prog, int* fwd_sweeps, int* bwd_sweeps,
 int qf_program_jit_status(const qf_program* prog, int* active, int* compiled, int* cached,
                           double* seconds, const char** error);
 
+/* Host-only introspection (no GPU needed): the compiled schedule as JSON
+ * {"n":..,"passes":{"fwd"|"bwd":{"k","R","n_taps","sweeps":[{"tile_bits",
+ * "tap_begin","phases":[{"reg_bits","ops":[[dev_kind,gate,tap],..]}]}],
+ * "taps":[[slot,coef],..]}}} (needed = bytes incl. NUL), and an NVRTC
+ * compile of every specialised kernel of the program for sm_100a. */
+int qf_plan_describe(int n_qubits, int n_ops, const qf_op* ops, const double* mats, int n_mats,
+                     int n_params, int precision, char* buf, size_t buflen, size_t* needed);
+int qf_jit_compile_check(int n_qubits, int n_ops, const qf_op* ops, const double* mats,
+                         int n_mats, int n_params, int precision, int* kernels);
+
 /* ---- observables (Pauli sums) ---- */
 /* codes: [n_terms][n_qubits], 0=I 1=X 2=Y 3=Z (pauli.hpp:11-17). */
 int qf_observable_create(qf_ctx* ctx, int n_qubits, int n_terms, const int8_t* codes,

@@ -635,6 +635,81 @@ int qf_program_destroy(qf_program* p) {
     return QF_OK;
 }
 
+static int build_plan_from_ops(int n, int n_ops, const qf_op* ops, const double* mats, int n_mats, int n_params,
+                               int precision, ProgramPlan& P) {
+    if (n_ops < 0 || (n_ops > 0 && !ops)) return set_err(QF_EINVAL, "bad ops");
+    std::vector<GateSpec> specs(n_ops);
+    for (int i = 0; i < n_ops; ++i)
+        specs[i] = GateSpec{ops[i].kind, ops[i].q0, ops[i].q1, ops[i].slot, ops[i].coef, ops[i].offset, ops[i].mat};
+    std::string e = build_program_plan(n, specs, mats, n_mats, n_params, precision, P);
+    if (!e.empty()) return set_err(QF_EINVAL, e);
+    return QF_OK;
+}
+
+int qf_plan_describe(int n, int n_ops, const qf_op* ops, const double* mats, int n_mats, int n_params,
+                     int precision, char* buf, size_t buflen, size_t* needed) {
+    ProgramPlan P;
+    int rc = build_plan_from_ops(n, n_ops, ops, mats, n_mats, n_params, precision, P);
+    if (rc) return rc;
+    std::string s = "{\"n\":" + std::to_string(n) + ",\"passes\":{";
+    for (int pi = 0; pi < 2; ++pi) {
+        const PassPlan& pp = pi ? P.bwd : P.fwd;
+        s += std::string(pi ? "," : "") + (pi ? "\"bwd\"" : "\"fwd\"") + ":{\"k\":" + std::to_string(pp.k) +
+             ",\"R\":" + std::to_string(pp.R) + ",\"n_taps\":" + std::to_string(pp.n_taps) + ",\"sweeps\":[";
+        for (size_t si = 0; si < pp.sweeps.size(); ++si) {
+            const DevSweep& sw = pp.sweeps[si];
+            s += std::string(si ? "," : "") + "{\"tile_bits\":[";
+            for (int t = 0; t < sw.k; ++t) s += std::string(t ? "," : "") + std::to_string(sw.tb[t]);
+            s += "],\"tap_begin\":" + std::to_string(sw.tap_begin) + ",\"phases\":[";
+            for (int f = 0; f < sw.n_phases; ++f) {
+                const DevPhase& ph = pp.phases[sw.phase_begin + f];
+                s += std::string(f ? "," : "") + "{\"reg_bits\":[";
+                for (int r = 0; r < pp.R; ++r) s += std::string(r ? "," : "") + std::to_string(sw.tb[(int)ph.reg_tl[r]]);
+                s += "],\"ops\":[";
+                for (int o = ph.op_begin; o < ph.op_end; ++o) {
+                    const DevOp& op = pp.ops[o];
+                    s += std::string(o > ph.op_begin ? "," : "") + "[" + std::to_string(op.kind) + "," +
+                         std::to_string(op.gate) + "," + std::to_string(op.tap) + "]";
+                }
+                s += "]}";
+            }
+            s += "]}";
+        }
+        s += "],\"taps\":[";
+        for (size_t t = 0; t < pp.taps.size(); ++t)
+            s += std::string(t ? "," : "") + "[" + std::to_string(pp.taps[t].slot) + "," + std::to_string(pp.taps[t].coef) + "]";
+        s += "]}";
+    }
+    s += "}}";
+    if (needed) *needed = s.size() + 1;
+    if (buf && buflen > 0) {
+        const size_t m = std::min(buflen - 1, s.size());
+        std::memcpy(buf, s.data(), m);
+        buf[m] = 0;
+        if (m < s.size()) return set_err(QF_EINVAL, "qf_plan_describe: buffer too small");
+    }
+    return QF_OK;
+}
+
+int qf_jit_compile_check(int n, int n_ops, const qf_op* ops, const double* mats, int n_mats, int n_params,
+                         int precision, int* kernels) {
+    ProgramPlan P;
+    int rc = build_plan_from_ops(n, n_ops, ops, mats, n_mats, n_params, precision, P);
+    if (rc) return rc;
+    int count = 0;
+    for (int pi = 0; pi < 2; ++pi) {
+        const PassPlan& pp = pi ? P.bwd : P.fwd;
+        for (size_t si = 0; si < pp.sweeps.size(); ++si) {
+            std::string cubin, err;
+            if (!jit_compile_source(jit_source(P, pp, (int)si, pi == 1), cubin, err))
+                return set_err(QF_ERUNTIME, err);
+            ++count;
+        }
+    }
+    if (kernels) *kernels = count;
+    return QF_OK;
+}
+
 int qf_program_info(const qf_program* p, int* fs, int* bs, int* fk, int* bk) {
     if (!p) return set_err(QF_EINVAL, "null program");
     if (fs) *fs = (int)p->plan.fwd.sweeps.size();

@@ -42,6 +42,7 @@ Geometry geometry(int prec, int n) {
     g.Rf = std::min(g.Rf, g.kf);
     g.Rb = std::min(g.Rb, g.kb);
     g.c = std::min(g.c, n);
+    g.c = std::max(0, std::min(g.c, std::min(g.kf, g.kb) - 2));  // leave room for 2-qubit gates
     return g;
 }
 

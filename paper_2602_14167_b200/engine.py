@@ -90,6 +90,49 @@ def default_context(device: Optional[int] = None) -> Context:
     return _default_ctx[device]
 
 
+def _op_array(ops):
+    arr = (QfOp * max(1, len(ops)))()
+    for i, op in enumerate(ops):
+        kind, q0, q1, slot, coef, offset, mat = op
+        if isinstance(kind, str):
+            kind = _lib.GATE_ID[kind]
+        arr[i] = QfOp(int(kind), int(q0), int(q1), int(slot), float(coef), float(offset), int(mat), 0)
+    return arr
+
+
+def _mats_array(mats):
+    if mats is not None and len(mats):
+        m = np.ascontiguousarray(np.asarray(mats, dtype=np.complex128).reshape(-1, 4, 4))
+        return m.view(np.float64).reshape(-1), m.shape[0]
+    return None, 0
+
+
+def describe_plan(n: int, ops: Sequence, n_params: int, precision="c128", mats=None) -> dict:
+    """The fused-sweep schedule of a circuit template (host only, no GPU)."""
+    import json
+
+    lib = _lib.load()
+    arr = _op_array(ops)
+    mv, nm = _mats_array(mats)
+    need = ctypes.c_size_t()
+    check(lib.qf_plan_describe(n, len(ops), arr, dptr(mv), nm, n_params, PRECISIONS[precision], None, 0,
+                               ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib.qf_plan_describe(n, len(ops), arr, dptr(mv), nm, n_params, PRECISIONS[precision], buf, need.value,
+                               ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+def jit_compile_check(n: int, ops: Sequence, n_params: int, precision="c128", mats=None) -> int:
+    """NVRTC-compile every specialised sweep kernel of the template (host only)."""
+    lib = _lib.load()
+    arr = _op_array(ops)
+    mv, nm = _mats_array(mats)
+    k = ctypes.c_int()
+    check(lib.qf_jit_compile_check(n, len(ops), arr, dptr(mv), nm, n_params, PRECISIONS[precision], ctypes.byref(k)))
+    return k.value
+
+
 class Program:
     """A compiled circuit template (qf_program).
 
@@ -101,18 +144,8 @@ class Program:
                  mats: Optional[np.ndarray] = None):
         self.ctx, self.n, self.n_params = ctx, n, n_params
         self.precision = PRECISIONS[precision]
-        arr = (QfOp * max(1, len(ops)))()
-        for i, op in enumerate(ops):
-            kind, q0, q1, slot, coef, offset, mat = op
-            if isinstance(kind, str):
-                kind = _lib.GATE_ID[kind]
-            arr[i] = QfOp(int(kind), int(q0), int(q1), int(slot), float(coef), float(offset), int(mat), 0)
-        if mats is not None and len(mats):
-            m = np.ascontiguousarray(np.asarray(mats, dtype=np.complex128).reshape(-1, 4, 4))
-            mv = m.view(np.float64).reshape(-1)
-            nm = m.shape[0]
-        else:
-            mv, nm = None, 0
+        arr = _op_array(ops)
+        mv, nm = _mats_array(mats)
         self._mats_keepalive = mv
         h = ctypes.c_void_p()
         check(ctx.lib.qf_program_create(ctx.handle, n, len(ops), arr, dptr(mv), nm, n_params,

@@ -478,7 +478,12 @@ def _probe(builder, P: int, values: np.ndarray) -> Circuit:
     return builder(values.copy())
 
 
-def _compile_ansatz(a: AnsatzSpec, precision: str, ctx) -> _eng.Program:
+def ansatz_template(a: AnsatzSpec):
+    """Parameter-slot discovery.  The builder is opaque
+    (std::function in the reference, variational.hpp:16), so it is probed with
+    four parameter vectors: every rotation angle must be coef * theta[slot] +
+    offset for a single slot, with a theta-independent gate structure.
+    Returns (n, ops, mats, initial_state) with ops in qf_op tuple form."""
     a.validate()
     P = a.n_params
     j = np.arange(P, dtype=np.float64)
@@ -493,11 +498,11 @@ def _compile_ansatz(a: AnsatzSpec, precision: str, ctx) -> _eng.Program:
                  "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)")
     _check_qubits(c0)
     slot_of = []
-    ratios = tb / ta
+    ratios = tb / ta if P else np.zeros(0)
     for i, op in enumerate(c0.ops):
         if Gate(op.name) not in (Gate.rx, Gate.ry, Gate.rz, Gate.rzz):
             for c in (ca, cb, cc):
-                _require(np.allclose(c.ops[i].params, op.params, rtol=0, atol=0) and
+                _require(np.array_equal(np.asarray(c.ops[i].params, dtype=float), np.asarray(op.params, dtype=float)) and
                          (op.matrix is None or np.array_equal(c.ops[i].matrix, op.matrix)),
                          "AnsatzSpec: theta feeds a gate without a Pauli generator "
                          "(su4/unitary parameters are not supported on the device path)")
@@ -510,20 +515,22 @@ def _compile_ansatz(a: AnsatzSpec, precision: str, ctx) -> _eng.Program:
             _require(float(cc.ops[i].params[0]) == o, "AnsatzSpec: builder is not affine in theta")
             slot_of.append(None)
             continue
-        _require(da != 0.0, "AnsatzSpec: builder is not affine in theta")
+        _require(da != 0.0 and P > 0, "AnsatzSpec: builder is not affine in theta")
         s = int(np.argmin(np.abs(ratios - db / da)))
         coef = da / ta[s]
         pred = coef * tc[s] + o
         _require(abs(pred - float(cc.ops[i].params[0])) <= 1e-9 * max(1.0, abs(pred)),
                  "AnsatzSpec: builder is not affine in a single theta slot")
-        if coef == 1.0 and o == 0.0:
-            slot_of.append((s, 1.0, 0.0))
-        else:
-            slot_of.append((s, coef, o))
+        slot_of.append((s, coef, o))
     ops, mats = _circuit_ops(c0, slot_of)
-    prog = _eng.Program(ctx, c0.n, ops, P, precision, mats)
-    if c0.initial_state is not None:
-        prog.set_initial_state(c0.initial_state)
+    return c0.n, ops, mats, c0.initial_state
+
+
+def _compile_ansatz(a: AnsatzSpec, precision: str, ctx) -> _eng.Program:
+    n, ops, mats, init = ansatz_template(a)
+    prog = _eng.Program(ctx, n, ops, a.n_params, precision, mats)
+    if init is not None:
+        prog.set_initial_state(init)
     return prog
 
 
