@@ -220,8 +220,9 @@ class Observable:
 def energy_grad_batch(ctx: Context, prog: Program, obs: Observable, thetas: np.ndarray,
                       grads: bool = True):
     """Host-buffer evaluation (qf_energy_grad_batch): returns (E[B], G[B, P] or None)."""
-    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(-1, prog.n_params)
-                              if prog.n_params else np.zeros((len(thetas), 0)))
+    th = np.asarray(thetas, dtype=np.float64)
+    th = np.ascontiguousarray(th.reshape(-1, prog.n_params) if prog.n_params
+                              else np.zeros((th.shape[0] if th.ndim == 2 else 1, 0)))
     B = th.shape[0]
     E = np.empty(B, dtype=np.float64)
     G = np.empty((B, prog.n_params), dtype=np.float64) if grads else None

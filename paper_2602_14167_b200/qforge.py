@@ -580,7 +580,11 @@ def energy_gradient_batch(ansatz: AnsatzSpec, thetas, h: PauliSum, grads: bool =
                           precision: Optional[str] = None):
     """Batched energy + adjoint gradient: (E[B], G[B, P])."""
     ansatz.validate()
-    th = np.asarray(thetas, dtype=np.float64).reshape(-1, ansatz.n_params)
+    th = np.asarray(thetas, dtype=np.float64)
+    if ansatz.n_params == 0:
+        th = th.reshape(th.shape[0] if th.ndim == 2 else 1, 0)
+    else:
+        th = th.reshape(-1, ansatz.n_params)
     ctx = _eng.default_context()
     prog = ansatz.program(precision, ctx)
     _require(h.n == prog.n, "expectation_pauli: size mismatch")
