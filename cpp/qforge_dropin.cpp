@@ -1,0 +1,641 @@
+// qforge_dropin.cpp -- the reference qforge hot-path API (include/qforge/*.hpp)
+// implemented over the C-ABI of the B200 engine (include/qforge_b200.h).
+// Host-only C++: validation and exceptions follow the reference
+// (require() -> std::invalid_argument); every state-vector operation runs on
+// the GPU through libqforge_b200.so.  Reference line citations are relative to
+// /root/reference/proj.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "qforge/circuit.hpp"
+#include "qforge/lattice.hpp"
+#include "qforge/pauli.hpp"
+#include "qforge/variational.hpp"
+#include "qforge_b200.h"
+
+namespace qforge {
+
+// ------------------------------------------------------------------ engine glue
+namespace {
+
+Precision g_prec = Precision::c128;
+std::mutex g_mu;
+
+void check(int rc) {
+    if (rc == QF_OK) return;
+    const std::string msg = qf_last_error();
+    if (rc == QF_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+qf_ctx* ctx() {
+    static qf_ctx* c = nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!c) {
+        const char* e = std::getenv("QF_DEVICE");
+        check(qf_ctx_create(e ? std::atoi(e) : 0, &c));
+    }
+    return c;
+}
+
+struct ProgramHandle {
+    qf_program* p = nullptr;
+    ~ProgramHandle() {
+        if (p) qf_program_destroy(p);
+    }
+};
+
+struct ObservableHandle {
+    qf_observable* o = nullptr;
+    ~ObservableHandle() {
+        if (o) qf_observable_destroy(o);
+    }
+};
+
+struct Template {
+    int n = 0;
+    std::vector<qf_op> ops;
+    std::vector<double> mats;  // [n_mats][4][4][2]
+    std::optional<ComplexVector> init;
+};
+
+void push_matrix(std::vector<double>& mats, const ComplexMatrix& m) {
+    const int d = (int)m.rows();
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            const cplx v = (r < d && c < d) ? m(r, c) : cplx(0.0);
+            mats.push_back(v.real());
+            mats.push_back(v.imag());
+        }
+}
+
+bool is_rotation(Gate g) { return g == Gate::rx || g == Gate::ry || g == Gate::rz || g == Gate::rzz; }
+
+// Circuit -> qf ops; slot_of[i] = {slot, coef, offset} for rotations fed by theta
+struct SlotMap {
+    int slot = -1;
+    double coef = 1.0, offset = 0.0;
+};
+Template circuit_template(const Circuit& c, const std::vector<SlotMap>* slots) {
+    require(c.d == 2, "device path: qubit circuits only (d == 2)");
+    Template t;
+    t.n = c.n;
+    t.init = c.initial_state;
+    for (size_t i = 0; i < c.ops.size(); ++i) {
+        const GateInstruction& op = c.ops[i];
+        qf_op q{};
+        q.kind = (int)op.name;
+        q.q0 = op.wires.at(0);
+        q.q1 = op.wires.size() > 1 ? op.wires[1] : -1;
+        q.slot = -1;
+        q.coef = 1.0;
+        q.offset = 0.0;
+        q.mat = -1;
+        if (op.name == Gate::su4 || op.name == Gate::unitary) {
+            push_matrix(t.mats, gate_matrix(op, 2));
+            q.mat = (int)(t.mats.size() / 32) - 1;
+        } else if (is_rotation(op.name)) {
+            if (slots && (*slots)[i].slot >= 0) {
+                q.slot = (*slots)[i].slot;
+                q.coef = (*slots)[i].coef;
+                q.offset = (*slots)[i].offset;
+            } else {
+                q.offset = op.params.at(0);
+            }
+        } else if (op.name == Gate::csum || op.name == Gate::subspace_ry || op.name == Gate::subspace_rz) {
+            throw std::invalid_argument("gate_matrix: qudit gates are not supported on the qubit device path");
+        }
+        t.ops.push_back(q);
+    }
+    return t;
+}
+
+std::shared_ptr<ProgramHandle> make_program(const Template& t, int n_params) {
+    auto h = std::make_shared<ProgramHandle>();
+    check(qf_program_create(ctx(), t.n, (int)t.ops.size(), t.ops.data(), t.mats.empty() ? nullptr : t.mats.data(),
+                            (int)(t.mats.size() / 32), n_params, (int)g_prec, &h->p));
+    if (t.init) {
+        require(t.init->size() == (std::int64_t)1 << t.n, "run: initial state size mismatch");
+        check(qf_program_set_initial_state(h->p, reinterpret_cast<const double*>(t.init->data())));
+    }
+    return h;
+}
+
+qf_observable* observable(const PauliSum& h) {
+    struct Cache {
+        std::shared_ptr<ObservableHandle> obs;
+        size_t terms = 0;
+    };
+    auto cache = std::static_pointer_cast<Cache>(h.device_cache);
+    if (!cache || cache->terms != h.terms.size()) {
+        cache = std::make_shared<Cache>();
+        std::vector<int8_t> codes;
+        std::vector<double> wr, wi;
+        for (const auto& t : h.terms) {
+            for (int c : t.codes) codes.push_back((int8_t)c);
+            wr.push_back(t.weight.real());
+            wi.push_back(t.weight.imag());
+        }
+        cache->obs = std::make_shared<ObservableHandle>();
+        check(qf_observable_create(ctx(), h.n, (int)h.terms.size(), codes.data(), wr.data(), wi.data(),
+                                   &cache->obs->o));
+        cache->terms = h.terms.size();
+        h.device_cache = cache;
+    }
+    return cache->obs->o;
+}
+
+// 4x4 (or 2x2) complex matrix exponential: scaling and squaring + Taylor
+ComplexMatrix expm_small(const ComplexMatrix& a) {
+    const int d = (int)a.rows();
+    double nrm = 0;
+    for (int r = 0; r < d; ++r) {
+        double s = 0;
+        for (int c = 0; c < d; ++c) s += std::abs(a(r, c));
+        nrm = std::max(nrm, s);
+    }
+    int sq = std::max(0, (int)std::ceil(std::log2(std::max(nrm, 1e-300))) + 1);
+    ComplexMatrix b = a * cplx(std::ldexp(1.0, -sq));
+    ComplexMatrix res = ComplexMatrix::Identity(d, d), term = ComplexMatrix::Identity(d, d);
+    for (int k = 1; k <= 20; ++k) {
+        term = term * b * cplx(1.0 / k);
+        res = res + term;
+    }
+    for (int i = 0; i < sq; ++i) res = res * res;
+    return res;
+}
+
+}  // namespace
+
+void set_device_precision(Precision p) { g_prec = p; }
+Precision device_precision() { return g_prec; }
+
+// ------------------------------------------------------------------ circuits
+std::string gate_name(Gate g) {
+    static const char* names[] = {"h", "x", "y", "z", "s", "rx", "ry", "rz", "rzz", "cx", "cz", "su4",
+                                  "csum", "subspace_ry", "subspace_rz", "unitary"};
+    const int i = (int)g;
+    return (i >= 0 && i < 16) ? names[i] : "?";
+}
+
+StateVector StateVector::zero_state(int n, int d) {  // circuit.cpp:69-76
+    StateVector psi;
+    psi.n = n;
+    psi.d = d;
+    std::int64_t dim = 1;
+    for (int i = 0; i < n; ++i) dim *= d;
+    psi.amps = ComplexVector::Zero(dim);
+    psi.amps[0] = 1.0;
+    return psi;
+}
+
+Circuit& Circuit::gate(Gate g, std::vector<int> wires, std::vector<double> params) {  // circuit.cpp:178-186
+    for (int w : wires) require(w >= 0 && w < n, "Circuit: wire out of range");
+    for (size_t a = 0; a < wires.size(); ++a)
+        for (size_t b = a + 1; b < wires.size(); ++b) require(wires[a] != wires[b], "Circuit: duplicate wires");
+    for (double p : params) require(std::isfinite(p), "Circuit: non-finite parameter");
+    ops.push_back({g, std::move(wires), std::move(params), {}});
+    return *this;
+}
+
+Circuit& Circuit::su4(int a, int b, const std::vector<double>& theta) {  // circuit.cpp:188-191
+    require(theta.size() == 15, "su4: needs 15 parameters");
+    return gate(Gate::su4, {a, b}, theta);
+}
+
+Circuit& Circuit::unitary(std::vector<int> wires, const ComplexMatrix& u) {  // circuit.cpp:193-200
+    ComplexMatrix check_m = u.adjoint() * u;
+    require((check_m - ComplexMatrix::Identity(u.rows(), u.cols())).cwiseAbs().maxCoeff() < 1e-10,
+            "unitary: matrix is not unitary");
+    gate(Gate::unitary, wires, {});
+    ops.back().matrix = u;
+    return *this;
+}
+
+ComplexMatrix gate_matrix(const GateInstruction& instr, int d) {  // circuit.cpp:202-302 (qubit gates)
+    require(d == 2, "gate_matrix: qubit-only gate in a qudit circuit");
+    const double isq = 1.0 / std::sqrt(2.0);
+    const cplx I(0.0, 1.0);
+    auto m2 = [](cplx a, cplx b, cplx c, cplx e) { return (ComplexMatrix(2, 2) << a, b, c, e).finished(); };
+    switch (instr.name) {
+        case Gate::h: return m2(isq, isq, isq, -isq);
+        case Gate::x: return m2(0, 1, 1, 0);
+        case Gate::y: return m2(0, -I, I, 0);
+        case Gate::z: return m2(1, 0, 0, -1);
+        case Gate::s: return m2(1, 0, 0, I);
+        case Gate::rx: {
+            const double t = instr.params.at(0);
+            const cplx c = std::cos(0.5 * t), s = cplx(0.0, -std::sin(0.5 * t));
+            return m2(c, s, s, c);
+        }
+        case Gate::ry: {
+            const double t = instr.params.at(0), c = std::cos(0.5 * t), s = std::sin(0.5 * t);
+            return m2(c, -s, s, c);
+        }
+        case Gate::rz: {
+            const double t = instr.params.at(0);
+            return m2(std::polar(1.0, -0.5 * t), 0, 0, std::polar(1.0, 0.5 * t));
+        }
+        case Gate::rzz: {
+            const double t = instr.params.at(0);
+            ComplexMatrix m = ComplexMatrix::Zero(4, 4);
+            const cplx em = std::polar(1.0, -0.5 * t), ep = std::polar(1.0, 0.5 * t);
+            m(0, 0) = em; m(1, 1) = ep; m(2, 2) = ep; m(3, 3) = em;
+            return m;
+        }
+        case Gate::cx: {
+            ComplexMatrix m = ComplexMatrix::Zero(4, 4);
+            m(0, 0) = m(1, 1) = m(2, 3) = m(3, 2) = 1.0;
+            return m;
+        }
+        case Gate::cz: {
+            ComplexMatrix m = ComplexMatrix::Identity(4, 4);
+            m(3, 3) = -1.0;
+            return m;
+        }
+        case Gate::su4: {  // exp(-i/2 sum theta_k P_k), lexicographic words without (0,0)
+            require(instr.params.size() == 15, "su4: needs 15 parameters");
+            const ComplexMatrix single[4] = {ComplexMatrix::Identity(2, 2), m2(0, 1, 1, 0), m2(0, -I, I, 0),
+                                             m2(1, 0, 0, -1)};
+            ComplexMatrix gen = ComplexMatrix::Zero(4, 4);
+            int k = 0;
+            for (int a = 0; a < 4; ++a)
+                for (int b = 0; b < 4; ++b) {
+                    if (a == 0 && b == 0) continue;
+                    for (int r = 0; r < 4; ++r)
+                        for (int c = 0; c < 4; ++c)
+                            gen(r, c) += instr.params[k] * single[a](r >> 1, c >> 1) * single[b](r & 1, c & 1);
+                    ++k;
+                }
+            return expm_small(gen * cplx(0.0, -0.5));
+        }
+        case Gate::unitary: return instr.matrix;
+        default: break;
+    }
+    throw std::invalid_argument("gate_matrix: qudit gates are not supported on the qubit device path");
+}
+
+StateVector run(const Circuit& c, std::size_t memory_guard_log2) {  // circuit.cpp:304-317
+    require(std::pow((double)c.d, c.n) <= std::pow(2.0, (double)memory_guard_log2),
+            "run: state dimension exceeds memory guard");
+    Template t = circuit_template(c, nullptr);
+    auto prog = make_program(t, 0);
+    StateVector psi;
+    psi.n = c.n;
+    psi.d = c.d;
+    psi.amps = ComplexVector::Zero((std::int64_t)1 << c.n);
+    check(qf_run_state(ctx(), prog->p, nullptr, (int)memory_guard_log2, reinterpret_cast<double*>(psi.amps.data())));
+    return psi;
+}
+
+void apply_local_unitary(StateVector& psi, const ComplexMatrix& u, const std::vector<int>& wires) {
+    const int k = (int)wires.size();
+    require(u.rows() == ((std::int64_t)1 << k) && u.cols() == ((std::int64_t)1 << k),
+            "apply_local_unitary: wrong gate size");
+    for (int w : wires) require(w >= 0 && w < psi.n, "apply_local_unitary: wire out of range");
+    require(k == 1 || k == 2, "apply_local_unitary: the device path supports 1- and 2-qubit gates");
+    Circuit c(psi.n);
+    c.ops.push_back({Gate::unitary, wires, {}, u});
+    c.initial_state = psi.amps;
+    auto prog = make_program(circuit_template(c, nullptr), 0);
+    check(qf_run_state(ctx(), prog->p, nullptr, 64, reinterpret_cast<double*>(psi.amps.data())));
+}
+
+cplx expectation_pauli(const StateVector& psi, const PauliSum& obs) {  // circuit.cpp:319-347
+    require(psi.d == 2, "expectation_pauli: qubits only");
+    require(obs.n == psi.n, "expectation_pauli: size mismatch");
+    Circuit c(psi.n);
+    c.initial_state = psi.amps;
+    auto prog = make_program(circuit_template(c, nullptr), 0);
+    double out[2];
+    check(qf_expectation(ctx(), prog->p, observable(obs), nullptr, out));
+    return cplx(out[0], out[1]);
+}
+
+// ------------------------------------------------------------------ lattice / Pauli sums
+Lattice build_lattice(LatticeKind kind, const std::vector<int>& size, const std::vector<bool>& pbc,
+                      double lattice_constant, int neighbor_order) {  // lattice.cpp:89-170 (chain)
+    require(kind == LatticeKind::chain, "build_lattice: only the chain lattice is on the device hot path");
+    require(lattice_constant > 0.0, "build_lattice: lattice_constant must be > 0");
+    require(size.size() == 1 && pbc.size() == 1, "build_lattice: wrong size rank");
+    const int n = size[0];
+    require(n >= 1, "build_lattice: size entries must be >= 1");
+    if (pbc[0]) require(n >= 3, "build_lattice: periodic dimension needs extent >= 3");
+    Lattice l;
+    l.kind = kind;
+    l.lattice_constant = lattice_constant;
+    l.n_sites = n;
+    struct P { double d; int i, j; };
+    std::vector<P> pairs;
+    for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+            double d = std::abs((double)(i - j)) * lattice_constant;
+            if (pbc[0])
+                for (int m = -1; m <= 1; ++m) d = std::min(d, std::abs((double)(i - j + m * n)) * lattice_constant);
+            pairs.push_back({d, i, j});
+        }
+    std::sort(pairs.begin(), pairs.end(), [](const P& a, const P& b) {
+        if (a.d != b.d) return a.d < b.d;
+        if (a.i != b.i) return a.i < b.i;
+        return a.j < b.j;
+    });
+    int order = 0;
+    double shell = -1.0;
+    for (const P& p : pairs) {
+        if (p.d <= 0.0) continue;
+        if (shell < 0.0 || p.d > shell * (1.0 + 1e-6)) {
+            ++order;
+            shell = p.d;
+        }
+        if (order > neighbor_order) break;
+        l.edges_by_order[order].push_back({p.i, p.j});
+    }
+    return l;
+}
+
+void PauliSum::add(cplx weight, const std::vector<int>& codes) {  // pauli.cpp:12-18
+    require(static_cast<int>(codes.size()) == n, "PauliSum::add: wrong code length");
+    for (int c : codes) require(c >= 0 && c <= 3, "PauliSum::add: code out of range");
+    require(std::isfinite(weight.real()) && std::isfinite(weight.imag()), "PauliSum::add: non-finite weight");
+    terms.push_back({weight, codes});
+}
+
+void PauliSum::add_word(cplx weight, const std::vector<std::pair<int, int>>& site_codes) {  // pauli.cpp:20-27
+    std::vector<int> codes(n, 0);
+    for (const auto& [site, code] : site_codes) {
+        require(site >= 0 && site < n, "PauliSum::add_word: site out of range");
+        codes[site] = code;
+    }
+    add(weight, codes);
+}
+
+PauliSum tfim_terms(const Lattice& l, double g) {  // pauli.cpp:181-189
+    PauliSum h;
+    h.n = static_cast<int>(l.num_sites());
+    auto it = l.edges_by_order.find(1);
+    require(it != l.edges_by_order.end(), "tfim_terms: lattice has no order-1 edges");
+    for (const auto& [i, j] : it->second) h.add_word(-1.0, {{i, 3}, {j, 3}});
+    for (int i = 0; i < h.n; ++i) h.add_word(-g, {{i, 1}});
+    return h;
+}
+
+PauliSum heisenberg_terms(const Lattice& l, double jx, double jy, double jz) {  // pauli.cpp:191-203
+    PauliSum h;
+    h.n = static_cast<int>(l.num_sites());
+    auto it = l.edges_by_order.find(1);
+    require(it != l.edges_by_order.end(), "heisenberg_terms: lattice has no order-1 edges");
+    const double js[3] = {jx, jy, jz};
+    for (const auto& [i, j] : it->second)
+        for (int axis = 0; axis < 3; ++axis)
+            if (js[axis] != 0.0) h.add_word(js[axis], {{i, axis + 1}, {j, axis + 1}});
+    return h;
+}
+
+// ------------------------------------------------------------------ variational
+void AnsatzSpec::validate() const {  // variational.cpp:11-16
+    require(n_params >= 0, "AnsatzSpec: negative parameter count");
+    require(static_cast<bool>(builder), "AnsatzSpec: missing builder");
+    require(shift_eligible.size() == static_cast<std::size_t>(n_params),
+            "AnsatzSpec: eligibility tags do not match parameter count");
+}
+
+AnsatzSpec tfim_chain_ansatz(int n, int layers) {  // variational.cpp:18-36
+    require(n >= 2, "tfim_chain_ansatz: n must be >= 2");
+    require(layers >= 1, "tfim_chain_ansatz: layers must be >= 1");
+    AnsatzSpec a;
+    a.n_params = layers * (2 * n - 1);
+    a.shift_eligible.assign(a.n_params, true);
+    a.builder = [n, layers](const RealVector& theta) {
+        Circuit c(n);
+        for (int q = 0; q < n; ++q) c.h(q);
+        int k = 0;
+        for (int l = 0; l < layers; ++l) {
+            for (int i = 0; i < n; ++i) c.rx(i, theta[k++]);
+            for (int i = 0; i + 1 < n; ++i) c.rzz(i, i + 1, theta[k++]);
+        }
+        return c;
+    };
+    return a;
+}
+
+AnsatzSpec hea_ansatz(int n, int layers) {
+    require(n >= 2 && layers >= 1, "hea_ansatz: n >= 2 and layers >= 1");
+    AnsatzSpec a;
+    a.n_params = 2 * n * layers;
+    a.shift_eligible.assign(a.n_params, true);
+    a.builder = [n, layers](const RealVector& theta) {
+        Circuit c(n);
+        int k = 0;
+        for (int l = 0; l < layers; ++l) {
+            for (int q = 0; q < n; ++q) c.ry(q, theta[k++]);
+            for (int q = 0; q < n; ++q) c.rz(q, theta[k++]);
+            for (int q = 0; q + 1 < n; ++q) c.cx(q, q + 1);
+        }
+        return c;
+    };
+    return a;
+}
+
+namespace {
+
+// Parameter-slot discovery: probe the opaque builder.
+std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
+    struct Cache {
+        std::map<int, std::shared_ptr<ProgramHandle>> by_prec;
+        int n = 0;
+    };
+    auto cache = std::static_pointer_cast<Cache>(a.device_cache);
+    if (cache) {
+        auto f = cache->by_prec.find((int)g_prec);
+        if (f != cache->by_prec.end()) return f->second;
+    }
+    a.validate();
+    const int P = a.n_params;
+    RealVector t0 = RealVector::Zero(P), ta(P), tb(P), tc(P);
+    for (int j = 0; j < P; ++j) {
+        ta[j] = 1.0 + 1e-3 * j + 0.137;
+        tb[j] = ta[j] * (2.0 + 1e-3 * j);
+        tc[j] = std::cos(3.7 * j + 0.3) * 2.1 + 0.05;
+    }
+    const Circuit c0 = a.builder(t0), ca = a.builder(ta), cb = a.builder(tb), cc = a.builder(tc);
+    for (const Circuit* c : {&ca, &cb, &cc}) {
+        bool same = c->n == c0.n && c->ops.size() == c0.ops.size();
+        for (size_t i = 0; same && i < c0.ops.size(); ++i)
+            same = c->ops[i].name == c0.ops[i].name && c->ops[i].wires == c0.ops[i].wires;
+        require(same, "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)");
+    }
+    std::vector<SlotMap> slots(c0.ops.size());
+    for (size_t i = 0; i < c0.ops.size(); ++i) {
+        const GateInstruction& op = c0.ops[i];
+        if (!is_rotation(op.name)) {
+            for (const Circuit* c : {&ca, &cb, &cc})
+                require(c->ops[i].params == op.params,
+                        "AnsatzSpec: theta feeds a gate without a Pauli generator "
+                        "(su4/unitary parameters are not supported on the device path)");
+            continue;
+        }
+        const double o = op.params.at(0);
+        const double da = ca.ops[i].params.at(0) - o, db = cb.ops[i].params.at(0) - o;
+        if (da == 0.0 && db == 0.0) {
+            require(cc.ops[i].params.at(0) == o, "AnsatzSpec: builder is not affine in theta");
+            continue;
+        }
+        require(da != 0.0 && P > 0, "AnsatzSpec: builder is not affine in theta");
+        int s = 0;
+        double best = INFINITY;
+        for (int j = 0; j < P; ++j) {
+            const double d = std::abs(tb[j] / ta[j] - db / da);
+            if (d < best) {
+                best = d;
+                s = j;
+            }
+        }
+        const double coef = da / ta[s];
+        const double pred = coef * tc[s] + o;
+        require(std::abs(pred - cc.ops[i].params.at(0)) <= 1e-9 * std::max(1.0, std::abs(pred)),
+                "AnsatzSpec: builder is not affine in a single theta slot");
+        slots[i] = {s, coef, o};
+    }
+    auto prog = make_program(circuit_template(c0, &slots), P);
+    if (!cache) {
+        cache = std::make_shared<Cache>();
+        a.device_cache = cache;
+    }
+    cache->n = c0.n;
+    cache->by_prec[(int)g_prec] = prog;
+    return prog;
+}
+
+void batch_eval(const AnsatzSpec& a, const std::vector<double>& flat, int batch, const PauliSum& h,
+                std::vector<double>& E, std::vector<double>* G) {
+    auto prog = ansatz_program(a);
+    E.assign(batch, 0.0);
+    if (G) G->assign((size_t)batch * a.n_params, 0.0);
+    if (batch == 0) return;
+    check(qf_energy_grad_batch(ctx(), prog->p, observable(h), batch, flat.data(), E.data(), G ? G->data() : nullptr));
+}
+
+}  // namespace
+
+double energy(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum& h) {  // variational.cpp:38-43
+    ansatz.validate();
+    require(theta.size() == ansatz.n_params, "energy: parameter count mismatch");
+    std::vector<double> flat(theta.data(), theta.data() + theta.size()), E;
+    batch_eval(ansatz, flat, 1, h, E, nullptr);
+    return E[0];
+}
+
+RealVector gradient(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum& h, GradMode mode,
+                    double fd_step, int /*workers: results never depend on it*/) {  // variational.cpp:54-81
+    ansatz.validate();
+    require(theta.size() == ansatz.n_params, "gradient: parameter count mismatch");
+    const int P = ansatz.n_params;
+    RealVector grad(P);
+    if (mode == GradMode::adjoint) {
+        std::vector<double> flat(theta.data(), theta.data() + P), E, G;
+        batch_eval(ansatz, flat, 1, h, E, &G);
+        for (int j = 0; j < P; ++j) grad[j] = G[j];
+        return grad;
+    }
+    if (mode == GradMode::parameter_shift) {
+        for (int j = 0; j < P; ++j)
+            require(ansatz.shift_eligible[j], "gradient: parameter not shift-eligible, use finite_diff");
+    } else {
+        require(fd_step > 0.0, "gradient: finite-diff step must be positive");
+    }
+    const double shift = mode == GradMode::parameter_shift ? M_PI / 2.0 : fd_step;
+    const double denom = mode == GradMode::parameter_shift ? 2.0 : 2.0 * fd_step;
+    std::vector<double> flat((size_t)2 * P * P), E;  // all 2P shifted energies in one device batch
+    for (int j = 0; j < P; ++j)
+        for (int s = 0; s < 2; ++s) {
+            double* row = flat.data() + ((size_t)2 * j + s) * P;
+            for (int i = 0; i < P; ++i) row[i] = theta[i];
+            row[j] = theta[j] + (s == 0 ? shift : -shift);
+        }
+    batch_eval(ansatz, flat, 2 * P, h, E, nullptr);
+    for (int j = 0; j < P; ++j) grad[j] = (E[2 * j] - E[2 * j + 1]) / denom;
+    return grad;
+}
+
+void energy_gradient_batch(const AnsatzSpec& ansatz, const std::vector<RealVector>& thetas, const PauliSum& h,
+                           std::vector<double>& energies, std::vector<RealVector>* grads) {
+    ansatz.validate();
+    const int P = ansatz.n_params, B = (int)thetas.size();
+    std::vector<double> flat((size_t)B * P), G;
+    for (int b = 0; b < B; ++b) {
+        require(thetas[b].size() == P, "energy: parameter count mismatch");
+        std::memcpy(flat.data() + (size_t)b * P, thetas[b].data(), sizeof(double) * P);
+    }
+    batch_eval(ansatz, flat, B, h, energies, grads ? &G : nullptr);
+    if (grads) {
+        grads->assign(B, RealVector(P));
+        for (int b = 0; b < B; ++b)
+            for (int j = 0; j < P; ++j) (*grads)[b][j] = G[(size_t)b * P + j];
+    }
+}
+
+void adam_step(AdamState& state, RealVector& theta, const RealVector& grad, double lr, double beta1, double beta2,
+               double eps) {  // variational.cpp:83-101
+    require(theta.size() == grad.size(), "adam_step: shape mismatch");
+    if (state.t == 0) {
+        state.m = RealVector::Zero(theta.size());
+        state.v = RealVector::Zero(theta.size());
+    }
+    require(state.m.size() == theta.size(), "adam_step: state shape mismatch");
+    ++state.t;
+    state.m = beta1 * state.m + (1.0 - beta1) * grad;
+    state.v = beta2 * state.v + (1.0 - beta2) * grad.cwiseProduct(grad);
+    const double c1 = 1.0 - std::pow(beta1, state.t);
+    const double c2 = 1.0 - std::pow(beta2, state.t);
+    for (std::int64_t i = 0; i < theta.size(); ++i) {
+        const double mhat = state.m[i] / c1;
+        const double vhat = state.v[i] / c2;
+        theta[i] -= lr * mhat / (std::sqrt(vhat) + eps);
+    }
+}
+
+VqeResult vqe_run(const AnsatzSpec& ansatz, const std::vector<RealVector>& theta0_batch, const PauliSum& h, int steps,
+                  double lr, GradMode grad_mode, int /*workers*/) {  // variational.cpp:103-143
+    ansatz.validate();
+    require(!theta0_batch.empty(), "vqe_run: empty batch");
+    require(steps >= 1, "vqe_run: steps must be >= 1");
+    const int B = (int)theta0_batch.size();
+    VqeResult out;
+    out.traces.assign(B, {});
+    std::vector<RealVector> th = theta0_batch;
+    std::vector<AdamState> adam(B);
+    for (int s = 0; s < steps; ++s) {  // the whole batch advances together: one device call per step
+        std::vector<double> E;
+        std::vector<RealVector> G;
+        if (grad_mode == GradMode::adjoint) {
+            energy_gradient_batch(ansatz, th, h, E, &G);
+        } else {
+            energy_gradient_batch(ansatz, th, h, E, nullptr);
+            G.resize(B);
+            for (int b = 0; b < B; ++b) G[b] = gradient(ansatz, th[b], h, grad_mode, 1e-5, 1);
+        }
+        for (int b = 0; b < B; ++b) {
+            out.traces[b].push_back(E[b]);
+            adam_step(adam[b], th[b], G[b], lr);
+        }
+    }
+    std::vector<double> E;
+    energy_gradient_batch(ansatz, th, h, E, nullptr);
+    out.best_energy = INFINITY;
+    for (int b = 0; b < B; ++b) {
+        out.traces[b].push_back(E[b]);
+        if (E[b] < out.best_energy) {
+            out.best_energy = E[b];
+            out.best_index = b;
+        }
+    }
+    out.final_thetas = th;
+    return out;
+}
+
+}  // namespace qforge
