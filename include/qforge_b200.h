@@ -100,7 +100,9 @@ int qf_ctx_destroy(qf_ctx* ctx);
 int qf_ctx_set_memory_budget(qf_ctx* ctx, size_t bytes);
 /* Multi-GPU: one process per GPU.  Rank 0 calls qf_nccl_unique_id, ships the
  * 128 bytes to the other ranks (e.g. torch.distributed broadcast), then every
- * rank calls qf_ctx_set_comm.  world == 1 detaches. */
+ * rank calls qf_ctx_set_comm.  world == 1 with an all-zero id detaches; world == 1
+ * with a real id builds a single-rank communicator (exercises the collective
+ * path on one GPU). */
 int qf_nccl_unique_id(uint8_t out[128]);
 int qf_ctx_set_comm(qf_ctx* ctx, int rank, int world, const uint8_t unique_id[128]);
 /* Stream (cudaStream_t as void*) that *_device calls are ordered on. */

@@ -140,6 +140,7 @@ struct qf_program {
     DevBuf gates, cmats;
     DevPass fwd, bwd;
     DevBuf slot_ptr, slot_taps, slot_coef;
+    DevBuf goff_fwd, goff_bwd;  // per op: offset of its matrix in the per-state table (-1: none)
     DevBuf init;  // optional initial state (RT)
     bool has_init = false;
     // NVRTC-specialised sweep kernels (jit.hpp); the AOT interpreter is the fallback
@@ -169,7 +170,7 @@ struct qf_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     size_t budget = 0;
-    DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init;
+    DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init, gmat;
     HostBuf pin;
     // NCCL
     NcclComm comm = nullptr;
@@ -262,6 +263,19 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     sa.batch_offset = b0;
     sa.gates = (const DevGate*)prog->gates.p;
     sa.cmats = (const double*)prog->cmats.p;
+    sa.gmat = ctx->gmat.p;
+    sa.gmat_stride = P.fwd.total_mat + P.bwd.total_mat;
+    sa.gmat_pass_base = 0;
+    QF_CUDA(launch_mats(prec, false, (const DevOp*)prog->fwd.ops.p, (const int*)prog->goff_fwd.p,
+                        (int)P.fwd.ops.size(), sa.gates, sa.cmats, d_thetas, P_, b0, ctx->gmat.p, sa.gmat_stride, 0,
+                        bc, s));
+    ctx->launches++;
+    if (grads) {
+        QF_CUDA(launch_mats(prec, true, (const DevOp*)prog->bwd.ops.p, (const int*)prog->goff_bwd.p,
+                            (int)P.bwd.ops.size(), sa.gates, sa.cmats, d_thetas, P_, b0, ctx->gmat.p,
+                            sa.gmat_stride, P.fwd.total_mat, bc, s));
+        ctx->launches++;
+    }
     const bool first_from_zero = !prog->has_init && !P.fwd.sweeps.empty();
     if (prog->has_init) {
         QF_CUDA(launch_init_state(prec, ctx->psi.p, prog->init.p, n, bc, s));
@@ -336,6 +350,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         sa.from_zero = 0;
         sa.tap_part = (double*)ctx->tap_part.p;
         sa.n_taps_total = nt;
+        sa.gmat_pass_base = P.fwd.total_mat;
         for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) {
             sa.sw = P.bwd.sweeps[i];
             if (prog->use_jit)
@@ -376,7 +391,7 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     const Geometry geo = geometry(prec, n);
     ObsDev* od = &obs->dev[prec];
     int rc;
-    if (term_shard && ctx->world > 1) {
+    if (term_shard && ctx->comm) {
         const int T = (int)obs->w_re.size();
         const int t0 = (int)((long long)T * ctx->rank / ctx->world);
         const int t1 = (int)((long long)T * (ctx->rank + 1) / ctx->world);
@@ -400,7 +415,7 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     const size_t tiles_b = size_t(1) << (n - P.bwd.k);
     const size_t tiles_h = size_t(1) << (n - geo.kh);
     const size_t per_entry = N * vs * (grads ? 2 : 1) + (grads ? (size_t)nt * tiles_b * 8 + (size_t)nt * 8 : 0) +
-                             tiles_h * 8;
+                             tiles_h * 8 + (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs;
     size_t budget = ctx->budget;
     if (!budget) {
         size_t fr = 0, tot = 0;
@@ -420,6 +435,7 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
         QF_CUDA(ctx->tapsum.reserve(std::max<size_t>(16, bc * (size_t)nt * 8)));
     }
     QF_CUDA(ctx->epart.reserve(bc * tiles_h * 8));
+    QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, bc * (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs)));
     if (!prog->has_init && P.fwd.sweeps.empty()) {
         if (ctx->zero_init.cap < N * vs) {
             QF_CUDA(ctx->zero_init.reserve(N * vs));
@@ -484,7 +500,8 @@ int qf_ctx_destroy(qf_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.commDestroy(c->comm);
-    for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init})
+    for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
+                      &c->gmat})
         b->release();
     c->pin.release();
     for (auto& ev : c->ev_pool) cudaEventDestroy(ev);
@@ -522,7 +539,9 @@ int qf_ctx_set_comm(qf_ctx* c, int rank, int world, const uint8_t unique_id[128]
     }
     c->rank = rank;
     c->world = world;
-    if (world == 1) return QF_OK;
+    bool zero_id = true;
+    for (int i = 0; i < 128 && unique_id; ++i) zero_id &= unique_id[i] == 0;
+    if (world == 1 && (zero_id || !unique_id)) return QF_OK;  // detach
     std::string why;
     if (!g_nccl.load(why)) return set_err(QF_ENCCL, why);
     QF_CUDA(cudaSetDevice(c->device));
@@ -579,6 +598,14 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
         taps[fill[tp.slot]] = (int)t;
         coef[fill[tp.slot]++] = tp.coef;
     }
+    for (int pi = 0; pi < 2; ++pi) {
+        const PassPlan& pp = pi ? p->plan.bwd : p->plan.fwd;
+        std::vector<int> goff(pp.ops.size(), -1);
+        for (const DevSweep& sw : pp.sweeps)
+            for (int o = sw.op_begin; o < sw.op_end; ++o)
+                if (pp.ops[o].moff >= 0) goff[o] = sw.mbase + pp.ops[o].moff;
+        if ((ce = upload(pi ? p->goff_bwd : p->goff_fwd, goff, s)) != cudaSuccess) return fail(ce);
+    }
     if ((ce = upload(p->slot_ptr, ptr, s)) != cudaSuccess) return fail(ce);
     if ((ce = upload(p->slot_taps, taps, s)) != cudaSuccess) return fail(ce);
     if ((ce = upload(p->slot_coef, coef, s)) != cudaSuccess) return fail(ce);
@@ -629,7 +656,7 @@ int qf_program_destroy(qf_program* p) {
     cudaSetDevice(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
     for (DevBuf* b : {&p->gates, &p->cmats, &p->fwd.phases, &p->fwd.ops, &p->bwd.phases, &p->bwd.ops,
-                      &p->slot_ptr, &p->slot_taps, &p->slot_coef, &p->init})
+                      &p->slot_ptr, &p->slot_taps, &p->slot_coef, &p->goff_fwd, &p->goff_bwd, &p->init})
         b->release();
     delete p;
     return QF_OK;
@@ -802,7 +829,7 @@ int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observab
     QF_CUDA(ctx->out.reserve(out_n * 8));
     double* dE = (double*)ctx->out.p;
     double* dG = grads ? dE + batch : nullptr;
-    const bool sharded = ctx->world > 1 && ctx->comm;
+    const bool sharded = ctx->comm != nullptr;
     const bool term_shard = sharded && obs->term_shard;
     if (sharded && !term_shard) {
         // batch sharding: rank r owns rows [b0, b1); zero elsewhere; one all-reduce (exact: x + 0 = x)
@@ -879,6 +906,13 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
     sa.n = n;
     sa.gates = (const DevGate*)prog->gates.p;
     sa.cmats = (const double*)prog->cmats.p;
+    QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs)));
+    sa.gmat = ctx->gmat.p;
+    sa.gmat_stride = P.fwd.total_mat + P.bwd.total_mat;
+    sa.gmat_pass_base = 0;
+    QF_CUDA(launch_mats(P.prec, false, (const DevOp*)prog->fwd.ops.p, (const int*)prog->goff_fwd.p,
+                        (int)P.fwd.ops.size(), sa.gates, sa.cmats, sa.theta, P.n_params, 0, ctx->gmat.p,
+                        sa.gmat_stride, 0, 1, s));
     sa.phases = (const DevPhase*)prog->fwd.phases.p;
     sa.ops = (const DevOp*)prog->fwd.ops.p;
     for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {

@@ -62,21 +62,29 @@ struct BitSrc {
 
 }  // namespace
 
+// Gradient taps are staged per thread in shared memory ([slots][T] reals) and
+// reduced in batches at fixed points (no per-tap shuffle chains).
+int jit_tap_stage(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
+    if (!bwd) return 0;
+    const int cap = P.prec == QF_C128 ? 16 : 32;
+    return std::min(pass.sweeps[si].n_taps, cap);
+}
+
 size_t jit_smem_bytes(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
     const DevSweep& sw = pass.sweeps[si];
     const size_t vs = P.prec == QF_C128 ? 16 : 8;
     const int T = 1 << (sw.k - sw.R);
     const int nwarps = (T + 31) / 32;
+    (void)nwarps;
     size_t b = ((size_t)1 << sw.k) * vs * (bwd ? 2 : 1);
     b += (size_t)((sw.n_mat + 1) & ~1) * vs;
-    b += (size_t)sw.n_taps * nwarps * 8;
+    b += (size_t)jit_tap_stage(P, pass, si, bwd) * T * (vs / 2);
     return b;
 }
 
 std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
     const DevSweep& sw = pass.sweeps[si];
     const int k = sw.k, R = sw.R, NR = 1 << R, T = 1 << (k - R);
-    const int nwarps = (T + 31) / 32;
     const bool dbl = P.prec == QF_C128;
     const int W = dbl ? 3 : 4;
     const char* Vt = dbl ? "double2" : "float2";
@@ -103,8 +111,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     o("  V* tile = reinterpret_cast<V*>(smem_raw);");
     o("  V* tile2 = tile + %u;", bwd ? (1u << k) : 0u);
     o("  V* smat = tile2 + %u;", 1u << k);
-    o("  double* stap = reinterpret_cast<double*>(smat + %d);", (sw.n_mat + 1) & ~1);
-    o("  (void)tile; (void)tile2; (void)stap;");
+    const int S = jit_tap_stage(P, pass, si, bwd);
+    o("  RT* stg = reinterpret_cast<RT*>(smat + %d);", (sw.n_mat + 1) & ~1);
+    o("  (void)tile; (void)tile2; (void)stg;");
     o("  const uint32_t tid = threadIdx.x, tile_id = blockIdx.x; const int b = blockIdx.y;");
     o("  V* st = reinterpret_cast<V*>(a.psi) + (size_t)b * %zuull;", (size_t)1 << P.n);
     if (bwd) o("  V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", (size_t)1 << P.n);
@@ -167,13 +176,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 o("  V v%d = st[g_ld | %uu]; V w%d = lm[g_ld | %uu];", j, joff[j], j, joff[j]);
         }
     }
-    o("  {");
-    o("    const double* th = a.theta + (size_t)(b + a.batch_offset) * a.P;");
-    o("    for (int op_i = %d + (int)tid; op_i < %d; op_i += %d) {", sw.op_begin, sw.op_end, T);
-    o("      const DevOp op = a.ops[op_i];");
-    o("      if (op.moff >= 0) build_matrix<V, %s>(op, a.gates[op.gate], th, a.cmats, smat + op.moff);",
-      bwd ? "true" : "false");
-    o("    }");
+    o("  {  // this sweep's gate matrices (precomputed once per parameter set)");
+    o("    const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + %d;",
+      sw.mbase);
+    o("    for (int i = (int)tid; i < %d; i += %d) smat[i] = gm[i];", sw.n_mat, T);
     o("  }");
     if (!direct_first) {
         for (int j = 0; j < NR; ++j) {
@@ -189,6 +195,15 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     std::vector<const char*> arrs = {"x"};
     if (bwd) arrs.push_back("y");
     int uid = 0;  // unique names inside fused blocks
+    auto emit_flush = [&](int first, int cnt) {
+        o("    __syncthreads();");
+        o("    tap_flush<RT>(stg, %d, %d, a.tap_part + ((size_t)b * a.n_taps_total + %d) * gridDim.x + tile_id, gridDim.x);",
+          cnt, T, sw.tap_begin + first);
+        o("    __syncthreads();");
+    };
+    auto emit_flush_if_full = [&](int tap) {
+        if (tap % S == S - 1) emit_flush(tap - (S - 1), S);
+    };
 
     for (int f = 0; f < nph; ++f) {
         const DevPhase& ph = phase(f);
@@ -280,7 +295,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     if (s0.rb < 0) rt = s0.expr;
                     if (op.kind == DK_TZZ && s1.rb < 0) rt = rt.empty() ? s1.expr : "(" + rt + " ^ " + s1.expr + ")";
                     if (!rt.empty()) o("        if (%s) s = -s;", rt.c_str());
-                    o("        tap_store<RT>(s, stap, %d, %d, %d); }", op.tap, nwarps, T);
+                    o("        stg[%d * %d + tid] = s; }", op.tap % S, T);
+                    emit_flush_if_full(op.tap);
                     continue;
                 }
                 if (op.kind == DK_D1) {
@@ -456,7 +472,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         for (auto pr : pairs(op.rb0))
                             o("      s += recv(y%d, x%d) - recv(y%d, x%d);", pr.second, pr.first, pr.first, pr.second);
                     }
-                    o("      tap_store<RT>(s, stap, %d, %d, %d); }", op.tap, nwarps, T);
+                    o("      stg[%d * %d + tid] = s; }", op.tap % S, T);
+                    emit_flush_if_full(op.tap);
                     break;
                 }
                 default:
@@ -474,7 +491,6 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     o("    st[g_pl | %uu] = x%d;", off, phys[l]);
             }
             o("  }");
-            if (bwd && sw.n_taps > 0) o("  __syncthreads();");
         } else {
             for (int l = 0; l < NR; ++l) {
                 if (bwd)
@@ -501,12 +517,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 o("  st[g_ld | %uu] = v%d_o;", joff[j], j);
         }
     }
-    if (bwd && sw.n_taps > 0) {
-        o("  for (int t = (int)tid; t < %d; t += %d) {", sw.n_taps, T);
-        o("    double s = 0;");
-        o("    for (int w = 0; w < %d; ++w) s += stap[t * %d + w];", nwarps, nwarps);
-        o("    a.tap_part[((size_t)b * a.n_taps_total + %d + t) * gridDim.x + tile_id] = s;", sw.tap_begin);
-        o("  }");
+    if (bwd && sw.n_taps % std::max(S, 1) != 0) {
+        const int rem = sw.n_taps % S;
+        emit_flush(sw.n_taps - rem, rem);
     }
     o("}");
     o("}  // namespace qfb");

@@ -35,6 +35,7 @@ struct JitStats {
 // Source of the specialised kernel for sweep `si` of `pass` (exposed for tests).
 std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd);
 size_t jit_smem_bytes(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd);
+int jit_tap_stage(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd);
 
 // NVRTC compile of one generated source to an sm_100a cubin (no GPU needed).
 bool jit_compile_source(const std::string& src, std::string& cubin, std::string& err);

@@ -62,4 +62,18 @@ template <typename V> __device__ __forceinline__ void jg2(V& a0, V& a1, V& a2, V
     a3 = cfma(m[15], v3, cfma(m[14], v2, cfma(m[13], v1, cmul(m[12], v0))));
 }
 
+// Reduce `cnt` staged taps ([cnt][T] per-thread partials in shared memory) in a
+// fixed order (deterministic) and write one partial per tap: out[t * stride].
+template <typename RT>
+__device__ __forceinline__ void tap_flush(const RT* stg, int cnt, int T, double* out, int stride) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (T + 31) >> 5;
+    const unsigned m = lane_mask(T);
+    for (int t = warp; t < cnt; t += nw) {
+        RT acc = 0;
+        for (int j = lane; j < T; j += 32) acc += stg[t * T + j];
+        for (int o = (T >= 32 ? 16 : T / 2); o > 0; o >>= 1) acc += __shfl_xor_sync(m, acc, o);
+        if (lane == 0) out[(size_t)t * stride] = (double)acc;
+    }
+}
+
 }  // namespace qfb

@@ -121,6 +121,19 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
     }
 }
 
+// gate matrices of every op of one pass, once per parameter set (instead of per CTA)
+template <typename RT, bool ADJ>
+__global__ void mats_kernel(const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
+                            const double* cmats, const double* theta, int P, int batch_offset,
+                            typename CxT<RT>::T* out, int stride, int pass_base) {
+    const int b = blockIdx.y;
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n_ops || goff[o] < 0) return;
+    const DevOp op = ops[o];
+    build_matrix<typename CxT<RT>::T, ADJ>(op, gates[op.gate], theta + (size_t)(b + batch_offset) * P, cmats,
+                                           out + (size_t)b * stride + pass_base + goff[o]);
+}
+
 template <typename RT>
 __global__ void init_state_kernel(typename CxT<RT>::T* psi, const typename CxT<RT>::T* init, size_t N) {
     const size_t b = blockIdx.y;
@@ -235,6 +248,21 @@ static cudaError_t dispatch_hpsi(const HArgs& a, int batch, cudaStream_t s) {
 
 cudaError_t launch_hpsi(int prec, const HArgs& a, int batch, cudaStream_t s) {
     return prec == QF_C128 ? dispatch_hpsi<double>(a, batch, s) : dispatch_hpsi<float>(a, batch, s);
+}
+
+cudaError_t launch_mats(int prec, bool adj, const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
+                        const double* cmats, const double* theta, int P, int batch_offset, void* out, int stride,
+                        int pass_base, int batch, cudaStream_t s) {
+    if (n_ops == 0) return cudaSuccess;
+    dim3 grid((n_ops + 127) / 128, batch);
+    if (prec == QF_C128) {
+        if (adj) mats_kernel<double, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base);
+        else mats_kernel<double, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base);
+    } else {
+        if (adj) mats_kernel<float, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base);
+        else mats_kernel<float, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_init_state(int prec, void* psi, const void* init, int n, int batch, cudaStream_t s) {

@@ -32,6 +32,9 @@ size_t sweep_smem_bytes(int prec, bool bwd, const DevSweep& sw, int max_mat, int
 cudaError_t launch_sweep(int prec, bool bwd, const SweepArgs& a, int batch, int max_mat,
                          int max_taps, cudaStream_t s);
 cudaError_t launch_hpsi(int prec, const HArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_mats(int prec, bool adj, const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
+                        const double* cmats, const double* theta, int P, int batch_offset, void* out, int stride,
+                        int pass_base, int batch, cudaStream_t s);
 cudaError_t launch_init_state(int prec, void* psi, const void* init, int n, int batch,
                               cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, int batch, cudaStream_t s);

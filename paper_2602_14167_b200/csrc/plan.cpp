@@ -361,6 +361,8 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
         ds.n_phases = (int)phases.size();
         ds.op_end = (int)out.ops.size();
         ds.n_mat = moff;
+        ds.mbase = out.total_mat;
+        out.total_mat += (moff + 1) & ~1;  // keep 16-byte alignment of every block
         ds.n_taps = ntap;
         out.n_taps += ntap;
         out.max_mat = std::max(out.max_mat, moff);

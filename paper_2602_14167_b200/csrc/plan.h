@@ -83,6 +83,7 @@ struct DevSweep {
     int32_t phase_begin;
     int32_t op_begin, op_end;   // all ops of the sweep (matrix prologue)
     int32_t n_mat;              // complex entries of the sweep matrix block
+    int32_t mbase;              // offset of the block in the pass's per-state matrix table
     int32_t tap_begin, n_taps;  // taps of this sweep (global numbering)
     uint32_t out_mask;          // memory bits not in the tile
     int8_t tb[kMaxTileBits];    // tile-local bit -> memory bit position
@@ -141,6 +142,9 @@ struct SweepArgs {
     const double* cmats;       // constant matrices [n][16][2]
     double* tap_part;          // [B][n_taps_total][tiles]
     int n_taps_total;
+    const void* gmat;          // per-state gate-matrix table [B][gmat_stride] complex (RT)
+    int gmat_stride;           // complex entries per state (forward block then adjoint block)
+    int gmat_pass_base;        // offset of this pass's block inside a state's table
 };
 
 }  // namespace qfb

@@ -35,6 +35,7 @@ struct PassPlan {
     std::vector<DevOp> ops;
     std::vector<DevTap> taps;  // global tap index -> (slot, coef)
     int max_mat = 0;           // max complex entries of any sweep matrix block
+    int total_mat = 0;         // complex entries of all blocks (per-state matrix table)
     int max_ops = 0;           // max ops in a sweep
     int max_taps = 0;          // max taps in a sweep
 };

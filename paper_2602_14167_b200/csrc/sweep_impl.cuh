@@ -409,10 +409,9 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const SweepArgs a) {
     // op list, phases and gate matrices of this sweep -> shared memory
     for (int o = tid; o < n_ops; o += T) sops[o] = a.ops[sw.op_begin + o];
     for (int f = tid; f < sw.n_phases; f += T) sph[f] = a.phases[sw.phase_begin + f];
-    const double* th = a.theta + (size_t)(b + a.batch_offset) * a.P;
-    for (int o = sw.op_begin + tid; o < sw.op_end; o += T) {
-        const DevOp op = a.ops[o];
-        if (op.moff >= 0) build_matrix<V, BWD>(op, a.gates[op.gate], th, a.cmats, smat + op.moff);
+    {
+        const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + sw.mbase;
+        for (int i = tid; i < sw.n_mat; i += T) smat[i] = gm[i];
     }
 #pragma unroll
     for (int j = 0; j < NR; ++j) {

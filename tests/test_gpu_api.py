@@ -249,3 +249,24 @@ def test_single_gpu_comm_detach(ctx):
     E, G = engine.energy_grad_batch(ctx, prog, engine.Observable(ctx, n, h.codes, h.wr + 0j),
                                     np.zeros((2, P)))
     assert np.isfinite(E).all()
+
+
+def test_nccl_single_rank_collective_path(ctx):
+    """The sharded path (NCCL all-reduce of the zero-padded [B x (1+P)] result)
+    on a single-rank communicator: bitwise equal to the unsharded call, for both
+    batch and term sharding."""
+    from paper_2602_14167_b200 import _lib
+    n, ops, P = po.hea_template(10, 2)
+    h = po.random_sum(10, 30, po.Rng(5), True)
+    th = np.stack([np.linspace(-1, 1, P) * (b + 1) for b in range(3)])
+    c2 = engine.Context(0)
+    prog = engine.Program(c2, n, ops, P, "c64")
+    obs = engine.Observable(c2, n, h.codes, h.wr + 0j)
+    E0, G0 = engine.energy_grad_batch(c2, prog, obs, th)
+    c2.set_comm(0, 1, engine.Context.nccl_unique_id())
+    E1, G1 = engine.energy_grad_batch(c2, prog, obs, th)
+    assert np.array_equal(E0, E1) and np.array_equal(G0, G1)
+    obs.set_sharding(_lib.QF_SHARD_TERMS)
+    E2, G2 = engine.energy_grad_batch(c2, prog, obs, th)
+    assert np.array_equal(E0, E2) and np.array_equal(G0, G2)
+    c2.set_comm(0, 1, None)
