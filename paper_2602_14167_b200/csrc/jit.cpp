@@ -102,6 +102,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         return !(e && e[0] == '0');
     }();
     Out o;
+    if (const char* e = std::getenv("QF_JIT_SCALAR"))
+        if (e[0] == '1') o.s += "// qf-option: scalar-fp32\n";
     o.s += kPrelude;
     o.s += "\n";
     o("namespace qfb {");
@@ -404,7 +406,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             for (const char* A : arrs)
                 for (int l = 0; l < NR; ++l) {
                     const std::string& fac = tab[tidx(l)];
-                    if (!fac.empty()) o("      %s%d = cmul(%s%d, %s);", A, phys[l], A, phys[l], fac.c_str());
+                    if (!fac.empty()) o("      %s%d = jcmul(%s%d, %s);", A, phys[l], A, phys[l], fac.c_str());
                 }
             o("    }");
         };
@@ -604,13 +606,14 @@ bool read_file(const std::string& p, std::string& out) {
 }
 
 bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
-    static const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DQF_JIT=1"};
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DQF_JIT=1"};
+    if (src.find("// qf-option: scalar-fp32") != std::string::npos) opts.push_back("-DQF_JIT_SCALAR=1");
     nvrtcProgram prog = nullptr;
     if (g_nvrtc.create(&prog, src.c_str(), "qf_sweep.cu", 0, nullptr, nullptr) != 0) {
         err = "nvrtcCreateProgram failed";
         return false;
     }
-    int rc = g_nvrtc.compile(prog, 4, opts);
+    int rc = g_nvrtc.compile(prog, (int)opts.size(), opts.data());
     if (rc != 0) {
         size_t n = 0;
         g_nvrtc.logSize(prog, &n);

@@ -26,9 +26,38 @@ template <typename V> __device__ __forceinline__ V mk_basis(bool one) {
     return v;
 }
 
+// ---- amplitude arithmetic.  complex64 uses the sm_100 packed FP32 pipe
+// (FFMA2 / FMUL2 with scalar-broadcast and swapped-lane operands): a complex
+// multiply is 2 instructions instead of 4.  complex128 stays scalar (DFMA).
+
+__device__ __forceinline__ float2 swp(float2 a) { return make_float2(a.y, a.x); }
+
+#ifdef QF_JIT_SCALAR  // A/B switch: scalar FP32 helpers
+__device__ __forceinline__ float2 __fmul2_rn(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 __ffma2_rn(float2 a, float2 b, float2 c) {
+    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+#endif
+
+// a * d (complex)
+__device__ __forceinline__ float2 jcmul(float2 a, float2 d) {
+    return __ffma2_rn(swp(a), make_float2(-d.y, d.y), __fmul2_rn(a, make_float2(d.x, d.x)));
+}
+__device__ __forceinline__ double2 jcmul(double2 a, double2 d) { return cmul(a, d); }
+// acc + a * d (complex)
+__device__ __forceinline__ float2 jcfma(float2 a, float2 d, float2 acc) {
+    return __ffma2_rn(swp(a), make_float2(-d.y, d.y), __ffma2_rn(a, make_float2(d.x, d.x), acc));
+}
+__device__ __forceinline__ double2 jcfma(double2 a, double2 d, double2 acc) { return cfma(d, a, acc); }
+
 // real 2x2 [[m0, m1], [m2, m3]] (real parts) on (a0, a1)
-template <typename V> __device__ __forceinline__ void jr1(V& a0, V& a1, V m0, V m1, V m2, V m3) {
-    const V t0 = a0, t1 = a1;
+__device__ __forceinline__ void jr1(float2& a0, float2& a1, float2 m0, float2 m1, float2 m2, float2 m3) {
+    const float2 t0 = a0, t1 = a1;
+    a0 = __ffma2_rn(t1, make_float2(m1.x, m1.x), __fmul2_rn(t0, make_float2(m0.x, m0.x)));
+    a1 = __ffma2_rn(t1, make_float2(m3.x, m3.x), __fmul2_rn(t0, make_float2(m2.x, m2.x)));
+}
+__device__ __forceinline__ void jr1(double2& a0, double2& a1, double2 m0, double2 m1, double2 m2, double2 m3) {
+    const double2 t0 = a0, t1 = a1;
     a0.x = fma(m1.x, t1.x, m0.x * t0.x);
     a0.y = fma(m1.x, t1.y, m0.x * t0.y);
     a1.x = fma(m3.x, t1.x, m2.x * t0.x);
@@ -37,12 +66,18 @@ template <typename V> __device__ __forceinline__ void jr1(V& a0, V& a1, V m0, V 
 // general complex 2x2
 template <typename V> __device__ __forceinline__ void jg1(V& a0, V& a1, V m0, V m1, V m2, V m3) {
     const V t0 = a0, t1 = a1;
-    a0 = cfma(m1, t1, cmul(m0, t0));
-    a1 = cfma(m3, t1, cmul(m2, t0));
+    a0 = jcfma(t1, m1, jcmul(t0, m0));
+    a1 = jcfma(t1, m3, jcmul(t0, m2));
 }
-// [[c, -i s], [-i s, c]] with m0 = (c, s)
-template <typename V> __device__ __forceinline__ void jrx(V& a0, V& a1, V m0) {
-    const V t0 = a0, t1 = a1;
+// [[c, -i s], [-i s, c]] with m0 = (c, s):  a0' = c a0 + s (a1.y, -a1.x)
+__device__ __forceinline__ void jrx(float2& a0, float2& a1, float2 m0) {
+    const float2 t0 = a0, t1 = a1;
+    const float2 cc = make_float2(m0.x, m0.x), ss = make_float2(m0.y, -m0.y);
+    a0 = __ffma2_rn(swp(t1), ss, __fmul2_rn(t0, cc));
+    a1 = __ffma2_rn(swp(t0), ss, __fmul2_rn(t1, cc));
+}
+__device__ __forceinline__ void jrx(double2& a0, double2& a1, double2 m0) {
+    const double2 t0 = a0, t1 = a1;
     a0.x = fma(m0.y, t1.y, m0.x * t0.x);
     a0.y = fma(-m0.y, t1.x, m0.x * t0.y);
     a1.x = fma(m0.y, t0.y, m0.x * t1.x);
@@ -56,10 +91,10 @@ template <typename V> __device__ __forceinline__ void jcswap(V& a, V& b, bool c)
 // dense 4x4 (row-major m[16]) on (a0, a1, a2, a3) = local basis 00, 01, 10, 11
 template <typename V> __device__ __forceinline__ void jg2(V& a0, V& a1, V& a2, V& a3, const V* m) {
     const V v0 = a0, v1 = a1, v2 = a2, v3 = a3;
-    a0 = cfma(m[3], v3, cfma(m[2], v2, cfma(m[1], v1, cmul(m[0], v0))));
-    a1 = cfma(m[7], v3, cfma(m[6], v2, cfma(m[5], v1, cmul(m[4], v0))));
-    a2 = cfma(m[11], v3, cfma(m[10], v2, cfma(m[9], v1, cmul(m[8], v0))));
-    a3 = cfma(m[15], v3, cfma(m[14], v2, cfma(m[13], v1, cmul(m[12], v0))));
+    a0 = jcfma(v3, m[3], jcfma(v2, m[2], jcfma(v1, m[1], jcmul(v0, m[0]))));
+    a1 = jcfma(v3, m[7], jcfma(v2, m[6], jcfma(v1, m[5], jcmul(v0, m[4]))));
+    a2 = jcfma(v3, m[11], jcfma(v2, m[10], jcfma(v1, m[9], jcmul(v0, m[8]))));
+    a3 = jcfma(v3, m[15], jcfma(v2, m[14], jcfma(v1, m[13], jcmul(v0, m[12]))));
 }
 
 // Reduce `cnt` staged taps ([cnt][T] per-thread partials in shared memory) in a

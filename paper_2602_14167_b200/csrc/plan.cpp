@@ -248,6 +248,7 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
         ds.tap_begin = out.n_taps;
 
         // phases: schedule the sweep's gates over tile-local bits with budget R
+        auto order_of = [&](int it) { return order[it]; };
         std::map<int, int> local;  // index in `order` -> index in sweep
         for (size_t i = 0; i < sw.items.size(); ++i) local[sw.items[i]] = (int)i;
         std::vector<uint64_t> lneed(sw.items.size());
@@ -264,6 +265,44 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             }
         }
         auto phases = schedule_groups(lneed, lpreds, 0, R);
+        // Inside a phase, issue ready non-diagonal gates first and release the
+        // diagonal ones (which commute with each other) in batches: long runs of
+        // diagonal gates and Z taps are fused by the kernel generator.
+        for (auto& ph : phases) {
+            std::map<int, int> pos;  // local item -> position in phase
+            for (size_t i = 0; i < ph.items.size(); ++i) pos[ph.items[i]] = (int)i;
+            std::vector<int> indeg(ph.items.size(), 0);
+            std::vector<std::vector<int>> succ(ph.items.size());
+            for (size_t i = 0; i < ph.items.size(); ++i)
+                for (int pr : lpreds[ph.items[i]]) {
+                    auto f = pos.find(pr);
+                    if (f == pos.end()) continue;
+                    ++indeg[i];
+                    succ[f->second].push_back((int)i);
+                }
+            std::set<int> ready;
+            for (size_t i = 0; i < ph.items.size(); ++i)
+                if (!indeg[i]) ready.insert((int)i);
+            std::vector<int> order;
+            auto take = [&](int i) {
+                ready.erase(i);
+                order.push_back(ph.items[i]);
+                for (int s2 : succ[i])
+                    if (--indeg[s2] == 0) ready.insert(s2);
+            };
+            while (!ready.empty()) {
+                int pick = -1;
+                for (int i : ready)
+                    if (!P.gates[order_of(sw.items[ph.items[i]])].diag) { pick = i; break; }
+                if (pick >= 0) {
+                    take(pick);
+                    continue;
+                }
+                std::vector<int> diag(ready.begin(), ready.end());  // all ready are diagonal
+                for (int i : diag) take(i);
+            }
+            ph.items.swap(order);
+        }
         int moff = 0, ntap = 0;
         for (auto& ph : phases) {
             DevPhase dp{};
