@@ -924,14 +924,34 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
             QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
         ctx->launches++;
     }
+    // Shear-form rotations (DK_RS) may apply -R: a global sign, irrelevant to
+    // energies and gradients but not to the state itself -- undo it here.
+    double sign = 1.0;
+    {
+        std::vector<unsigned char> tab((size_t)P.fwd.total_mat * vs);
+        if (!tab.empty())
+            QF_CUDA(cudaMemcpyAsync(tab.data(), ctx->gmat.p, tab.size(), cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaStreamSynchronize(s));
+        for (const DevSweep& sw : P.fwd.sweeps)
+            for (int o = sw.op_begin; o < sw.op_end; ++o) {
+                const DevOp& op = P.fwd.ops[o];
+                if (op.kind != DK_RS) continue;
+                const size_t e = (size_t)(sw.mbase + op.moff + 1);
+                const double sg = P.prec == QF_C128 ? reinterpret_cast<const double*>(tab.data())[2 * e]
+                                                    : reinterpret_cast<const float*>(tab.data())[2 * e];
+                if (sg < 0) sign = -sign;
+            }
+    }
     if (P.prec == QF_C128) {
         QF_CUDA(cudaMemcpyAsync(amps_out, ctx->psi.p, N * 16, cudaMemcpyDeviceToHost, s));
         QF_CUDA(cudaStreamSynchronize(s));
+        if (sign < 0)
+            for (size_t i = 0; i < 2 * N; ++i) amps_out[i] = -amps_out[i];
     } else {
         std::vector<float> f(2 * N);
         QF_CUDA(cudaMemcpyAsync(f.data(), ctx->psi.p, N * 8, cudaMemcpyDeviceToHost, s));
         QF_CUDA(cudaStreamSynchronize(s));
-        for (size_t i = 0; i < 2 * N; ++i) amps_out[i] = f[i];
+        for (size_t i = 0; i < 2 * N; ++i) amps_out[i] = sign * f[i];
     }
     return QF_OK;
 }

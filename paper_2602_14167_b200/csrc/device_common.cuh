@@ -77,7 +77,19 @@ __device__ void build_matrix(const DevOp& op, const DevGate& g, const double* th
             put_c<V, false>(out, 0, isq, 0); put_c<V, false>(out, 1, isq, 0);
             put_c<V, false>(out, 2, isq, 0); put_c<V, false>(out, 3, -isq, 0);
             return;
-        case GK_RY:  // [[c, -s], [s, c]]; adjoint = transpose
+        case GK_RY:
+            if (op.kind == DK_RS) {  // shear form: t = tan(phi/2) with |t| <= 1, sign folded as a global phase
+                const double sg = ADJ ? -s : s;
+                if (c >= 0) {
+                    put_c<V, false>(out, 0, sg / (1.0 + c), sg);
+                    put_c<V, false>(out, 1, 1.0, 0.0);
+                } else {
+                    put_c<V, false>(out, 0, -sg / (1.0 - c), -sg);
+                    put_c<V, false>(out, 1, -1.0, 0.0);
+                }
+                return;
+            }
+            // [[c, -s], [s, c]]; adjoint = transpose
             put_c<V, false>(out, 0, c, 0); put_c<V, false>(out, 1, ADJ ? s : -s, 0);
             put_c<V, false>(out, 2, ADJ ? -s : s, 0); put_c<V, false>(out, 3, c, 0);
             return;

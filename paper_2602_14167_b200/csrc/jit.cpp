@@ -436,6 +436,13 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     o("    }");
                     break;
                 }
+                case DK_RS: {
+                    o("    { const V m0 = smat[%d];", op.moff);
+                    for (const char* A : arrs)
+                        for (auto pr : pairs(op.rb0)) o("      jrs(%s%d, %s%d, m0);", A, pr.first, A, pr.second);
+                    o("    }");
+                    break;
+                }
                 case DK_X1:
                     rename(op.rb0, -1);
                     break;

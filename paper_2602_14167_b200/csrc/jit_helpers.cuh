@@ -83,6 +83,21 @@ __device__ __forceinline__ void jrx(double2& a0, double2& a1, double2 m0) {
     a1.x = fma(m0.y, t0.y, m0.x * t1.x);
     a1.y = fma(-m0.y, t0.x, m0.x * t1.y);
 }
+// rotation [[c, -s], [s, c]] (up to a global sign) as three shears, m0 = (t, s)
+__device__ __forceinline__ void jrs(float2& a0, float2& a1, float2 m0) {
+    const float2 mt = make_float2(-m0.x, -m0.x), ms = make_float2(m0.y, m0.y);
+    a0 = __ffma2_rn(a1, mt, a0);
+    a1 = __ffma2_rn(a0, ms, a1);
+    a0 = __ffma2_rn(a1, mt, a0);
+}
+__device__ __forceinline__ void jrs(double2& a0, double2& a1, double2 m0) {
+    a0.x = fma(-m0.x, a1.x, a0.x);
+    a0.y = fma(-m0.x, a1.y, a0.y);
+    a1.x = fma(m0.y, a0.x, a1.x);
+    a1.y = fma(m0.y, a0.y, a1.y);
+    a0.x = fma(-m0.x, a1.x, a0.x);
+    a0.y = fma(-m0.x, a1.y, a0.y);
+}
 template <typename V> __device__ __forceinline__ void jcswap(V& a, V& b, bool c) {
     const V t0 = a, t1 = b;
     a = c ? t1 : t0;

@@ -207,6 +207,7 @@ static std::string classify(int n, const GateSpec& s, const double* mats, int n_
 static int mat_size(uint8_t kind) {
     switch (kind) {
         case DK_G1: case DK_R1: case DK_RX: return 4;
+        case DK_RS: return 2;
         case DK_D1: return 2;
         case DK_D2: return 4;
         case DK_G2: return 16;
@@ -377,7 +378,8 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
                     op.kind = gi.nw == 2 ? DK_D2 : DK_D1;
                 } else {
                     switch (s.kind) {
-                        case QF_H: case QF_RY: op.kind = DK_R1; break;
+                        case QF_H: op.kind = DK_R1; break;
+                        case QF_RY: op.kind = DK_RS; break;
                         case QF_RX: op.kind = DK_RX; break;
                         case QF_X: op.kind = DK_X1; break;
                         case QF_CX:

@@ -56,6 +56,8 @@ enum DevKind : uint8_t {
     DK_TY = 9,   // G = Y on rb0
     DK_TZ = 10,  // G = Z on pos0 (rb0 register bit or -1)
     DK_TZZ = 11, // G = Z Z on pos0,pos1
+    DK_RS = 12,  // real rotation [[c,-s],[s,c]] on rb0 applied as three shears; block (t, s), (sigma, 0):
+                 // sigma = -1 means the kernel applies -R (a global phase)
     DK_NONE = 255
 };
 

@@ -66,6 +66,24 @@ __device__ __forceinline__ void k_rx(V* x, RT c, RT s) {
         x[j].y = fma(-s, a0.x, c * a1.y);
     }
 }
+// rotation as three shears: a0 -= t a1; a1 += s a0; a0 -= t a1   (m = (t, s))
+template <int RB, int NR, typename V, typename RT>
+__device__ __forceinline__ void k_rs(V* x, RT t, RT s) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        if (i & (1 << RB)) continue;
+        const int j = i | (1 << RB);
+        V a0 = x[i], a1 = x[j];
+        a0.x = fma(-t, a1.x, a0.x);
+        a0.y = fma(-t, a1.y, a0.y);
+        a1.x = fma(s, a0.x, a1.x);
+        a1.y = fma(s, a0.y, a1.y);
+        a0.x = fma(-t, a1.x, a0.x);
+        a0.y = fma(-t, a1.y, a0.y);
+        x[i] = a0;
+        x[j] = a1;
+    }
+}
 template <int RB, int NR, typename V> __device__ __forceinline__ void k_x1(V* x) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
@@ -211,6 +229,14 @@ __device__ __forceinline__ void apply_op(const DevOp& op, V* x, V* y, uint32_t g
             with_rb<R>(op.rb0, [&](auto B) {
                 k_rx<decltype(B)::value, NR>(x, c, s);
                 if constexpr (BWD) k_rx<decltype(B)::value, NR>(y, c, s);
+            });
+            break;
+        }
+        case DK_RS: {
+            const RT t = smat[op.moff].x, s = smat[op.moff].y;
+            with_rb<R>(op.rb0, [&](auto B) {
+                k_rs<decltype(B)::value, NR>(x, t, s);
+                if constexpr (BWD) k_rs<decltype(B)::value, NR>(y, t, s);
             });
             break;
         }
