@@ -62,6 +62,11 @@ struct BitSrc {
 
 }  // namespace
 
+bool jit_pipe_mode() {
+    const char* e = std::getenv("QF_JIT_PIPE");
+    return e && e[0] == '1';
+}
+
 // Gradient taps are staged per thread in shared memory ([slots][T] reals) and
 // reduced in batches at fixed points (no per-tap shuffle chains).
 int jit_tap_stage(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
@@ -76,7 +81,7 @@ size_t jit_smem_bytes(const ProgramPlan& P, const PassPlan& pass, int si, bool b
     const int T = 1 << (sw.k - sw.R);
     const int nwarps = (T + 31) / 32;
     (void)nwarps;
-    size_t b = ((size_t)1 << sw.k) * vs * (bwd ? 2 : 1);
+    size_t b = ((size_t)1 << sw.k) * vs * (bwd ? 2 : 1) * (jit_pipe_mode() ? 2 : 1);
     b += (size_t)((sw.n_mat + 1) & ~1) * vs;
     b += (size_t)jit_tap_stage(P, pass, si, bwd) * T * (vs / 2);
     return b;
@@ -101,7 +106,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         const char* e = std::getenv("QF_JIT_FUSE");
         return !(e && e[0] == '0');
     }();
+    const bool pipe = jit_pipe_mode();
     Out o;
+    if (pipe) o.s += "// qf-option: pipelined\n";
     if (const char* e = std::getenv("QF_JIT_SCALAR"))
         if (e[0] == '1') o.s += "// qf-option: scalar-fp32\n";
     o.s += kPrelude;
@@ -110,16 +117,83 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) qf_sweep(const SweepArgs a) {", T, minb);
     o("  typedef %s V; typedef %s RT;", Vt, RTt);
     o("  extern __shared__ __align__(16) unsigned char smem_raw[];");
-    o("  V* tile = reinterpret_cast<V*>(smem_raw);");
-    o("  V* tile2 = tile + %u;", bwd ? (1u << k) : 0u);
-    o("  V* smat = tile2 + %u;", 1u << k);
+    const unsigned TSZ = (1u << k) * (bwd ? 2u : 1u);  // one tile buffer (psi [+ lambda])
     const int S = jit_tap_stage(P, pass, si, bwd);
-    o("  RT* stg = reinterpret_cast<RT*>(smat + %d);", (sw.n_mat + 1) & ~1);
-    o("  (void)tile; (void)tile2; (void)stg;");
-    o("  const uint32_t tid = threadIdx.x, tile_id = blockIdx.x; const int b = blockIdx.y;");
-    o("  V* st = reinterpret_cast<V*>(a.psi) + (size_t)b * %zuull;", (size_t)1 << P.n);
-    if (bwd) o("  V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", (size_t)1 << P.n);
-    o("  const uint32_t tile_base = pdep_u32(tile_id, %uu);", sw.out_mask);
+    const unsigned ntiles = 1u << (P.n - k);
+    std::vector<uint32_t> joff(NR);
+    for (int j = 0; j < NR; ++j) {
+        uint32_t off = 0;
+        for (int r = 0; r < R; ++r)
+            if ((j >> r) & 1) off |= 1u << sw.tb[k - R + r];
+        joff[j] = off;
+    }
+    if (!pipe) {
+        o("  V* tile = reinterpret_cast<V*>(smem_raw);");
+        o("  V* tile2 = tile + %u;", bwd ? (1u << k) : 0u);
+        o("  V* smat = tile2 + %u;", 1u << k);
+        o("  RT* stg = reinterpret_cast<RT*>(smat + %d);", (sw.n_mat + 1) & ~1);
+        o("  (void)tile; (void)tile2; (void)stg;");
+        o("  const uint32_t tid = threadIdx.x, tile_id = blockIdx.x; const int b = blockIdx.y;");
+        o("  const uint32_t ntiles = gridDim.x;");
+        o("  V* st = reinterpret_cast<V*>(a.psi) + (size_t)b * %zuull;", (size_t)1 << P.n);
+        if (bwd) o("  V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", (size_t)1 << P.n);
+        o("  const uint32_t tile_base = pdep_u32(tile_id, %uu);", sw.out_mask);
+    } else {
+        // Persistent CTA over a contiguous range of (state, tile) items; tile i+1 is
+        // prefetched with cp.async into the second buffer while tile i is computed.
+        o("  V* bufA = reinterpret_cast<V*>(smem_raw);");
+        o("  V* bufB = bufA + %u;", TSZ);
+        o("  V* smat = bufB + %u;", TSZ);
+        o("  RT* stg = reinterpret_cast<RT*>(smat + %d);", (sw.n_mat + 1) & ~1);
+        o("  (void)stg;");
+        o("  const uint32_t tid = threadIdx.x;");
+        o("  const uint32_t ntiles = %uu;", ntiles);
+        o("  const long long items = (long long)%u * a.batch;", ntiles);
+        o("  const long long per = (items + gridDim.x - 1) / gridDim.x;");
+        o("  const long long it0 = (long long)blockIdx.x * per;");
+        o("  const long long it1 = it0 + per < items ? it0 + per : items;");
+        o("  if (it0 >= it1) return;");
+        o("  uint32_t g_thr = 0;");
+        for (int j = 0; j < k - R; ++j) o("  g_thr |= ((tid >> %d) & 1u) << %d;", j, sw.tb[j]);
+        o("  auto prefetch = [&](V* buf, long long item) {");
+        o("    const int pb = (int)(item >> %d);", P.n - k);
+        o("    const uint32_t gb = pdep_u32((uint32_t)(item & %uu), %uu) | g_thr;", ntiles - 1, sw.out_mask);
+        o("    const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)pb * %zuull;", (size_t)1 << P.n);
+        if (bwd) o("    const V* pl = reinterpret_cast<const V*>(a.lam) + (size_t)pb * %zuull;", (size_t)1 << P.n);
+        if (!bwd) {
+            o("    if (a.from_zero) {");
+            for (int j = 0; j < NR; ++j)
+                o("      buf[swz<%d>(tid + %uu)] = mk_basis<V>((gb | %uu) == 0u);", W, (unsigned)(T * j), joff[j]);
+            o("      return;");
+            o("    }");
+        }
+        for (int j = 0; j < NR; ++j) {
+            o("    cp_async_v(buf + swz<%d>(tid + %uu), ps + (gb | %uu));", W, (unsigned)(T * j), joff[j]);
+            if (bwd) o("    cp_async_v(buf + %u + swz<%d>(tid + %uu), pl + (gb | %uu));", 1u << k, W, (unsigned)(T * j), joff[j]);
+        }
+        o("  };");
+        o("  V* cur = bufA; V* nxt = bufB;");
+        o("  prefetch(cur, it0);");
+        o("  cp_async_commit();");
+        o("  int cur_b = -1;");
+        o("  for (long long it = it0; it < it1; ++it) {");
+        o("  if (it + 1 < it1) prefetch(nxt, it + 1);");
+        o("  cp_async_commit();");
+        o("  cp_async_wait_1();");
+        o("  __syncthreads();");
+        o("  const int b = (int)(it >> %d); const uint32_t tile_id = (uint32_t)(it & %uu);", P.n - k, ntiles - 1);
+        o("  V* tile = cur; V* tile2 = cur + %u; (void)tile2;", bwd ? (1u << k) : 0u);
+        o("  V* st = reinterpret_cast<V*>(a.psi) + (size_t)b * %zuull;", (size_t)1 << P.n);
+        if (bwd) o("  V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", (size_t)1 << P.n);
+        o("  const uint32_t tile_base = pdep_u32(tile_id, %uu);", sw.out_mask);
+        o("  if (b != cur_b) {");
+        o("    const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + %d;",
+          sw.mbase);
+        o("    for (int i = (int)tid; i < %d; i += %d) smat[i] = gm[i];", sw.n_mat, T);
+        o("    cur_b = b;");
+        o("    __syncthreads();");
+        o("  }");
+    }
 
     int tl_of_pos[64];
     for (int p = 0; p < 64; ++p) tl_of_pos[p] = -1;
@@ -136,7 +210,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if (ph.thr_tl[j] < need) ++have;
         return have == need;
     };
-    const bool direct_first = allow_direct && nph > 0 && lanes_cover_low(phase(0));
+    const bool direct_first = !pipe && allow_direct && nph > 0 && lanes_cover_low(phase(0));
     const bool direct_last = allow_direct && nph > 0 && lanes_cover_low(phase(nph - 1));
     // memory offset of register index l in phase f, and of the phase's thread base
     auto reg_goff = [&](const DevPhase& ph, int l) {
@@ -150,18 +224,13 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         for (int j = 0; j < k - R; ++j) o("  %s |= ((tid >> %d) & 1u) << %d;", name, j, sw.tb[(int)ph.thr_tl[j]]);
     };
 
-    std::vector<uint32_t> joff(NR);
-    for (int j = 0; j < NR; ++j) {
-        uint32_t off = 0;
-        for (int r = 0; r < R; ++r)
-            if ((j >> r) & 1) off |= 1u << sw.tb[k - R + r];
-        joff[j] = off;
-    }
     if (!direct_first || !direct_last) {
         o("  uint32_t g_ld = tile_base;");
         for (int j = 0; j < k - R; ++j) o("  g_ld |= ((tid >> %d) & 1u) << %d;", j, sw.tb[j]);
     }
-    if (direct_first) {
+    if (pipe) {
+        // loads / matrices handled in the loop header
+    } else if (direct_first) {
         emit_gbase(phase(0), "g_p0");
         for (int l = 0; l < NR; ++l) {
             const uint32_t off = reg_goff(phase(0), l);
@@ -178,12 +247,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 o("  V v%d = st[g_ld | %uu]; V w%d = lm[g_ld | %uu];", j, joff[j], j, joff[j]);
         }
     }
-    o("  {  // this sweep's gate matrices (precomputed once per parameter set)");
-    o("    const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + %d;",
-      sw.mbase);
-    o("    for (int i = (int)tid; i < %d; i += %d) smat[i] = gm[i];", sw.n_mat, T);
-    o("  }");
-    if (!direct_first) {
+    if (!pipe) {
+        o("  {  // this sweep's gate matrices (precomputed once per parameter set)");
+        o("    const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + %d;",
+          sw.mbase);
+        o("    for (int i = (int)tid; i < %d; i += %d) smat[i] = gm[i];", sw.n_mat, T);
+        o("  }");
+    }
+    if (!direct_first && !pipe) {
         for (int j = 0; j < NR; ++j) {
             if (bwd)
                 o("  tile[swz<%d>(tid + %uu)] = v%d; tile2[swz<%d>(tid + %uu)] = w%d;", W, (unsigned)(T * j), j, W,
@@ -192,14 +263,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 o("  tile[swz<%d>(tid + %uu)] = v%d;", W, (unsigned)(T * j), j);
         }
     }
-    o("  __syncthreads();");
+    if (!pipe) o("  __syncthreads();");
 
     std::vector<const char*> arrs = {"x"};
     if (bwd) arrs.push_back("y");
     int uid = 0;  // unique names inside fused blocks
     auto emit_flush = [&](int first, int cnt) {
         o("    __syncthreads();");
-        o("    tap_flush<RT>(stg, %d, %d, a.tap_part + ((size_t)b * a.n_taps_total + %d) * gridDim.x + tile_id, gridDim.x);",
+        o("    tap_flush<RT>(stg, %d, %d, a.tap_part + ((size_t)b * a.n_taps_total + %d) * ntiles + tile_id, ntiles);",
           cnt, T, sw.tap_begin + first);
         o("    __syncthreads();");
     };
@@ -530,6 +601,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         const int rem = sw.n_taps % S;
         emit_flush(sw.n_taps - rem, rem);
     }
+    if (pipe) {
+        o("  __syncthreads();");
+        o("  { V* t_ = cur; cur = nxt; nxt = t_; }");
+        o("  }");
+    }
     o("}");
     o("}  // namespace qfb");
     return o.s;
@@ -736,6 +812,16 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
                 return false;
             }
         }
+        jk.pipe = jit_pipe_mode();
+        if (jk.pipe) {
+            int dev = 0, sms = 148, per = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)kern, jk.threads, jk.smem) != cudaSuccess ||
+                per < 1)
+                per = 1;
+            jk.ctas = sms * per;
+        }
         (jb.bwd ? bwd : fwd).sweeps[jb.si] = jk;
         if (jb.from_cache) st.cached++;
         else st.compiled++;
@@ -746,9 +832,15 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
 }
 
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream) {
-    void* args[] = {const_cast<SweepArgs*>(&a)};
-    cudaError_t e = cudaLaunchKernel((const void*)k.kernel, dim3(tiles, batch), dim3(k.threads), args, k.smem,
-                                     (cudaStream_t)stream);
+    SweepArgs aa = a;
+    aa.batch = batch;
+    void* args[] = {&aa};
+    dim3 grid(tiles, batch);
+    if (k.pipe) {
+        const long long items = (long long)tiles * batch;
+        grid = dim3((unsigned)std::min<long long>(items, (long long)k.ctas));
+    }
+    cudaError_t e = cudaLaunchKernel((const void*)k.kernel, grid, dim3(k.threads), args, k.smem, (cudaStream_t)stream);
     return (int)e;
 }
 

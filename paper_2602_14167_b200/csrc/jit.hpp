@@ -19,7 +19,11 @@ struct JitKernel {
     void* kernel = nullptr;  // cudaKernel_t
     int threads = 0;
     size_t smem = 0;
+    bool pipe = false;       // persistent, cp.async double-buffered variant
+    int ctas = 0;            // resident CTAs (pipe mode grid)
 };
+
+bool jit_pipe_mode();
 
 struct JitPass {
     std::vector<JitKernel> sweeps;

@@ -112,6 +112,18 @@ template <typename V> __device__ __forceinline__ void jg2(V& a0, V& a1, V& a2, V
     a3 = jcfma(v3, m[15], jcfma(v2, m[14], jcfma(v1, m[13], jcmul(v0, m[12]))));
 }
 
+// cp.async (LDGSTS) of one amplitude into shared memory (8 B for c64, 16 B for c128)
+__device__ __forceinline__ void cp_async_v(float2* dst, const float2* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_v(double2* dst, const double2* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
 // Reduce `cnt` staged taps ([cnt][T] per-thread partials in shared memory) in a
 // fixed order (deterministic) and write one partial per tap: out[t * stride].
 template <typename RT>

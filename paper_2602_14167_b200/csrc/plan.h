@@ -147,6 +147,7 @@ struct SweepArgs {
     const void* gmat;          // per-state gate-matrix table [B][gmat_stride] complex (RT)
     int gmat_stride;           // complex entries per state (forward block then adjoint block)
     int gmat_pass_base;        // offset of this pass's block inside a state's table
+    int batch;                 // states in this launch (persistent kernels)
 };
 
 }  // namespace qfb
