@@ -50,7 +50,7 @@ static int popc(uint64_t x) { return __builtin_popcountll(x); }
 
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget) {
+                                   uint64_t fixed_bits, int budget, int max_items) {
     const int n = (int)need.size();
     std::vector<int> indeg(n, 0);
     std::vector<std::vector<int>> succ(n);
@@ -68,7 +68,7 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
         g.bits = fixed_bits;
         for (;;) {
             bool progress = true;
-            while (progress) {
+            while (progress && (max_items <= 0 || (int)g.items.size() < max_items)) {
                 progress = false;
                 for (int it : ready) {
                     if ((need[it] & ~g.bits) == 0) {
@@ -83,6 +83,7 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                 }
             }
             int best = -1, best_cost = 1 << 30;
+            if (max_items > 0 && (int)g.items.size() >= max_items) break;
             for (int it : ready) {
                 int extra = popc(need[it] & ~g.bits);
                 if (popc(g.bits) + extra <= budget && extra < best_cost) {
@@ -226,7 +227,11 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
     for (size_t i = 0; i < order.size(); ++i) need[i] = P.gates[order[i]].need;
     const uint64_t all = (n >= 64) ? ~0ull : ((1ull << n) - 1);
     const uint64_t fixed = (n <= k) ? all : ((1ull << c) - 1);
-    auto sweeps = schedule_groups(need, preds_in_order, fixed, k);
+    // cap the gates per sweep: the specialised kernels are straight-line code, and
+    // very long sweeps overflow the instruction cache
+    int max_ops = 0;
+    if (const char* e = std::getenv("QF_MAX_SWEEP_OPS")) max_ops = std::atoi(e);
+    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops);
 
     for (auto& sw : sweeps) {
         // pad the tile to exactly k bits with the lowest free positions
