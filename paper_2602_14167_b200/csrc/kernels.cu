@@ -21,6 +21,18 @@
 
 namespace qfb {
 
+// acc + k * s  and  acc + k * i s  (k real); complex64 on the packed FP32 pipe
+__device__ __forceinline__ float2 hp_axpy(float k, float2 s, float2 acc) { return __ffma2_rn(make_float2(k, k), s, acc); }
+__device__ __forceinline__ double2 hp_axpy(double k, double2 s, double2 acc) {
+    return make_double2(fma(k, s.x, acc.x), fma(k, s.y, acc.y));
+}
+__device__ __forceinline__ float2 hp_iaxpy(float k, float2 s, float2 acc) {
+    return __ffma2_rn(make_float2(-k, k), make_float2(s.y, s.x), acc);
+}
+__device__ __forceinline__ double2 hp_iaxpy(double k, double2 s, double2 acc) {
+    return make_double2(fma(-k, s.y, acc.x), fma(k, s.x, acc.y));
+}
+
 // ---------------------------------------------------------------------------
 // lambda = H psi and E = Re<psi|lambda>, output-stationary per tile
 // ---------------------------------------------------------------------------
@@ -75,24 +87,23 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
                     const uint32_t par = (__popc(p & zlo) ^ cpar) & 1;
                     dg[i] += par ? -cr : cr;
                 }
-            } else if (d.kind == TK_FLIP) {
-                V c;
-                c.x = cr;
-                c.y = ci;
+            } else if (!d.yodd) {
+                // real coefficient (Re(w) i^y with y even): acc += (+-cr) src
 #pragma unroll
                 for (int i = 0; i < NA; ++i) {
                     const uint32_t p = tid + (uint32_t)T * i;
-                    acc[i] = cfma(c, src[p ^ d.f_in], acc[i]);
+                    RT k = cr;
+                    if (d.kind == TK_GEN && ((__popc(p & zlo) ^ cpar) & 1)) k = -k;
+                    acc[i] = hp_axpy(k, src[p ^ d.f_in], acc[i]);
                 }
             } else {
+                // imaginary coefficient (y odd): acc += (+-ci) i src
 #pragma unroll
                 for (int i = 0; i < NA; ++i) {
                     const uint32_t p = tid + (uint32_t)T * i;
-                    const uint32_t par = (__popc(p & zlo) ^ cpar) & 1;
-                    V c;
-                    c.x = par ? -cr : cr;
-                    c.y = par ? -ci : ci;
-                    acc[i] = cfma(c, src[p ^ d.f_in], acc[i]);
+                    RT k = ci;
+                    if ((__popc(p & zlo) ^ cpar) & 1) k = -k;
+                    acc[i] = hp_iaxpy(k, src[p ^ d.f_in], acc[i]);
                 }
             }
         }

@@ -503,6 +503,7 @@ std::string build_observable_plan(int n, int n_terms, const int8_t* codes, const
         d.f_in = flip & lo;
         d.z = z;
         d.fz_par = (uint32_t)(__builtin_popcount(flip & z) & 1);
+        d.yodd = y & 1;
         d.kind = flip == 0 ? TK_DIAG : (z == 0 ? TK_FLIP : TK_GEN);
         groups[flip & ~lo].push_back(d);
     }

@@ -118,6 +118,7 @@ struct DevTerm {
     uint32_t f_in;     // flip bits inside the tile
     uint32_t z;        // z mask (all bits)
     uint32_t fz_par;   // parity(f & z) & 1 (folded into the sign)
+    int32_t yodd;      // odd number of Y: the coefficient is purely imaginary
     double c_re, c_im; // Re(w) * i^y  (Hermitian part)
     double ci_re, ci_im; // Im(w) * i^y (imaginary part of expectation_pauli)
 };
