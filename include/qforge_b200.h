@@ -164,6 +164,15 @@ int qf_expectation(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs
 int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs,
                          int batch, const double* thetas, double* energies, double* grads);
 
+/* pauli_sum_to_coo (reference src/pauli.cpp:89-153): the Pauli sum as a canonical
+ * sparse matrix (row-major, ascending columns, duplicates summed per flip mask,
+ * exact zeros dropped), complex128 values [nnz][2].  Call with NULL outputs to
+ * get nnz, then with buffers of capacity >= nnz (device pointers when
+ * device_buffers != 0).  n_qubits > n_guard -> QF_EINVAL (reference guard 26). */
+int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int device_buffers,
+                        int64_t* rows, int64_t* cols, double* vals, int64_t capacity,
+                        int64_t* nnz);
+
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
  * float64 device pointers.  Single-GPU semantics (no collective). */

@@ -216,6 +216,22 @@ def expectation(n, psi, h: Hamil):
 MODES = {"parameter_shift": 0, "finite_diff": 1, "adjoint": 2}
 
 
+def pauli_sum_to_coo(h: Hamil):
+    L = lib()
+    L.qo_pauli_sum_to_coo.restype = ctypes.c_longlong
+    L.qo_pauli_sum_to_coo.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int8),
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]
+    c8 = h.codes.ctypes.data_as(ctypes.POINTER(ctypes.c_int8))
+    nnz = L.qo_pauli_sum_to_coo(h.n, len(h.wr), _d(h.wr), _d(h.wi), c8, None, None, None, 0)
+    rows = np.zeros(nnz, np.int64)
+    cols = np.zeros(nnz, np.int64)
+    vals = np.zeros(nnz, np.complex128)
+    L.qo_pauli_sum_to_coo(h.n, len(h.wr), _d(h.wr), _d(h.wi), c8, rows.ctypes.data, cols.ctypes.data,
+                          vals.ctypes.data, nnz)
+    return rows, cols, vals
+
+
 def energy(a: Ansatz, theta, h: Hamil):
     th = np.ascontiguousarray(np.asarray(theta, np.float64).reshape(-1)) if a.n_params else np.zeros(1)
     e = np.zeros(1)

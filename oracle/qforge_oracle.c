@@ -553,6 +553,67 @@ int qo_energy_grad_batch(const qo_ansatz* a, int batch, const double* thetas,
 }
 
 /* ------------------------------------------------------------------------ */
+/* pauli_sum_to_coo: src/pauli.cpp:89-153 (single worker; per-row entries      */
+/* sorted by column with a stable insertion sort, duplicates summed in term  */
+/* order, exact zeros dropped)                                                */
+/* ------------------------------------------------------------------------ */
+long long qo_pauli_sum_to_coo(int n, int n_terms, const double* w_re, const double* w_im,
+                              const int8_t* codes, long long* rows, long long* cols,
+                              double complex* vals, long long capacity) {
+    static const double complex ipow[4] = {1.0, CMPLX(0, 1), -1.0, CMPLX(0, -1)};
+    if (n < 1) { fail("pauli_sum_to_coo: empty system"); return -1; }
+    const uint64_t dim = 1ULL << n;
+    uint64_t* flip = malloc(sizeof(uint64_t) * (n_terms + 1));
+    uint64_t* zm = malloc(sizeof(uint64_t) * (n_terms + 1));
+    double complex* base = malloc(sizeof(double complex) * (n_terms + 1));
+    for (int t = 0; t < n_terms; ++t) { /* compile_term, pauli.cpp:61-74 */
+        flip[t] = zm[t] = 0;
+        int y = 0;
+        for (int i = 0; i < n; ++i) {
+            uint64_t bit = 1ULL << (n - 1 - i);
+            switch (codes[(size_t)t * n + i]) {
+                case 1: flip[t] |= bit; break;
+                case 2: flip[t] |= bit; zm[t] |= bit; ++y; break;
+                case 3: zm[t] |= bit; break;
+            }
+        }
+        base[t] = CMPLX(w_re[t], w_im[t]) * ipow[y & 3];
+    }
+    uint64_t* ec = malloc(sizeof(uint64_t) * (n_terms + 1));
+    double complex* ev = malloc(sizeof(double complex) * (n_terms + 1));
+    long long total = 0;
+    for (uint64_t row = 0; row < dim; ++row) {
+        int m = 0;
+        for (int t = 0; t < n_terms; ++t) { /* term_value, pauli.cpp:79-85 */
+            uint64_t col = row ^ flip[t];
+            double complex v = base[t];
+            if (__builtin_parityll(col & zm[t])) v = -v;
+            int j = m++;
+            while (j > 0 && ec[j - 1] > col) { ec[j] = ec[j - 1]; ev[j] = ev[j - 1]; --j; }
+            ec[j] = col;
+            ev[j] = v;
+        }
+        int k = 0;
+        while (k < m) {
+            double complex v = ev[k];
+            int k2 = k + 1;
+            while (k2 < m && ec[k2] == ec[k]) v += ev[k2++];
+            if (v != 0.0) {
+                if (rows && total < capacity) {
+                    rows[total] = (long long)row;
+                    cols[total] = (long long)ec[k];
+                    vals[total] = v;
+                }
+                ++total;
+            }
+            k = k2;
+        }
+    }
+    free(flip); free(zm); free(base); free(ec); free(ev);
+    return total;
+}
+
+/* ------------------------------------------------------------------------ */
 /* model builders                                                            */
 /* ------------------------------------------------------------------------ */
 typedef struct { double d; int i, j; } pair_t;

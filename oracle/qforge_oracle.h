@@ -114,6 +114,12 @@ int qo_heisenberg_terms(int n, int pbc, double jx, double jy, double jz, double*
 void qo_random_pauli_sum(int n, int terms, qo_rng* rng, int real_weights, double* w_re,
                          double* w_im, int8_t* codes);
 
+/* pauli_sum_to_coo (src/pauli.cpp:89-153): returns nnz; with non-NULL outputs
+ * (capacity >= nnz) fills canonical row-major triplets. */
+long long qo_pauli_sum_to_coo(int n, int n_terms, const double* w_re, const double* w_im,
+                              const int8_t* codes, long long* rows, long long* cols,
+                              double complex* vals, long long capacity);
+
 const char* qo_last_error(void);
 
 #ifdef __cplusplus

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -171,6 +172,7 @@ struct qf_ctx {
     cudaStream_t stream = nullptr;
     size_t budget = 0;
     DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init, gmat;
+    DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_rows, coo_cols, coo_vals;
     HostBuf pin;
     // NCCL
     NcclComm comm = nullptr;
@@ -501,7 +503,8 @@ int qf_ctx_destroy(qf_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.commDestroy(c->comm);
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
-                      &c->gmat})
+                      &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_rows,
+                      &c->coo_cols, &c->coo_vals})
         b->release();
     c->pin.release();
     for (auto& ev : c->ev_pool) cudaEventDestroy(ev);
@@ -983,6 +986,92 @@ int qf_adam_step_device(qf_ctx* ctx, int batch, int P, double* th, double* m, do
     const double c1 = 1.0 - std::pow(b1, t);
     const double c2 = 1.0 - std::pow(b2, t);
     QF_CUDA(launch_adam(batch * P, th, m, v, g, lr, b1, b2, eps, c1, c2, ctx->stream));
+    return QF_OK;
+}
+
+int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int device_buffers, int64_t* rows,
+                        int64_t* cols, double* vals, int64_t capacity, int64_t* nnz) {
+    // reference src/pauli.cpp:89-153
+    if (!ctx || !obs || !nnz) return set_err(QF_EINVAL, "qf_pauli_sum_to_coo: null argument");
+    const int n = obs->n;
+    if (n < 1) return set_err(QF_EINVAL, "pauli_sum_to_coo: empty system");
+    if (n > n_guard) return set_err(QF_EINVAL, "pauli_sum_to_coo: qubit count exceeds memory guard");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const int T = (int)obs->w_re.size();
+    if (T == 0) {
+        *nnz = 0;
+        return QF_OK;
+    }
+    // group terms by flip mask (ascending), input order inside a group
+    std::map<uint64_t, std::vector<CooTerm>> by_flip;
+    static const double ip[4][2] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    for (int t = 0; t < T; ++t) {
+        uint64_t flip = 0, z = 0;
+        int y = 0;
+        for (int i = 0; i < n; ++i) {
+            const int c = obs->codes[(size_t)t * n + i];
+            const uint64_t bit = 1ull << (n - 1 - i);
+            if (c == 1) flip |= bit;
+            if (c == 2) { flip |= bit; z |= bit; ++y; }
+            if (c == 3) z |= bit;
+        }
+        const double wr = obs->w_re[t], wi = obs->w_im[t];
+        CooTerm ct;
+        ct.z = z;
+        ct.c_re = wr * ip[y & 3][0] - wi * ip[y & 3][1];
+        ct.c_im = wr * ip[y & 3][1] + wi * ip[y & 3][0];
+        by_flip[flip].push_back(ct);
+    }
+    std::vector<CooGroup> groups;
+    std::vector<CooTerm> terms;
+    for (auto& [f, ts] : by_flip) {
+        CooGroup g;
+        g.flip = f;
+        g.term_begin = (int)terms.size();
+        terms.insert(terms.end(), ts.begin(), ts.end());
+        g.term_end = (int)terms.size();
+        groups.push_back(g);
+    }
+    const int64_t dim = (int64_t)1 << n;
+    QF_CUDA(upload(ctx->coo_groups, groups, s));
+    QF_CUDA(upload(ctx->coo_terms, terms, s));
+    QF_CUDA(ctx->coo_off.reserve((size_t)(2 * dim + 2) * 8));  // counts [dim + 1] then offsets [dim + 1]
+    int64_t* counts = (int64_t*)ctx->coo_off.p;
+    int64_t* offsets = counts + dim + 1;
+    QF_CUDA(cudaMemsetAsync(counts + dim, 0, 8, s));
+    QF_CUDA(launch_coo_count((const CooGroup*)ctx->coo_groups.p, (int)groups.size(),
+                             (const CooTerm*)ctx->coo_terms.p, n, counts, s));
+    size_t scratch = 0;
+    QF_CUDA(coo_scan(counts, offsets, dim, nullptr, &scratch, s));
+    QF_CUDA(ctx->coo_scratch.reserve(std::max<size_t>(scratch, 16)));
+    QF_CUDA(coo_scan(counts, offsets, dim, ctx->coo_scratch.p, &scratch, s));
+    int64_t total = 0;
+    QF_CUDA(cudaMemcpyAsync(&total, offsets + dim, 8, cudaMemcpyDeviceToHost, s));
+    QF_CUDA(cudaStreamSynchronize(s));
+    *nnz = total;
+    if (!rows && !cols && !vals) return QF_OK;
+    if (!rows || !cols || !vals || capacity < total)
+        return set_err(QF_EINVAL, "qf_pauli_sum_to_coo: output buffers missing or too small");
+    int64_t *dr = rows, *dc = cols;
+    double2* dv = reinterpret_cast<double2*>(vals);
+    if (!device_buffers) {
+        QF_CUDA(ctx->coo_rows.reserve(std::max<size_t>(16, (size_t)total * 8)));
+        QF_CUDA(ctx->coo_cols.reserve(std::max<size_t>(16, (size_t)total * 8)));
+        QF_CUDA(ctx->coo_vals.reserve(std::max<size_t>(16, (size_t)total * 16)));
+        dr = (int64_t*)ctx->coo_rows.p;
+        dc = (int64_t*)ctx->coo_cols.p;
+        dv = (double2*)ctx->coo_vals.p;
+    }
+    QF_CUDA(launch_coo_write((const CooGroup*)ctx->coo_groups.p, (int)groups.size(), (const CooTerm*)ctx->coo_terms.p,
+                             n, offsets, dr, dc, dv, s));
+    ctx->launches += 3;
+    if (!device_buffers && total > 0) {
+        QF_CUDA(cudaMemcpyAsync(rows, dr, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaMemcpyAsync(cols, dc, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaMemcpyAsync(vals, dv, (size_t)total * 16, cudaMemcpyDeviceToHost, s));
+    }
+    QF_CUDA(cudaStreamSynchronize(s));
     return QF_OK;
 }
 

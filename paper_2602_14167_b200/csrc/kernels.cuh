@@ -48,3 +48,26 @@ cudaError_t launch_convert_state(int prec, const void* src, double* dst, int64_t
                                  cudaStream_t s);
 
 }  // namespace qfb
+
+namespace qfb {
+
+// ---- pauli_sum_to_coo (reference src/pauli.cpp:89-153) ----
+struct CooGroup {          // terms sharing one flip mask
+    uint64_t flip;
+    int32_t term_begin, term_end;
+};
+struct CooTerm {
+    uint64_t z;
+    double c_re, c_im;     // w * i^y
+};
+// nnz per row (values summed per flip group, exact zeros dropped)
+cudaError_t launch_coo_count(const CooGroup* g, int n_groups, const CooTerm* t, int n, int64_t* counts,
+                             cudaStream_t s);
+// exclusive scan counts -> offsets (offsets[dim] = nnz); scratch via cub
+cudaError_t coo_scan(const int64_t* counts, int64_t* offsets, int64_t dim, void* scratch, size_t* scratch_bytes,
+                     cudaStream_t s);
+// rows / cols ascending per row, complex128 values
+cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n, const int64_t* offsets,
+                             int64_t* rows, int64_t* cols, double2* vals, cudaStream_t s);
+
+}  // namespace qfb

@@ -257,6 +257,32 @@ def expectation(ctx: Context, prog: Program, obs: Observable, theta: np.ndarray)
     return complex(out[0], out[1])
 
 
+def pauli_sum_to_coo(ctx: Context, obs: Observable, n_guard: int = 26, device: bool = False):
+    """Canonical COO of the observable (qf_pauli_sum_to_coo): numpy arrays
+    (rows, cols, vals complex128), or torch CUDA tensors when device=True."""
+    nnz = ctypes.c_int64()
+    check(ctx.lib.qf_pauli_sum_to_coo(ctx.handle, obs.handle, n_guard, 0, None, None, None, 0, ctypes.byref(nnz)))
+    m = nnz.value
+    if device:
+        import torch
+        dev = torch.device("cuda", ctx.device)
+        rows = torch.empty(m, dtype=torch.int64, device=dev)
+        cols = torch.empty(m, dtype=torch.int64, device=dev)
+        vals = torch.empty(m, dtype=torch.complex128, device=dev)
+        ptr = lambda t: ctypes.c_void_p(t.data_ptr()) if m else None  # noqa: E731
+        check(ctx.lib.qf_pauli_sum_to_coo(ctx.handle, obs.handle, n_guard, 1, ptr(rows), ptr(cols), ptr(vals), m,
+                                          ctypes.byref(nnz)))
+        return rows, cols, vals
+    rows = np.empty(m, dtype=np.int64)
+    cols = np.empty(m, dtype=np.int64)
+    vals = np.empty(m, dtype=np.complex128)
+    if m:
+        check(ctx.lib.qf_pauli_sum_to_coo(ctx.handle, obs.handle, n_guard, 0, ctypes.c_void_p(rows.ctypes.data),
+                                          ctypes.c_void_p(cols.ctypes.data), ctypes.c_void_p(vals.ctypes.data), m,
+                                          ctypes.byref(nnz)))
+    return rows, cols, vals
+
+
 def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
                      eps=1e-8) -> None:
     B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))

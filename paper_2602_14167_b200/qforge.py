@@ -435,6 +435,32 @@ def random_pauli_sum(n: int, terms: int, rng, real_weights: bool = True) -> Paul
     return h
 
 
+class SparseCOO:  # include/qforge/sparse.hpp:12-36 (canonical coordinate format)
+    def __init__(self, dim: int = 0, rows=None, cols=None, vals=None):
+        self.dim = dim
+        self.rows = np.zeros(0, np.int64) if rows is None else rows
+        self.cols = np.zeros(0, np.int64) if cols is None else cols
+        self.vals = np.zeros(0, np.complex128) if vals is None else vals
+
+    def nnz(self) -> int:
+        return int(len(self.vals))
+
+    def to_dense(self) -> np.ndarray:  # sparse.cpp:59-65 (test helper)
+        m = np.zeros((self.dim, self.dim), dtype=np.complex128)
+        np.add.at(m, (self.rows, self.cols), self.vals)
+        return m
+
+
+def pauli_sum_to_coo(h: PauliSum, n_guard: int = 26, workers: int = 1) -> SparseCOO:
+    """pauli.cpp:89-153 on the GPU (qf_pauli_sum_to_coo); `workers` is accepted for
+    signature compatibility (the output never depends on it)."""
+    _require(h.n >= 1, "pauli_sum_to_coo: empty system")
+    _require(h.n <= n_guard, "pauli_sum_to_coo: qubit count exceeds memory guard")
+    ctx = _eng.default_context()
+    rows, cols, vals = _eng.pauli_sum_to_coo(ctx, h.observable(ctx), n_guard)
+    return SparseCOO(1 << h.n, rows, cols, vals)
+
+
 def expectation_pauli(psi: StateVector, obs: PauliSum) -> complex:  # circuit.cpp:319-347
     _require(psi.d == 2, "expectation_pauli: qubits only")
     _require(obs.n == psi.n, "expectation_pauli: size mismatch")

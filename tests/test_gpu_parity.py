@@ -231,3 +231,30 @@ def test_all_gate_kinds_state_and_expectation(ctx):
         assert np.abs(psi - ref).max() <= TOL[prec] * 10
         e = engine.expectation(ctx, prog, engine.Observable(ctx, 15, h.codes, h.wr + 1j * h.wi), np.zeros(0))
         assert abs(e - eref) <= TOL[prec] * max(1.0, abs(eref)) * 10
+
+
+def test_pauli_sum_to_coo_matches_oracle(ctx):
+    """pauli_sum_to_coo (pauli.cpp:89-153): identical canonical triplets."""
+    from paper_2602_14167_b200 import qforge as qf
+    cases = [po.tfim(10, 1.3), po.heisenberg(9, 1.0, 0.5, 0.25), po.random_sum(8, 40, po.Rng(3), False),
+             po.random_sum(7, 300, po.Rng(4), True)]  # 300 terms: block-per-row sort path
+    for ho in cases:
+        r0, c0, v0 = po.pauli_sum_to_coo(ho)
+        r, c, v = engine.pauli_sum_to_coo(ctx, engine.Observable(ctx, ho.n, ho.codes, ho.wr + 1j * ho.wi))
+        assert np.array_equal(r, r0) and np.array_equal(c, c0)
+        assert np.abs(v - v0).max() <= 1e-12 * max(1.0, np.abs(v0).max())
+    h = qf.tfim_terms(qf.build_lattice("chain", [6], [False]), 0.7)
+    coo = qf.pauli_sum_to_coo(h)
+    codes, w = h.arrays()
+    P = [np.eye(2), np.array([[0, 1], [1, 0]]), np.array([[0, -1j], [1j, 0]]), np.diag([1, -1])]
+    dense = np.zeros((64, 64), complex)
+    for t in range(len(w)):
+        m = np.eye(1)
+        for cc in codes[t]:
+            m = np.kron(m, P[cc])
+        dense += w[t] * m
+    assert np.abs(coo.to_dense() - dense).max() < 1e-12
+    with pytest.raises(ValueError, match="memory guard"):
+        qf.pauli_sum_to_coo(qf.tfim_terms(qf.build_lattice("chain", [27], [False]), 1.0))
+    empty = qf.PauliSum(3)
+    assert qf.pauli_sum_to_coo(empty).nnz() == 0

@@ -349,3 +349,16 @@ def test_model_builders():
     assert po.heisenberg(26, 1.0, 1.0, 0.5).codes.shape == (75, 26)
     # periodic chain: (0, n-1) joins the first shell (lattice.cpp:29-48, 89-122)
     assert len(po.tfim(5, 1.0, pbc=True).wr) == 10
+
+
+def test_oracle_coo_matches_dense():
+    """test_hamiltonian.cpp:18-50: COO lowering equals the dense Kronecker sum."""
+    for ho in (po.tfim(5, 0.7), po.heisenberg(4, 1.0, 1.0, 1.0), po.random_sum(5, 12, po.Rng(8), False)):
+        r, c, v = po.pauli_sum_to_coo(ho)
+        m = np.zeros((1 << ho.n, 1 << ho.n), complex)
+        np.add.at(m, (r, c), v)
+        assert np.abs(m - pauli_sum_dense(ho)).max() < 1e-12
+        assert np.all(np.diff(r) >= 0)
+        same = r[1:] == r[:-1]
+        assert np.all(c[1:][same] > c[:-1][same])
+        assert np.all(v != 0)
