@@ -6,6 +6,8 @@
 //   adjoint sweeps with gradient taps -> fixed-order reductions.
 // The reference evaluates 1 + 2P full energies per gradient
 // (src/variational.cpp:54-81); this evaluates one forward and one adjoint pass.
+#include <array>
+#include <atomic>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -165,6 +167,7 @@ struct qf_observable {
     bool term_shard = false;
     int shard_world = 0;   // term-sharded sub-plan cache key
     ObsDev shard_dev[2];
+    uint64_t uid = 0;      // identity for the context's COO offset cache
 };
 
 struct qf_ctx {
@@ -172,7 +175,10 @@ struct qf_ctx {
     cudaStream_t stream = nullptr;
     size_t budget = 0;
     DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init, gmat;
-    DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_rows, coo_cols, coo_vals;
+    DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_nodes, coo_rows, coo_cols, coo_vals;
+    uint64_t coo_uid = 0;  // observable whose groups/terms/offsets coo_* currently hold (0: none)
+    int coo_n_groups = 0, coo_n_events = 0, coo_n_terms = 0;
+    int64_t coo_total = 0;
     HostBuf pin;
     // NCCL
     NcclComm comm = nullptr;
@@ -503,7 +509,7 @@ int qf_ctx_destroy(qf_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.commDestroy(c->comm);
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
-                      &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_rows,
+                      &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_nodes, &c->coo_rows,
                       &c->coo_cols, &c->coo_vals})
         b->release();
     c->pin.release();
@@ -756,8 +762,10 @@ int qf_observable_create(qf_ctx* ctx, int n, int n_terms, const int8_t* codes, c
     if (n_terms < 0 || (n_terms > 0 && (!codes || !w_re)))
         return set_err(QF_EINVAL, "qf_observable_create: bad terms");
     qf_observable* o = new qf_observable();
+    static std::atomic<uint64_t> next_uid{1};
     o->ctx = ctx;
     o->n = n;
+    o->uid = next_uid++;
     o->codes.assign(codes, codes + (size_t)n_terms * n);
     o->w_re.assign(w_re, w_re + n_terms);
     o->w_im.assign(n_terms, 0.0);
@@ -1003,6 +1011,14 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
         *nnz = 0;
         return QF_OK;
     }
+    const int64_t dim = (int64_t)1 << n;
+    int64_t* offsets = nullptr;
+    int64_t total = 0;
+    if (ctx->coo_uid == obs->uid) {  // sizing call already counted this observable: reuse its offsets
+        offsets = (int64_t*)ctx->coo_off.p + dim + 1;
+        total = ctx->coo_total;
+    } else {
+    ctx->coo_uid = 0;
     // group terms by flip mask (ascending), input order inside a group
     std::map<uint64_t, std::vector<CooTerm>> by_flip;
     static const double ip[4][2] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
@@ -1033,22 +1049,50 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
         g.term_end = (int)terms.size();
         groups.push_back(g);
     }
-    const int64_t dim = (int64_t)1 << n;
+    // flip-trie rank events for the tiled writer (groups ascend by flip; kernels.cuh CooEvent)
+    std::vector<CooEvent> events;
+    if (groups.size() <= 32) {
+        auto bits = [](int a, int b) { return (uint32_t)((((uint64_t)1 << b) - 1) & ~(((uint64_t)1 << a) - 1)); };
+        std::vector<std::array<int, 2>> stack{{0, (int)groups.size()}};
+        while (!stack.empty()) {
+            const auto [lo, hi] = stack.back();
+            stack.pop_back();
+            if (hi - lo < 2) continue;
+            const int d = 63 - __builtin_clzll(groups[lo].flip ^ groups[hi - 1].flip);
+            int mid = lo;
+            while (!((groups[mid].flip >> d) & 1)) ++mid;
+            events.push_back({lo, d, 1, bits(mid, hi)});
+            events.push_back({mid, d, -1, bits(lo, hi)});
+            events.push_back({hi, d, 1, bits(lo, mid)});
+            stack.push_back({lo, mid});
+            stack.push_back({mid, hi});
+        }
+        std::stable_sort(events.begin(), events.end(),
+                         [](const CooEvent& x, const CooEvent& y) { return x.pos < y.pos; });
+    }
+    if (events.empty()) events.push_back({1 << 30, 0, 0, 0});
+    ctx->coo_n_events = (int)events.size();
+    QF_CUDA(upload(ctx->coo_nodes, events, s));
     QF_CUDA(upload(ctx->coo_groups, groups, s));
     QF_CUDA(upload(ctx->coo_terms, terms, s));
     QF_CUDA(ctx->coo_off.reserve((size_t)(2 * dim + 2) * 8));  // counts [dim + 1] then offsets [dim + 1]
     int64_t* counts = (int64_t*)ctx->coo_off.p;
-    int64_t* offsets = counts + dim + 1;
+    offsets = counts + dim + 1;
     QF_CUDA(cudaMemsetAsync(counts + dim, 0, 8, s));
     QF_CUDA(launch_coo_count((const CooGroup*)ctx->coo_groups.p, (int)groups.size(),
-                             (const CooTerm*)ctx->coo_terms.p, n, counts, s));
+                             (const CooTerm*)ctx->coo_terms.p, (int)terms.size(), n, counts, s));
     size_t scratch = 0;
     QF_CUDA(coo_scan(counts, offsets, dim, nullptr, &scratch, s));
     QF_CUDA(ctx->coo_scratch.reserve(std::max<size_t>(scratch, 16)));
     QF_CUDA(coo_scan(counts, offsets, dim, ctx->coo_scratch.p, &scratch, s));
-    int64_t total = 0;
     QF_CUDA(cudaMemcpyAsync(&total, offsets + dim, 8, cudaMemcpyDeviceToHost, s));
     QF_CUDA(cudaStreamSynchronize(s));
+    ctx->launches += 2;
+    ctx->coo_uid = obs->uid;
+    ctx->coo_n_groups = (int)groups.size();
+    ctx->coo_n_terms = (int)terms.size();
+    ctx->coo_total = total;
+    }
     *nnz = total;
     if (!rows && !cols && !vals) return QF_OK;
     if (!rows || !cols || !vals || capacity < total)
@@ -1063,9 +1107,9 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
         dc = (int64_t*)ctx->coo_cols.p;
         dv = (double2*)ctx->coo_vals.p;
     }
-    QF_CUDA(launch_coo_write((const CooGroup*)ctx->coo_groups.p, (int)groups.size(), (const CooTerm*)ctx->coo_terms.p,
-                             n, offsets, dr, dc, dv, s));
-    ctx->launches += 3;
+    QF_CUDA(launch_coo_write((const CooGroup*)ctx->coo_groups.p, ctx->coo_n_groups, (const CooTerm*)ctx->coo_terms.p,
+                             ctx->coo_n_terms, (const CooEvent*)ctx->coo_nodes.p, ctx->coo_n_events, n, offsets, dr, dc, dv, s));
+    ctx->launches += 1;
     if (!device_buffers && total > 0) {
         QF_CUDA(cudaMemcpyAsync(rows, dr, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
         QF_CUDA(cudaMemcpyAsync(cols, dc, (size_t)total * 8, cudaMemcpyDeviceToHost, s));

@@ -60,14 +60,25 @@ struct CooTerm {
     uint64_t z;
     double c_re, c_im;     // w * i^y
 };
+// Column ranking for <= 32 flip groups.  Binary trie over the ascending flip
+// masks: an internal node at bit d splits the group range [lo, hi) at mid (first
+// flip with bit d set), and rows with bit d set list [mid, hi) before [lo, mid).
+// As a difference array over the group index each such node contributes
+// +cnt[mid,hi) at lo, -cnt[lo,hi) at mid and +cnt[lo,mid) at hi; one event per
+// contribution, sorted by position (cnt = non-zero groups under `mask`).
+struct CooEvent {
+    int32_t pos, d, sign;
+    uint32_t mask;
+};
 // nnz per row (values summed per flip group, exact zeros dropped)
-cudaError_t launch_coo_count(const CooGroup* g, int n_groups, const CooTerm* t, int n, int64_t* counts,
+cudaError_t launch_coo_count(const CooGroup* g, int n_groups, const CooTerm* t, int n_terms, int n, int64_t* counts,
                              cudaStream_t s);
 // exclusive scan counts -> offsets (offsets[dim] = nnz); scratch via cub
 cudaError_t coo_scan(const int64_t* counts, int64_t* offsets, int64_t dim, void* scratch, size_t* scratch_bytes,
                      cudaStream_t s);
 // rows / cols ascending per row, complex128 values
-cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n, const int64_t* offsets,
+cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n_terms, const CooEvent* ev,
+                             int n_ev, int n, const int64_t* offsets,
                              int64_t* rows, int64_t* cols, double2* vals, cudaStream_t s);
 
 }  // namespace qfb

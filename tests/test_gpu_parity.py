@@ -237,7 +237,18 @@ def test_pauli_sum_to_coo_matches_oracle(ctx):
     """pauli_sum_to_coo (pauli.cpp:89-153): identical canonical triplets."""
     from paper_2602_14167_b200 import qforge as qf
     cases = [po.tfim(10, 1.3), po.heisenberg(9, 1.0, 0.5, 0.25), po.random_sum(8, 40, po.Rng(3), False),
-             po.random_sum(7, 300, po.Rng(4), True)]  # 300 terms: block-per-row sort path
+             po.random_sum(7, 300, po.Rng(4), True),  # 300 terms: block-per-row sort path
+             po.random_sum(9, 50, po.Rng(5), False),  # 33..64 groups: thread-per-row path
+             po.random_sum(1, 3, po.Rng(6), False), po.random_sum(2, 9, po.Rng(7), True)]
+    # exact cancellations: XX + YY vanishes on rows with equal bits, Z0 - Z1 likewise
+    codes = np.zeros((6, 5), np.int8)
+    codes[0, :2] = 1
+    codes[1, :2] = 2
+    codes[2, 0] = 3
+    codes[3, 1] = 3
+    codes[4, 3] = 1
+    codes[5, 2:4] = [1, 3]
+    cases.append(po.Hamil(5, codes, np.array([1.0, 1.0, 0.5, -0.5, 0.25, 0.25 + 0.5j])))
     for ho in cases:
         r0, c0, v0 = po.pauli_sum_to_coo(ho)
         r, c, v = engine.pauli_sum_to_coo(ctx, engine.Observable(ctx, ho.n, ho.codes, ho.wr + 1j * ho.wi))
