@@ -17,6 +17,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
+#include <map>
+#include <set>
 #include <mutex>
 #include <sstream>
 #include <thread>
@@ -114,6 +117,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     o.s += kPrelude;
     o.s += "\n";
     o("namespace qfb {");
+    const size_t decl_pos = o.s.size();  // namespace-scope tables are inserted here
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) qf_sweep(const SweepArgs a) {", T, minb);
     o("  typedef %s V; typedef %s RT;", Vt, RTt);
     o("  extern __shared__ __align__(16) unsigned char smem_raw[];");
@@ -264,6 +268,12 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
     }
     if (!pipe) o("  __syncthreads();");
+    // Uniform (per-state) products of a diagonal run's register-bit factors are
+    // built once per CTA into shared memory (the prologue is inserted here once
+    // every run is known); each entry lists its factor indices into smat.
+    const size_t stab_pos = o.s.size();
+    const bool use_stab = !pipe;
+    std::vector<std::vector<int>> stab_entries;
 
     std::vector<const char*> arrs = {"x"};
     if (bwd) arrs.push_back("y");
@@ -342,13 +352,75 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             o("    { // fused diagonal run (%d ops)", oe - ob);
             // taps first: v_l = Im(conj(lambda_l) psi_l) is invariant under diagonal
             // unitaries applied to both states, so every tap of the run shares it
-            bool any_tap = false;
-            for (int oi = ob; oi < oe; ++oi) any_tap |= pass.ops[oi].kind == DK_TZ || pass.ops[oi].kind == DK_TZZ;
-            if (any_tap)
-                for (int l = 0; l < NR; ++l) o("      const RT v%d_%d = imcv(y%d, x%d);", id, l, phys[l], phys[l]);
+            // Signed sums sum_l (-1)^{popc(l & mask)} v_l for every register-bit mask the
+            // run's taps need come from one memoised Walsh tree (pair sums / differences
+            // along register bit 0, then 1, ...); c64 keeps v_l as packed lane pairs
+            // (FMUL2 / FADD2) and differences the lanes once per tap.
+            std::map<int, std::string> wsum;
+            {
+                std::set<int> masks;
+                for (int oi = ob; oi < oe; ++oi) {
+                    const DevOp& op = pass.ops[oi];
+                    if (op.kind != DK_TZ && op.kind != DK_TZZ) continue;
+                    BitSrc s0 = src(op.pos0);
+                    BitSrc s1 = op.kind == DK_TZZ ? src(op.pos1) : BitSrc{};
+                    int m = 0;
+                    if (s0.rb >= 0) m ^= 1 << s0.rb;
+                    if (op.kind == DK_TZZ && s1.rb >= 0) m ^= 1 << s1.rb;
+                    masks.insert(m);
+                }
+                if (!masks.empty()) {
+                    const char* TT = dbl ? "RT" : "V";
+                    std::vector<std::string> vec(NR);
+                    for (int l = 0; l < NR; ++l) {
+                        vec[l] = "v" + std::to_string(id) + "_" + std::to_string(l);
+                        if (dbl)
+                            o("      const RT %s = imcv(y%d, x%d);", vec[l].c_str(), phys[l], phys[l]);
+                        else
+                            o("      const V %s = jim2(y%d, x%d);", vec[l].c_str(), phys[l], phys[l]);
+                    }
+                    int wc = 0;
+                    std::function<std::map<int, std::string>(const std::vector<std::string>&, const std::set<int>&)> walsh =
+                        [&](const std::vector<std::string>& v, const std::set<int>& ms) {
+                            std::map<int, std::string> res;
+                            if (v.size() == 1) {
+                                res[0] = v[0];
+                                return res;
+                            }
+                            std::set<int> m0, m1;
+                            for (int m : ms) ((m & 1) ? m1 : m0).insert(m >> 1);
+                            for (int par = 0; par < 2; ++par) {
+                                const std::set<int>& mm = par ? m1 : m0;
+                                if (mm.empty()) continue;
+                                std::vector<std::string> h(v.size() / 2);
+                                for (size_t j = 0; j < h.size(); ++j) {
+                                    h[j] = "w" + std::to_string(id) + "_" + std::to_string(wc++);
+                                    if (dbl)
+                                        o("      const RT %s = %s %c %s;", h[j].c_str(), v[2 * j].c_str(), par ? '-' : '+',
+                                          v[2 * j + 1].c_str());
+                                    else
+                                        o("      const V %s = %s(%s, %s);", h[j].c_str(), par ? "jsub2" : "jadd2",
+                                          v[2 * j].c_str(), v[2 * j + 1].c_str());
+                                }
+                                for (auto& kv : walsh(h, mm)) res[(kv.first << 1) | par] = kv.second;
+                            }
+                            return res;
+                        };
+                    for (auto& kv : walsh(vec, masks)) {
+                        const std::string nm = "W" + std::to_string(id) + "_" + std::to_string(kv.first);
+                        if (dbl)
+                            o("      const RT %s = %s;", nm.c_str(), kv.second.c_str());
+                        else
+                            o("      const RT %s = %s.x - %s.y;", nm.c_str(), kv.second.c_str(), kv.second.c_str());
+                        wsum[kv.first] = nm;
+                    }
+                    (void)TT;
+                }
+            }
             std::vector<std::string> rt_factors;                   // per-thread scalars
             std::vector<std::vector<std::pair<std::string, std::string>>> perbit(R);  // (f0, f1) per register bit
-            struct D2s { int r0, r1; std::string d[4]; };
+            std::vector<std::vector<std::pair<int, int>>> perbit_idx(R);  // their smat indices (-1: per-thread)
+            struct D2s { int r0, r1; std::string d[4]; int moff = 0; };
             std::vector<D2s> d2s;
             for (int oi = ob; oi < oe; ++oi) {
                 const DevOp& op = pass.ops[oi];
@@ -356,14 +428,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 if (op.kind == DK_TZ || op.kind == DK_TZZ) {
                     BitSrc s0 = src(op.pos0);
                     BitSrc s1 = op.kind == DK_TZZ ? src(op.pos1) : BitSrc{};
-                    std::string sum;
-                    o("      { RT s = 0;");
-                    for (int l = 0; l < NR; ++l) {
-                        int sg = 0;
-                        if (s0.rb >= 0) sg ^= (l >> s0.rb) & 1;
-                        if (op.kind == DK_TZZ && s1.rb >= 0) sg ^= (l >> s1.rb) & 1;
-                        o("        s %s= v%d_%d;", sg ? "-" : "+", id, l);
-                    }
+                    int m = 0;
+                    if (s0.rb >= 0) m ^= 1 << s0.rb;
+                    if (op.kind == DK_TZZ && s1.rb >= 0) m ^= 1 << s1.rb;
+                    o("      { RT s = %s;", wsum.at(m).c_str());
                     std::string rt;
                     if (s0.rb < 0) rt = s0.expr;
                     if (op.kind == DK_TZZ && s1.rb < 0) rt = rt.empty() ? s1.expr : "(" + rt + " ^ " + s1.expr + ")";
@@ -375,9 +443,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 if (op.kind == DK_D1) {
                     o("      const V %s_0 = smat[%d], %s_1 = smat[%d];", nm.c_str(), op.moff, nm.c_str(), op.moff + 1);
                     BitSrc s0 = src(op.pos0);
-                    if (s0.rb >= 0)
+                    if (s0.rb >= 0) {
                         perbit[s0.rb].push_back({nm + "_0", nm + "_1"});
-                    else
+                        perbit_idx[s0.rb].push_back({op.moff, op.moff + 1});
+                    } else
                         rt_factors.push_back("(" + s0.expr + " ? " + nm + "_1 : " + nm + "_0)");
                 } else {  // DK_D2
                     o("      const V %s_0 = smat[%d], %s_1 = smat[%d], %s_2 = smat[%d], %s_3 = smat[%d];", nm.c_str(),
@@ -390,21 +459,86 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         o("      const V %s_e0 = %s ? %s_1 : %s_0, %s_e1 = %s ? %s_3 : %s_2;", nm.c_str(), s1.expr.c_str(),
                           nm.c_str(), nm.c_str(), nm.c_str(), s1.expr.c_str(), nm.c_str(), nm.c_str());
                         perbit[s0.rb].push_back({nm + "_e0", nm + "_e1"});
+                        perbit_idx[s0.rb].push_back({-1, -1});
                     } else if (s0.rb < 0 && s1.rb >= 0) {
                         o("      const V %s_e0 = %s ? %s_2 : %s_0, %s_e1 = %s ? %s_3 : %s_1;", nm.c_str(), s0.expr.c_str(),
                           nm.c_str(), nm.c_str(), nm.c_str(), s0.expr.c_str(), nm.c_str(), nm.c_str());
                         perbit[s1.rb].push_back({nm + "_e0", nm + "_e1"});
+                        perbit_idx[s1.rb].push_back({-1, -1});
                     } else {
                         D2s d;
                         d.r0 = s0.rb;
                         d.r1 = s1.rb;
                         for (int q = 0; q < 4; ++q) d.d[q] = nm + "_" + std::to_string(q);
+                        d.moff = op.moff;
                         d2s.push_back(d);
                     }
                 }
             }
             // combine per-thread scalars
             const bool have_c = !rt_factors.empty();
+            {
+                std::vector<int> ubits;
+                bool uniform = use_stab;
+                for (int r = 0; r < R; ++r) {
+                    bool used = !perbit[r].empty();
+                    for (auto& d : d2s) used |= d.r0 == r || d.r1 == r;
+                    if (used) ubits.push_back(r);
+                    for (auto& pi : perbit_idx[r]) uniform &= pi.first >= 0;
+                }
+                if (uniform && !ubits.empty()) {
+                    // Adjoint pass: only conj(lambda) psi products are ever used, so each
+                    // single-qubit diagonal may carry its own global phase: diag(d0, d1)
+                    // is applied as diag(1, d1 conj(d0)) and amplitudes whose register
+                    // bits are all 0 are left untouched (kRatio entries).
+                    const int kRatio = 0x8000;
+                    const int ne = 1 << ubits.size();
+                    std::vector<int> slot(ne, -1);
+                    for (int e = 0; e < ne; ++e) {
+                        std::vector<int> f;
+                        for (size_t bi = 0; bi < ubits.size(); ++bi)
+                            for (auto& pi : perbit_idx[ubits[bi]]) {
+                                if (bwd) {
+                                    if ((e >> bi) & 1) f.push_back(kRatio | pi.first);
+                                } else {
+                                    f.push_back(((e >> bi) & 1) ? pi.second : pi.first);
+                                }
+                            }
+                        for (auto& d : d2s) {
+                            const int i0 = (int)(std::find(ubits.begin(), ubits.end(), d.r0) - ubits.begin());
+                            const int i1 = (int)(std::find(ubits.begin(), ubits.end(), d.r1) - ubits.begin());
+                            f.push_back(d.moff + (((e >> i0) & 1) << 1 | ((e >> i1) & 1)));
+                        }
+                        if (f.empty()) continue;  // identity
+                        slot[e] = (int)stab_entries.size();
+                        stab_entries.push_back(f);
+                    }
+                    if (have_c) {
+                        o("      V c%d = %s;", id, rt_factors[0].c_str());
+                        for (size_t q = 1; q < rt_factors.size(); ++q)
+                            o("      c%d = cmul(c%d, %s);", id, id, rt_factors[q].c_str());
+                    }
+                    for (int e = 0; e < ne; ++e) {
+                        if (slot[e] < 0) {
+                            if (have_c) o("      const V u%d_%d = c%d;", id, e, id);
+                        } else if (have_c) {
+                            o("      const V u%d_%d = jcmul(stab[%d], c%d);", id, e, slot[e], id);
+                        } else {
+                            o("      const V u%d_%d = stab[%d];", id, e, slot[e]);
+                        }
+                    }
+                    for (const char* A : arrs)
+                        for (int l = 0; l < NR; ++l) {
+                            int e = 0;
+                            for (size_t bi = 0; bi < ubits.size(); ++bi)
+                                if ((l >> ubits[bi]) & 1) e |= 1 << bi;
+                            if (slot[e] < 0 && !have_c) continue;
+                            o("      %s%d = jcmul(%s%d, u%d_%d);", A, phys[l], A, phys[l], id, e);
+                        }
+                    o("    }");
+                    return;
+                }
+            }
             if (have_c) {
                 o("      V c%d = %s;", id, rt_factors[0].c_str());
                 for (size_t q = 1; q < rt_factors.size(); ++q) o("      c%d = cmul(c%d, %s);", id, id, rt_factors[q].c_str());
@@ -544,6 +678,26 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     break;
                 }
                 case DK_TX: case DK_TY: {
+                    if (!dbl) {  // c64: packed lane-pair accumulators (2 FFMA2 per amplitude pair)
+                        const auto prs = pairs(op.rb0);
+                        o("    { V P, M;");
+                        for (size_t q = 0; q < prs.size(); ++q) {
+                            const int f = prs[q].first, g = prs[q].second;
+                            if (op.kind == DK_TX) {  // Im(conj(y_f) x_g) + Im(conj(y_g) x_f)
+                                if (q == 0) o("      P = jim2(y%d, x%d); M = jim2(y%d, x%d);", f, g, g, f);
+                                else o("      P = jim2a(y%d, x%d, P); M = jim2a(y%d, x%d, M);", f, g, g, f);
+                            } else {  // Re(conj(y_g) x_f) - Re(conj(y_f) x_g)
+                                if (q == 0) o("      P = jre2(y%d, x%d); M = jre2(y%d, x%d);", g, f, f, g);
+                                else o("      P = jre2a(y%d, x%d, P); M = jre2a(y%d, x%d, M);", g, f, f, g);
+                            }
+                        }
+                        if (op.kind == DK_TX)
+                            o("      stg[%d * %d + tid] = (P.x - P.y) + (M.x - M.y); }", op.tap % S, T);
+                        else
+                            o("      stg[%d * %d + tid] = (P.x + P.y) - (M.x + M.y); }", op.tap % S, T);
+                        emit_flush_if_full(op.tap);
+                        break;
+                    }
                     o("    { RT s = 0;");
                     if (op.kind == DK_TX) {
                         for (auto pr : pairs(op.rb0))
@@ -608,6 +762,39 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     }
     o("}");
     o("}  // namespace qfb");
+    if (!stab_entries.empty()) {
+        size_t nf = 1;
+        for (auto& f : stab_entries) nf = std::max(nf, f.size());
+        const size_t ne = stab_entries.size();
+        std::string decl = "__device__ const unsigned short qf_stab_f[" + std::to_string(ne) + "][" +
+                           std::to_string(nf) + "] = {";
+        for (size_t e = 0; e < ne; ++e) {
+            decl += e ? ",{" : "{";
+            for (size_t q = 0; q < nf; ++q) {
+                if (q) decl += ",";
+                decl += std::to_string(q < stab_entries[e].size() ? stab_entries[e][q] : 0xffff);
+            }
+            decl += "}";
+        }
+        decl += "};\n";
+        char buf[1024];
+        snprintf(buf, sizeof buf,
+                 "  __shared__ __align__(16) V stab[%zu];\n"
+                 "  for (int e = (int)tid; e < %zu; e += %d) {  // diagonal-run tables (uniform per state)\n"
+                 "    V acc; acc.x = 1; acc.y = 0;\n"
+                 "    for (int q = 0; q < %zu; ++q) {\n"
+                 "      const unsigned i = qf_stab_f[e][q];\n"
+                 "      if (i == 0xffffu) break;\n"
+                 "      if (i & 0x8000u) { V d0 = smat[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(smat[(i & 0x7fffu) + 1], d0)); }\n"
+                 "      else acc = cmul(acc, smat[i]);\n"
+                 "    }\n"
+                 "    stab[e] = acc;\n"
+                 "  }\n"
+                 "  __syncthreads();\n",
+                 ne, ne, T, nf);
+        o.s.insert(stab_pos, buf);
+        o.s.insert(decl_pos, decl);
+    }
     return o.s;
 }
 
@@ -689,6 +876,10 @@ bool read_file(const std::string& p, std::string& out) {
 }
 
 bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
+    if (const char* d = std::getenv("QF_JIT_DUMP")) {  // debugging: keep the generated source and cubin
+        const std::string base = std::string(d) + "/qf_" + std::to_string(fnv1a(src));
+        std::ofstream(base + ".cu") << src;
+    }
     std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DQF_JIT=1"};
     if (src.find("// qf-option: scalar-fp32") != std::string::npos) opts.push_back("-DQF_JIT_SCALAR=1");
     nvrtcProgram prog = nullptr;

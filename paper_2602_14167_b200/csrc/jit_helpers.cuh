@@ -98,6 +98,14 @@ __device__ __forceinline__ void jrs(double2& a0, double2& a1, double2 m0) {
     a0.x = fma(-m0.x, a1.x, a0.x);
     a0.y = fma(-m0.x, a1.y, a0.y);
 }
+// packed tap products (c64): lanes (u.x v.x, u.y v.y) sum to Re(conj(u) v);
+// lanes (u.x v.y, u.y v.x) differ to Im(conj(u) v)
+__device__ __forceinline__ float2 jre2(float2 u, float2 v) { return __fmul2_rn(u, v); }
+__device__ __forceinline__ float2 jre2a(float2 u, float2 v, float2 acc) { return __ffma2_rn(u, v, acc); }
+__device__ __forceinline__ float2 jim2(float2 u, float2 v) { return __fmul2_rn(u, swp(v)); }
+__device__ __forceinline__ float2 jim2a(float2 u, float2 v, float2 acc) { return __ffma2_rn(u, swp(v), acc); }
+__device__ __forceinline__ float2 jadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 jsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 template <typename V> __device__ __forceinline__ void jcswap(V& a, V& b, bool c) {
     const V t0 = a, t1 = b;
     a = c ? t1 : t0;
