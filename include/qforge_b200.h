@@ -136,6 +136,11 @@ int qf_plan_describe(int n_qubits, int n_ops, const qf_op* ops, const double* ma
                      int n_params, int precision, char* buf, size_t buflen, size_t* needed);
 int qf_jit_compile_check(int n_qubits, int n_ops, const qf_op* ops, const double* mats,
                          int n_mats, int n_params, int precision, int* kernels);
+/* Host-only: NVRTC compile of the specialised H|psi> kernel of a Pauli sum
+ * (codes/weights as qf_observable_create); *compiled = 0 when the sum is above
+ * the specialisation limit and the generic kernel would be used. */
+int qf_jit_hpsi_check(int n_qubits, int n_terms, const int8_t* codes, const double* w_re, const double* w_im,
+                      int precision, int* compiled);
 
 /* ---- observables (Pauli sums) ---- */
 /* codes: [n_terms][n_qubits], 0=I 1=X 2=Y 3=Z (pauli.hpp:11-17). */

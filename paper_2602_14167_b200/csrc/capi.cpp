@@ -156,6 +156,8 @@ struct ObsDev {
     ObservablePlan plan;
     DevBuf groups, terms;
     bool ready = false;
+    JitKernel hj;       // specialised H|psi> kernel (jit.hpp)
+    int hj_state = 0;   // 0 not built, 1 ready, -1 unavailable (AOT hpsi_kernel)
 };
 
 struct qf_observable {
@@ -206,6 +208,7 @@ int ensure_obs_dev(qf_observable* o, int prec, int kh, ObsDev& d, int t_begin, i
     QF_CUDA(upload(d.groups, d.plan.groups, s));
     QF_CUDA(upload(d.terms, d.plan.terms, s));
     d.ready = true;
+    d.hj_state = 0;  // plan (re)built: the specialised H|psi> kernel follows it
     (void)prec;
     return QF_OK;
 }
@@ -323,7 +326,15 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.write_lam = grads ? 1 : 0;
     ha.use_imag = 0;
     ha.epart = (double*)ctx->epart.p;
-    QF_CUDA(launch_hpsi(prec, ha, bc, s));
+    if (prog->use_jit && od->hj_state == 0) {
+        std::string err;
+        od->hj_state = ((int)od->plan.terms.size() <= kJitHpsiMaxTerms && jit_build_hpsi(od->plan, prec, od->hj, err))
+                           ? 1 : -1;
+    }
+    if (od->hj_state == 1)
+        QF_CUDA((cudaError_t)jit_launch_hpsi(od->hj, ha, tiles_h, bc, s));
+    else
+        QF_CUDA(launch_hpsi(prec, ha, bc, s));
     ctx->launches++;
     ctx->class_launches[1]++;
     ctx->bytes[1] += (double)bc * N * vs * (ha.n_groups + (grads ? 1 : 0));
@@ -743,6 +754,23 @@ int qf_jit_compile_check(int n, int n_ops, const qf_op* ops, const double* mats,
         }
     }
     if (kernels) *kernels = count;
+    return QF_OK;
+}
+
+int qf_jit_hpsi_check(int n, int n_terms, const int8_t* codes, const double* w_re, const double* w_im, int precision,
+                      int* compiled) {
+    if (n < 1 || n > 32 || n_terms < 0 || (n_terms > 0 && (!codes || !w_re)))
+        return set_err(QF_EINVAL, "qf_jit_hpsi_check: bad arguments");
+    if (precision != QF_C64 && precision != QF_C128) return set_err(QF_EINVAL, "qf_jit_hpsi_check: bad precision");
+    std::vector<double> wi(w_im ? std::vector<double>(w_im, w_im + n_terms) : std::vector<double>(n_terms, 0.0));
+    ObservablePlan plan;
+    const std::string e = build_observable_plan(n, n_terms, codes, w_re, wi.data(), geometry(precision, n).kh, plan);
+    if (!e.empty()) return set_err(QF_EINVAL, e);
+    if (compiled) *compiled = 0;
+    if ((int)plan.terms.size() > kJitHpsiMaxTerms) return QF_OK;
+    std::string cubin, err;
+    if (!jit_compile_source(jit_hpsi_source(plan, precision), cubin, err)) return set_err(QF_ERUNTIME, err);
+    if (compiled) *compiled = 1;
     return QF_OK;
 }
 

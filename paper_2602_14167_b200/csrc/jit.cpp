@@ -97,8 +97,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const int W = dbl ? 3 : 4;
     const char* Vt = dbl ? "double2" : "float2";
     const char* RTt = dbl ? "double" : "float";
-    const int minb = [] {
-        const char* e = std::getenv("QF_JIT_MINB");
+    const int minb = [bwd] {
+        const char* e = std::getenv(bwd ? "QF_JIT_MINB_BWD" : "QF_JIT_MINB_FWD");
+        if (!e) e = std::getenv("QF_JIT_MINB");
         return e ? std::max(1, atoi(e)) : 2;
     }();
     const bool allow_direct = [] {
@@ -347,9 +348,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         auto is_diagish = [&](uint8_t kd) { return kd == DK_D1 || kd == DK_D2 || kd == DK_TZ || kd == DK_TZZ; };
 
         // ---- fused run of diagonal gates and Z-type taps (they all commute) ----
-        auto flush_diag_run = [&](int ob, int oe) {
+        auto flush_diag_run = [&](const std::vector<int>& run) {
             const int id = uid++;
-            o("    { // fused diagonal run (%d ops)", oe - ob);
+            o("    { // fused diagonal run (%d ops)", (int)run.size());
             // taps first: v_l = Im(conj(lambda_l) psi_l) is invariant under diagonal
             // unitaries applied to both states, so every tap of the run shares it
             // Signed sums sum_l (-1)^{popc(l & mask)} v_l for every register-bit mask the
@@ -359,7 +360,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             std::map<int, std::string> wsum;
             {
                 std::set<int> masks;
-                for (int oi = ob; oi < oe; ++oi) {
+                for (int oi : run) {
                     const DevOp& op = pass.ops[oi];
                     if (op.kind != DK_TZ && op.kind != DK_TZZ) continue;
                     BitSrc s0 = src(op.pos0);
@@ -422,9 +423,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             std::vector<std::vector<std::pair<int, int>>> perbit_idx(R);  // their smat indices (-1: per-thread)
             struct D2s { int r0, r1; std::string d[4]; int moff = 0; };
             std::vector<D2s> d2s;
-            for (int oi = ob; oi < oe; ++oi) {
+            for (size_t ri = 0; ri < run.size(); ++ri) {
+                const int oi = run[ri];
                 const DevOp& op = pass.ops[oi];
-                const std::string nm = "f" + std::to_string(id) + "_" + std::to_string(oi - ob);
+                const std::string nm = "f" + std::to_string(id) + "_" + std::to_string(ri);
                 if (op.kind == DK_TZ || op.kind == DK_TZZ) {
                     BitSrc s0 = src(op.pos0);
                     BitSrc s1 = op.kind == DK_TZZ ? src(op.pos1) : BitSrc{};
@@ -616,15 +618,73 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             o("    }");
         };
 
+        // Diagonal ops and Z-type taps are held back and fused into one run, which is
+        // applied only when a later op acts non-diagonally on one of their qubits
+        // (they commute with everything else, and a tap on qubit q is invariant
+        // under gates on other qubits applied to both states) or at the phase end.
+        // Tap ops flush pending taps first so the staging slots fill in order.
+        std::vector<int> pend;
+        uint64_t pend_pos = 0;
+        bool pend_tap = false;
+        auto reg_pos = [&](int rb) { return (uint64_t)1 << sw.tb[(int)ph.reg_tl[rb]]; };
+        auto flush_pending = [&] {
+            if (!pend.empty()) flush_diag_run(pend);
+            pend.clear();
+            pend_pos = 0;
+            pend_tap = false;
+        };
+        // At a forced flush, later diagonal gates (not taps, whose staging order is
+        // fixed) are hoisted into the run when nothing in between acts
+        // non-diagonally on their qubits.
+        std::vector<char> hoisted(ph.op_end - ph.op_begin, 0);
+        auto op_touch = [&](const DevOp& x) {
+            uint64_t t = 0;
+            if (is_diagish(x.kind)) return t;
+            if (x.rb0 >= 0) t |= reg_pos(x.rb0);
+            if (x.kind == DK_G2 && x.rb1 >= 0) t |= reg_pos(x.rb1);
+            return t;
+        };
+        auto diag_pos = [&](const DevOp& x) {
+            uint64_t t = 0;
+            if (x.pos0 >= 0) t |= (uint64_t)1 << x.pos0;
+            if ((x.kind == DK_D2 || x.kind == DK_TZZ) && x.pos1 >= 0) t |= (uint64_t)1 << x.pos1;
+            return t;
+        };
+        auto hoist_from = [&](int from) {
+            uint64_t blocked = 0;
+            for (int j = from; j < ph.op_end; ++j) {
+                const DevOp& x = pass.ops[j];
+                if ((x.kind == DK_D1 || x.kind == DK_D2) && !hoisted[j - ph.op_begin] && !(diag_pos(x) & blocked)) {
+                    pend.push_back(j);
+                    hoisted[j - ph.op_begin] = 1;
+                }
+                blocked |= op_touch(x);
+            }
+        };
         int oi = ph.op_begin;
         while (oi < ph.op_end) {
             const DevOp& op = pass.ops[oi];
-            if (allow_fuse && is_diagish(op.kind)) {
-                int oe = oi;
-                while (oe < ph.op_end && is_diagish(pass.ops[oe].kind)) ++oe;
-                flush_diag_run(oi, oe);
-                oi = oe;
+            if (hoisted[oi - ph.op_begin]) {
+                ++oi;
                 continue;
+            }
+            if (allow_fuse && is_diagish(op.kind)) {
+                pend.push_back(oi);
+                if (op.pos0 >= 0) pend_pos |= (uint64_t)1 << op.pos0;
+                if ((op.kind == DK_D2 || op.kind == DK_TZZ) && op.pos1 >= 0) pend_pos |= (uint64_t)1 << op.pos1;
+                pend_tap |= op.kind == DK_TZ || op.kind == DK_TZZ;
+                ++oi;
+                continue;
+            }
+            if (!pend.empty()) {
+                uint64_t touch = 0;
+                if (op.rb0 >= 0) touch |= reg_pos(op.rb0);
+                if (op.kind == DK_G2 && op.rb1 >= 0) touch |= reg_pos(op.rb1);
+                const bool is_tap = op.kind == DK_TX || op.kind == DK_TY;
+                if ((touch & pend_pos) || (is_tap && pend_tap) || !allow_fuse) {
+                    hoist_from(oi);
+                    flush_pending();
+                }
             }
             switch (op.kind) {
                 case DK_G1: case DK_R1: case DK_RX: {
@@ -663,7 +723,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     }
                     break;
                 case DK_D1: case DK_D2: case DK_TZ: case DK_TZZ:
-                    flush_diag_run(oi, oi + 1);
+                    flush_diag_run(std::vector<int>{oi});
                     break;
                 case DK_G2: {
                     o("    { const V* m = smat + %d;", op.moff);
@@ -715,6 +775,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             }
             ++oi;
         }
+        flush_pending();
         if (dlast) {
             emit_gbase(ph, "g_pl");
             for (int l = 0; l < NR; ++l) {
@@ -795,6 +856,140 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         o.s.insert(stab_pos, buf);
         o.s.insert(decl_pos, decl);
     }
+    return o.s;
+}
+
+// ------------------------------------------------------------------ H|psi>
+// Specialised lambda = H psi + E = Re<psi|lambda> for one observable (same
+// output-stationary tiling as hpsi_kernel in kernels.cu, whose AOT form stays the
+// fallback).  Amplitude p = tid + T i of the tile: every term's sign splits into
+// a per-thread part (thread bits, bits above the tile, parity(f & z)) and a
+// compile-time part over the register index i.  Diagonal terms accumulate one
+// per-thread coefficient per register-bit mask and are expanded once at the end;
+// flips inside the registers read registers, flips of thread bits read the
+// shared-memory copy of the (own or partner) tile, partner tiles above the tile
+// are loaded into registers.
+int jit_hpsi_threads(const ObservablePlan& O) {
+    const int TS = 1 << O.kh;
+    return TS < 256 ? TS : 256;
+}
+
+size_t jit_hpsi_smem(const ObservablePlan& O, int prec) {
+    return ((size_t)2 << O.kh) * (prec == QF_C128 ? 16 : 8) + 64;
+}
+
+std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
+    const bool dbl = prec == QF_C128;
+    const int kh = O.kh, TS = 1 << kh, T = jit_hpsi_threads(O), NA = TS / T;
+    int LT = 0;
+    while ((1 << LT) < T) ++LT;
+    const size_t N = (size_t)1 << O.n;
+    Out o;
+    o.s += kPrelude;
+    o.s += "\n";
+    o("namespace qfb {");
+    o("extern \"C\" __global__ void __launch_bounds__(%d, 2) qf_hpsi(const HArgs a) {", T);
+    o("  typedef %s V; typedef %s RT;", dbl ? "double2" : "float2", dbl ? "double" : "float");
+    o("  extern __shared__ __align__(16) unsigned char smem_raw[];");
+    o("  V* own = reinterpret_cast<V*>(smem_raw); V* part = own + %d; (void)own; (void)part;", TS);
+    o("  double* red = reinterpret_cast<double*>(part + %d);", TS);
+    o("  const uint32_t tid = threadIdx.x, tile = blockIdx.x; const int b = blockIdx.y;");
+    o("  const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)b * %zuull;", N);
+    o("  const uint32_t base = tile << %d; (void)base;", kh);
+    for (int i = 0; i < NA; ++i) o("  const V po%d = ps[base + tid + %uu];", i, (unsigned)(T * i));
+    bool own_smem = false;
+    std::set<uint32_t> dmasks;
+    for (const DevGroup& g : O.groups)
+        for (int t = g.term_begin; t < g.term_end; ++t) {
+            const DevTerm& d = O.terms[t];
+            if (g.f_out == 0 && (d.f_in & (uint32_t)(T - 1))) own_smem = true;
+            if (d.kind == TK_DIAG) dmasks.insert((d.z >> LT) & (uint32_t)(NA - 1));
+        }
+    if (own_smem) {
+        for (int i = 0; i < NA; ++i) o("  own[tid + %uu] = po%d;", (unsigned)(T * i), i);
+        o("  __syncthreads();");
+    }
+    for (int i = 0; i < NA; ++i) o("  V acc%d; acc%d.x = 0; acc%d.y = 0;", i, i, i);
+    for (uint32_t m : dmasks) o("  RT dm%u = 0;", m);
+    bool part_live = false;
+    for (const DevGroup& g : O.groups) {
+        const bool outer = g.f_out != 0;
+        bool need_smem = false;
+        for (int t = g.term_begin; t < g.term_end; ++t) need_smem |= (O.terms[t].f_in & (uint32_t)(T - 1)) != 0;
+        o("  {  // flip group 0x%x", g.f_out);
+        if (outer) {
+            for (int i = 0; i < NA; ++i)
+                o("    const V q%d = ps[(base ^ %uu) + tid + %uu];", i, g.f_out, (unsigned)(T * i));
+            if (need_smem) {
+                if (part_live) o("    __syncthreads();");
+                for (int i = 0; i < NA; ++i) o("    part[tid + %uu] = q%d;", (unsigned)(T * i), i);
+                o("    __syncthreads();");
+                part_live = true;
+            }
+        }
+        const char* R = outer ? "q" : "po";
+        const char* S = outer ? "part" : "own";
+        for (int t = g.term_begin; t < g.term_end; ++t) {
+            const DevTerm& d = O.terms[t];
+            const uint32_t zt = d.z & (uint32_t)(T - 1), zr = (d.z >> LT) & (uint32_t)(NA - 1);
+            const uint32_t zh = d.z & ~(uint32_t)(TS - 1);
+            const uint32_t ft = d.f_in & (uint32_t)(T - 1), fr = (d.f_in >> LT) & (uint32_t)(NA - 1);
+            const double c = (d.kind != TK_DIAG && d.yodd) ? d.c_im : d.c_re;
+            std::string sg;
+            if (zt) sg += "__popc(tid & " + std::to_string(zt) + "u)";
+            if (zh) sg += std::string(sg.empty() ? "" : " + ") + "__popc(base & " + std::to_string(zh) + "u)";
+            if (d.fz_par & 1) sg += std::string(sg.empty() ? "" : " + ") + "1u";
+            if (sg.empty())
+                o("    { const RT k_ = (RT)(%.17g);", c);
+            else
+                o("    { const RT k_ = ((%s) & 1u) ? (RT)(%.17g) : (RT)(%.17g);", sg.c_str(), -c, c);
+            if (d.kind == TK_DIAG) {
+                o("      dm%u += k_; }", zr);
+                continue;
+            }
+            if (zr) o("      const RT nk_ = -k_;");
+            for (int i = 0; i < NA; ++i) {
+                const bool neg = __builtin_popcount((unsigned)i & zr) & 1;
+                char src[96];
+                if (ft)
+                    snprintf(src, sizeof src, "%s[(tid ^ %uu) + %uu]", S, ft, (unsigned)(T * ((unsigned)i ^ fr)));
+                else
+                    snprintf(src, sizeof src, "%s%u", R, (unsigned)i ^ fr);
+                o("      acc%d = %s(%s, %s, acc%d);", i, d.yodd ? "jiaxpy" : "jaxpy", neg ? "nk_" : "k_", src, i);
+            }
+            o("    }");
+        }
+        o("  }");
+    }
+    if (!dmasks.empty())
+        for (int i = 0; i < NA; ++i) {
+            std::string e;
+            for (uint32_t m : dmasks) {
+                const bool neg = __builtin_popcount((unsigned)i & m) & 1;
+                if (e.empty()) e = (neg ? "-dm" : "dm") + std::to_string(m);
+                else e += (neg ? " - dm" : " + dm") + std::to_string(m);
+            }
+            o("  { const RT dg = %s; acc%d.x = fma(dg, po%d.x, acc%d.x); acc%d.y = fma(dg, po%d.y, acc%d.y); }",
+              e.c_str(), i, i, i, i, i, i);
+        }
+    o("  double e = 0;");
+    for (int i = 0; i < NA; ++i)
+        o("  e += (double)po%d.x * (double)acc%d.x + (double)po%d.y * (double)acc%d.y;", i, i, i, i);
+    o("  if (a.write_lam) {");
+    o("    V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", N);
+    for (int i = 0; i < NA; ++i) o("    lm[base + tid + %uu] = acc%d;", (unsigned)(T * i), i);
+    o("  }");
+    o("  const unsigned m = lane_mask(%d);", T);
+    o("  for (int off = %d; off > 0; off >>= 1) e += __shfl_xor_sync(m, e, off);", T >= 32 ? 16 : T / 2);
+    o("  if ((tid & 31) == 0) red[tid >> 5] = e;");
+    o("  __syncthreads();");
+    o("  if (tid == 0) {");
+    o("    double s = 0;");
+    o("    for (int w = 0; w < %d; ++w) s += red[w];", (T + 31) / 32);
+    o("    a.epart[(size_t)b * gridDim.x + tile] = s;");
+    o("  }");
+    o("}");
+    o("}  // namespace qfb");
     return o.s;
 }
 
@@ -1020,6 +1215,64 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     fwd.ok = bwd.ok = true;
     st.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return true;
+}
+
+bool jit_build_hpsi(const ObservablePlan& O, int prec, JitKernel& out, std::string& err) {
+    {
+        std::lock_guard<std::mutex> lk(g_nvrtc_mu);
+        if (!g_nvrtc.load()) {
+            err = g_nvrtc.err;
+            return false;
+        }
+    }
+    int maj = 0, min = 0;
+    g_nvrtc.version(&maj, &min);
+    const std::string src = jit_hpsi_source(O, prec);
+    const std::string dir = cache_dir();
+    mkdirs(dir);
+    char key[64];
+    snprintf(key, sizeof key, "%016llx_%d_%d", (unsigned long long)fnv1a(src), maj, min);
+    const std::string path = dir + "/" + key + ".cubin";
+    std::string cubin;
+    if (!read_file(path, cubin)) {
+        if (!compile_one(src, cubin, err)) return false;
+        const std::string tmp = path + ".tmp" + std::to_string(getpid());
+        {
+            std::ofstream f(tmp, std::ios::binary);
+            f.write(cubin.data(), (std::streamsize)cubin.size());
+        }
+        rename(tmp.c_str(), path.c_str());
+    }
+    cudaLibrary_t lib;
+    cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        return false;
+    }
+    cudaKernel_t kern;
+    e = cudaLibraryGetKernel(&kern, lib, "qf_hpsi");
+    if (e != cudaSuccess) {
+        err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+        return false;
+    }
+    out.kernel = (void*)kern;
+    out.threads = jit_hpsi_threads(O);
+    out.smem = jit_hpsi_smem(O, prec);
+    if (out.smem > 48 * 1024) {
+        e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out.smem);
+        if (e != cudaSuccess) {
+            err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+            return false;
+        }
+    }
+    return true;
+}
+
+int jit_launch_hpsi(const JitKernel& k, const HArgs& a, int tiles, int batch, void* stream) {
+    HArgs aa = a;
+    void* args[] = {&aa};
+    return (int)cudaLaunchKernel((const void*)k.kernel, dim3(tiles, batch), dim3(k.threads), args, k.smem,
+                                 (cudaStream_t)stream);
 }
 
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream) {

@@ -51,4 +51,11 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st);
 // Launch one specialised sweep.
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream);
 
+// Specialised H|psi> + energy kernel of one observable (qf_hpsi); at most
+// kJitHpsiMaxTerms terms (larger sums keep the AOT hpsi_kernel).
+constexpr int kJitHpsiMaxTerms = 256;
+std::string jit_hpsi_source(const ObservablePlan& O, int prec);
+bool jit_build_hpsi(const ObservablePlan& O, int prec, JitKernel& out, std::string& err);
+int jit_launch_hpsi(const JitKernel& k, const HArgs& a, int tiles, int batch, void* stream);
+
 }  // namespace qfb

@@ -106,6 +106,17 @@ __device__ __forceinline__ float2 jim2(float2 u, float2 v) { return __fmul2_rn(u
 __device__ __forceinline__ float2 jim2a(float2 u, float2 v, float2 acc) { return __ffma2_rn(u, swp(v), acc); }
 __device__ __forceinline__ float2 jadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 jsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// acc + k v and acc + i k v (k real) for the specialised H|psi> kernels
+__device__ __forceinline__ float2 jaxpy(float k, float2 v, float2 acc) { return __ffma2_rn(make_float2(k, k), v, acc); }
+__device__ __forceinline__ double2 jaxpy(double k, double2 v, double2 acc) {
+    return make_double2(fma(k, v.x, acc.x), fma(k, v.y, acc.y));
+}
+__device__ __forceinline__ float2 jiaxpy(float k, float2 v, float2 acc) {
+    return __ffma2_rn(make_float2(-k, k), swp(v), acc);
+}
+__device__ __forceinline__ double2 jiaxpy(double k, double2 v, double2 acc) {
+    return make_double2(fma(-k, v.y, acc.x), fma(k, v.x, acc.y));
+}
 template <typename V> __device__ __forceinline__ void jcswap(V& a, V& b, bool c) {
     const V t0 = a, t1 = b;
     a = c ? t1 : t0;

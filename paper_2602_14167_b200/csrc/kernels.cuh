@@ -8,18 +8,6 @@
 
 namespace qfb {
 
-struct HArgs {
-    const void* psi;
-    void* lam;
-    int n, kh;
-    const DevGroup* groups;
-    int n_groups;
-    const DevTerm* terms;
-    int write_lam;
-    int use_imag;
-    double* epart;             // [B][tiles]
-};
-
 struct ReduceArgs {
     const double* part;        // [B][count][tiles]
     int count, tiles;

@@ -129,6 +129,19 @@ struct DevGroup {
     int32_t pad;
 };
 
+// Kernel arguments of one H|psi> launch (AOT kernel and NVRTC kernels).
+struct HArgs {
+    const void* psi;
+    void* lam;
+    int n, kh;
+    const DevGroup* groups;
+    int n_groups;
+    const DevTerm* terms;
+    int write_lam;
+    int use_imag;
+    double* epart;             // [B][tiles]
+};
+
 // Kernel arguments of one sweep launch (AOT interpreter and NVRTC kernels).
 struct SweepArgs {
     void* psi;                 // [B][N] complex (float2 / double2)

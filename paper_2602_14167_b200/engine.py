@@ -133,6 +133,19 @@ def jit_compile_check(n: int, ops: Sequence, n_params: int, precision="c128", ma
     return k.value
 
 
+def jit_hpsi_check(n: int, codes, weights, precision="c128") -> bool:
+    """NVRTC-compile the specialised H|psi> kernel of a Pauli sum (host only);
+    False when the sum is above the specialisation limit (generic kernel)."""
+    lib = _lib.load()
+    codes = np.ascontiguousarray(np.asarray(codes, dtype=np.int8).reshape(-1, n))
+    w = np.asarray(weights, dtype=np.complex128).reshape(-1)
+    wr, wi = np.ascontiguousarray(w.real), np.ascontiguousarray(w.imag)
+    k = ctypes.c_int()
+    check(lib.qf_jit_hpsi_check(n, int(w.size), ctypes.c_void_p(codes.ctypes.data), dptr(wr), dptr(wi),
+                                PRECISIONS[precision], ctypes.byref(k)))
+    return bool(k.value)
+
+
 class Program:
     """A compiled circuit template (qf_program).
 

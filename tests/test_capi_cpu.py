@@ -64,3 +64,15 @@ def test_specialised_kernels_compile_all_gate_kinds(monkeypatch):
            (G["unitary"], 3, 4, -1, 1, 0, 0), (G["rzz"], 0, 7, 4, 1, 0, -1)]
     k = engine.jit_compile_check(8, ops, 5, "c64", mats=[u])
     assert k >= 2
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_specialised_hpsi_compiles_for_sm100a(prec):
+    """qf_jit_hpsi_check: the observable-specialised H|psi> kernel (jit.cpp) for
+    TFIM / XXZ / complex random sums; sums above the limit use the generic kernel."""
+    from oracle import pyoracle as po
+    for h in [po.tfim(12, 0.7), po.heisenberg(9, 1.0, 0.5, 0.25), po.random_sum(7, 30, po.Rng(3), False),
+              po.random_sum(3, 5, po.Rng(4), True)]:
+        assert engine.jit_hpsi_check(h.n, h.codes, h.wr + 1j * h.wi, prec)
+    big = po.random_sum(10, 300, po.Rng(5), True)
+    assert not engine.jit_hpsi_check(big.n, big.codes, big.wr + 1j * big.wi, prec)
