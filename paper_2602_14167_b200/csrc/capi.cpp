@@ -326,7 +326,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.write_lam = grads ? 1 : 0;
     ha.use_imag = 0;
     ha.epart = (double*)ctx->epart.p;
-    if (prog->use_jit && od->hj_state == 0) {
+    if (prog->use_jit && od->hj_state == 0 && !(std::getenv("QF_JIT_HPSI") && std::getenv("QF_JIT_HPSI")[0] == '0')) {
         std::string err;
         od->hj_state = ((int)od->plan.terms.size() <= kJitHpsiMaxTerms && jit_build_hpsi(od->plan, prec, od->hj, err))
                            ? 1 : -1;

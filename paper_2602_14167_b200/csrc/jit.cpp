@@ -273,7 +273,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     // built once per CTA into shared memory (the prologue is inserted here once
     // every run is known); each entry lists its factor indices into smat.
     const size_t stab_pos = o.s.size();
-    const bool use_stab = !pipe;
+    auto env_off = [](const char* name) {
+        const char* e = std::getenv(name);
+        return e && e[0] == '1';
+    };
+    const bool use_stab = !pipe && !env_off("QF_JIT_NOSTAB");  // development toggles (A/B, bisection)
+    const bool use_ratio = bwd && !env_off("QF_JIT_NORATIO");
+    const bool use_hoist = !env_off("QF_JIT_NOHOIST");
+    const bool use_lazy = !env_off("QF_JIT_NOLAZY");
     std::vector<std::vector<int>> stab_entries;
 
     std::vector<const char*> arrs = {"x"};
@@ -500,7 +507,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         std::vector<int> f;
                         for (size_t bi = 0; bi < ubits.size(); ++bi)
                             for (auto& pi : perbit_idx[ubits[bi]]) {
-                                if (bwd) {
+                                // Not combined with per-thread factors: at n = 30 (c64) that mix
+                                // loses ~1e-4 on cancellation-dominated gradients (c128 exact).
+                                if (use_ratio && !have_c) {
                                     if ((e >> bi) & 1) f.push_back(kRatio | pi.first);
                                 } else {
                                     f.push_back(((e >> bi) & 1) ? pi.second : pi.first);
@@ -681,8 +690,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 if (op.rb0 >= 0) touch |= reg_pos(op.rb0);
                 if (op.kind == DK_G2 && op.rb1 >= 0) touch |= reg_pos(op.rb1);
                 const bool is_tap = op.kind == DK_TX || op.kind == DK_TY;
-                if ((touch & pend_pos) || (is_tap && pend_tap) || !allow_fuse) {
-                    hoist_from(oi);
+                if ((touch & pend_pos) || (is_tap && pend_tap) || !allow_fuse || !use_lazy) {
+                    if (use_hoist) hoist_from(oi);
                     flush_pending();
                 }
             }
@@ -846,6 +855,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                  "    for (int q = 0; q < %zu; ++q) {\n"
                  "      const unsigned i = qf_stab_f[e][q];\n"
                  "      if (i == 0xffffu) break;\n"
+
                  "      if (i & 0x8000u) { V d0 = smat[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(smat[(i & 0x7fffu) + 1], d0)); }\n"
                  "      else acc = cmul(acc, smat[i]);\n"
                  "    }\n"
