@@ -4,6 +4,7 @@
 // (require() -> std::invalid_argument); every state-vector operation runs on
 // the GPU through libqforge_b200.so.  Reference line citations are relative to
 // /root/reference/proj.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -396,6 +397,78 @@ PauliSum heisenberg_terms(const Lattice& l, double jx, double jy, double jz) {  
     return h;
 }
 
+// ------------------------------------------------------------------ sparse
+SparseCOO pauli_sum_to_coo(const PauliSum& h, int n_guard, std::size_t /*workers*/) {  // pauli.cpp:89-153
+    require(h.n >= 1, "pauli_sum_to_coo: empty system");
+    require(h.n <= n_guard, "pauli_sum_to_coo: qubit count exceeds memory guard");
+    SparseCOO out;
+    out.dim = (std::int64_t)1 << h.n;
+    std::int64_t nnz = 0;
+    check(qf_pauli_sum_to_coo(ctx(), observable(h), n_guard, 0, nullptr, nullptr, nullptr, 0, &nnz));
+    out.rows.resize((size_t)nnz);
+    out.cols.resize((size_t)nnz);
+    out.vals.resize((size_t)nnz);
+    if (nnz)
+        check(qf_pauli_sum_to_coo(ctx(), observable(h), n_guard, 0, out.rows.data(), out.cols.data(),
+                                  reinterpret_cast<double*>(out.vals.data()), nnz, &nnz));
+    return out;
+}
+
+void SparseCOO::canonicalize() {  // sparse.hpp:25 contract
+    std::vector<size_t> idx(vals.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+        return rows[a] != rows[b] ? rows[a] < rows[b] : cols[a] < cols[b];
+    });
+    SparseCOO c;
+    c.dim = dim;
+    for (size_t i : idx) {
+        if (!c.vals.empty() && c.rows.back() == rows[i] && c.cols.back() == cols[i]) c.vals.back() += vals[i];
+        else c.push(rows[i], cols[i], vals[i]);
+    }
+    SparseCOO z;
+    z.dim = dim;
+    for (size_t k = 0; k < c.vals.size(); ++k)
+        if (c.vals[k] != cplx(0.0)) z.push(c.rows[k], c.cols[k], c.vals[k]);
+    *this = std::move(z);
+}
+
+void SparseCOO::matvec(const ComplexVector& in, ComplexVector& out) const {
+    require(in.size() == dim, "SparseCOO::matvec: size mismatch");
+    out = ComplexVector::Zero(dim);
+    for (size_t k = 0; k < vals.size(); ++k) out[rows[k]] += vals[k] * in[cols[k]];
+}
+
+ComplexVector SparseCOO::apply(const ComplexVector& in) const {
+    ComplexVector out;
+    matvec(in, out);
+    return out;
+}
+
+ComplexMatrix SparseCOO::to_dense() const {
+    ComplexMatrix m = ComplexMatrix::Zero(dim, dim);
+    for (size_t k = 0; k < vals.size(); ++k) m(rows[k], cols[k]) += vals[k];
+    return m;
+}
+
+SparseCOO SparseCOO::from_dense(const ComplexMatrix& m) {
+    require(m.rows() == m.cols(), "SparseCOO::from_dense: matrix must be square");
+    SparseCOO s;
+    s.dim = m.rows();
+    for (std::int64_t r = 0; r < m.rows(); ++r)
+        for (std::int64_t c = 0; c < m.cols(); ++c)
+            if (m(r, c) != cplx(0.0)) s.push(r, c, m(r, c));
+    return s;
+}
+
+SparseCOO SparseCOO::operator+(const SparseCOO& other) const {
+    require(dim == other.dim, "SparseCOO::operator+: dimension mismatch");
+    SparseCOO s = *this;
+    for (size_t k = 0; k < other.vals.size(); ++k) s.push(other.rows[k], other.cols[k], other.vals[k]);
+    s.canonicalize();
+    return s;
+}
+
 // ------------------------------------------------------------------ variational
 void AnsatzSpec::validate() const {  // variational.cpp:11-16
     require(n_params >= 0, "AnsatzSpec: negative parameter count");
@@ -528,6 +601,16 @@ double energy(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum&
     std::vector<double> flat(theta.data(), theta.data() + theta.size()), E;
     batch_eval(ansatz, flat, 1, h, E, nullptr);
     return E[0];
+}
+
+double energy(const AnsatzSpec& ansatz, const RealVector& theta, const SparseCOO& h) {  // variational.cpp:45-52
+    ansatz.validate();
+    require(theta.size() == ansatz.n_params, "energy: parameter count mismatch");
+    auto prog = ansatz_program(ansatz);
+    double E = 0.0;
+    check(qf_sparse_energy(ctx(), prog->p, 1, theta.data(), h.dim, (std::int64_t)h.nnz(), h.rows.data(),
+                           h.cols.data(), reinterpret_cast<const double*>(h.vals.data()), 0, &E));
+    return E;
 }
 
 RealVector gradient(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum& h, GradMode mode,

@@ -71,6 +71,29 @@ int main() {
         for (int i = 0; i < t.n_params; ++i) theta[i] = rng.normal();
         PauliSum h = tfim_chain(5, 1.3);
         CHECK(energy(t, theta, h) == energy(t, theta, h));
+        const double e1 = energy(t, theta, h), e3 = energy(t, theta, pauli_sum_to_coo(h));  // operator formats
+        CHECK(approx(e1, e3, 1e-12));
+    });
+    test_case("sparse operator", [] {  // pauli.cpp:89-153, sparse.cpp:44-51
+        PauliSum h = tfim_chain(4, 0.7);
+        SparseCOO m = pauli_sum_to_coo(h);
+        CHECK(m.dim == 16 && m.nnz() == 16 * 5);
+        for (size_t k = 1; k < m.nnz(); ++k)
+            CHECK(m.rows[k - 1] < m.rows[k] || (m.rows[k - 1] == m.rows[k] && m.cols[k - 1] < m.cols[k]));
+        SparseCOO twice = m + m;
+        CHECK(twice.nnz() == m.nnz());
+        ComplexVector v = ComplexVector::Zero(16);
+        v[5] = 1.0;
+        ComplexVector w = m.apply(v);
+        CHECK(approx(w[5].real(), -1.0 * ((5 & 1) == ((5 >> 1) & 1) ? 1 : -1) - ((5 >> 1 & 1) == (5 >> 2 & 1) ? 1 : -1) -
+                                      ((5 >> 2 & 1) == (5 >> 3 & 1) ? 1 : -1), 1e-12));
+        bool threw = false;
+        try {
+            pauli_sum_to_coo(tfim_chain(27, 1.0));
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
     });
     test_case("gradients", [] {  // test_variational.cpp:103-154
         PauliSum z;

@@ -1,5 +1,5 @@
 // qforge/pauli.hpp -- Pauli-sum IR (reference include/qforge/pauli.hpp:13-41):
-// PauliTerm, PauliSum::add / add_word, tfim_terms, heisenberg_terms.
+// PauliTerm, PauliSum::add / add_word, tfim_terms, heisenberg_terms, pauli_sum_to_coo.
 #pragma once
 
 #include <memory>
@@ -8,6 +8,7 @@
 
 #include "qforge/common.hpp"
 #include "qforge/lattice.hpp"
+#include "qforge/sparse.hpp"
 
 namespace qforge {
 
@@ -28,6 +29,10 @@ struct PauliSum {
     mutable std::shared_ptr<void> device_cache;
     mutable std::size_t device_cache_terms = 0;
 };
+
+// canonical COO of the sum, built on the GPU (pauli.cpp:89-153); `workers` is
+// accepted for signature compatibility (the output never depends on it)
+SparseCOO pauli_sum_to_coo(const PauliSum& h, int n_guard = 26, std::size_t workers = 1);
 
 PauliSum tfim_terms(const Lattice& l, double g);
 PauliSum heisenberg_terms(const Lattice& l, double jx, double jy, double jz);

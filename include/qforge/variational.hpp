@@ -30,6 +30,7 @@ AnsatzSpec tfim_chain_ansatz(int n, int layers);
 AnsatzSpec hea_ansatz(int n, int layers);  // synthetic HEA of the benchmark configs
 
 double energy(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum& h);
+double energy(const AnsatzSpec& ansatz, const RealVector& theta, const SparseCOO& h);  // COO operator path
 
 enum class GradMode { parameter_shift, finite_diff, adjoint };
 

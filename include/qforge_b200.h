@@ -178,6 +178,16 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
                         int64_t* rows, int64_t* cols, double* vals, int64_t capacity,
                         int64_t* nnz);
 
+/* energy(ansatz, theta, SparseCOO) (reference variational.cpp:45-52 with the
+ * COO matvec of sparse.cpp:44-51): for each of `batch` parameter rows, the
+ * forward state psi and E = Re(psi^dagger H psi) over the canonical triplets
+ * (rows/cols int64, vals interleaved complex128; host arrays, or device
+ * pointers when coo_on_device).  dim must be 2^n ("energy: Hamiltonian
+ * dimension mismatch").  Deterministic (fixed-order reductions). */
+int qf_sparse_energy(qf_ctx* ctx, const qf_program* prog, int batch, const double* thetas, int64_t dim,
+                     int64_t nnz, const int64_t* rows, const int64_t* cols, const double* vals, int coo_on_device,
+                     double* energies);
+
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
  * float64 device pointers.  Single-GPU semantics (no collective). */

@@ -840,6 +840,54 @@ static int stage_thetas(qf_ctx* ctx, const qf_program* prog, int batch, const do
     return QF_OK;
 }
 
+// Forward pass of one parameter row (device theta) into ctx->psi (state 0).
+static int forward_one(qf_ctx* ctx, qf_program* prog, const double* d_theta) {
+    const int n = prog->plan.n;
+    const ProgramPlan& P = prog->plan;
+    const size_t N = size_t(1) << n;
+    const size_t vs = vsize(P.prec);
+    QF_CUDA(ctx->psi.reserve(N * vs));
+    cudaStream_t s = ctx->stream;
+    if (prog->has_init) {
+        QF_CUDA(launch_init_state(P.prec, ctx->psi.p, prog->init.p, n, 1, s));
+    } else if (P.fwd.sweeps.empty()) {
+        QF_CUDA(cudaMemsetAsync(ctx->psi.p, 0, N * vs, s));
+        if (P.prec == QF_C128) {
+            static const double one[2] = {1.0, 0.0};
+            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 16, cudaMemcpyHostToDevice, s));
+        } else {
+            static const float one[2] = {1.0f, 0.0f};
+            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 8, cudaMemcpyHostToDevice, s));
+        }
+    }
+    SweepArgs sa{};
+    sa.psi = ctx->psi.p;
+    sa.theta = d_theta;
+    sa.P = P.n_params;
+    sa.n = n;
+    sa.gates = (const DevGate*)prog->gates.p;
+    sa.cmats = (const double*)prog->cmats.p;
+    QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs)));
+    sa.gmat = ctx->gmat.p;
+    sa.gmat_stride = P.fwd.total_mat + P.bwd.total_mat;
+    sa.gmat_pass_base = 0;
+    QF_CUDA(launch_mats(P.prec, false, (const DevOp*)prog->fwd.ops.p, (const int*)prog->goff_fwd.p,
+                        (int)P.fwd.ops.size(), sa.gates, sa.cmats, sa.theta, P.n_params, 0, ctx->gmat.p,
+                        sa.gmat_stride, 0, 1, s));
+    sa.phases = (const DevPhase*)prog->fwd.phases.p;
+    sa.ops = (const DevOp*)prog->fwd.ops.p;
+    for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
+        sa.sw = P.fwd.sweeps[i];
+        sa.from_zero = (i == 0 && !prog->has_init) ? 1 : 0;
+        if (prog->use_jit)
+            QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), 1, s));
+        else
+            QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
+        ctx->launches++;
+    }
+    return QF_OK;
+}
+
 static void reset_stats(qf_ctx* ctx) {
     resolve_events(ctx);
     ctx->launches = 0;
@@ -920,49 +968,12 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
     cudaSetDevice(ctx->device);
     rc = stage_thetas(ctx, prog, 1, theta);
     if (rc) return rc;
-    // forward only: use a trivial observable-free path
+    rc = forward_one(ctx, prog, (const double*)ctx->thetas.p);
+    if (rc) return rc;
     const ProgramPlan& P = prog->plan;
     const size_t N = size_t(1) << n;
     const size_t vs = vsize(P.prec);
-    QF_CUDA(ctx->psi.reserve(N * vs));
     cudaStream_t s = ctx->stream;
-    if (prog->has_init) {
-        QF_CUDA(launch_init_state(P.prec, ctx->psi.p, prog->init.p, n, 1, s));
-    } else if (P.fwd.sweeps.empty()) {
-        QF_CUDA(cudaMemsetAsync(ctx->psi.p, 0, N * vs, s));
-        if (P.prec == QF_C128) {
-            static const double one[2] = {1.0, 0.0};
-            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 16, cudaMemcpyHostToDevice, s));
-        } else {
-            static const float one[2] = {1.0f, 0.0f};
-            QF_CUDA(cudaMemcpyAsync(ctx->psi.p, one, 8, cudaMemcpyHostToDevice, s));
-        }
-    }
-    SweepArgs sa{};
-    sa.psi = ctx->psi.p;
-    sa.theta = (const double*)ctx->thetas.p;
-    sa.P = P.n_params;
-    sa.n = n;
-    sa.gates = (const DevGate*)prog->gates.p;
-    sa.cmats = (const double*)prog->cmats.p;
-    QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs)));
-    sa.gmat = ctx->gmat.p;
-    sa.gmat_stride = P.fwd.total_mat + P.bwd.total_mat;
-    sa.gmat_pass_base = 0;
-    QF_CUDA(launch_mats(P.prec, false, (const DevOp*)prog->fwd.ops.p, (const int*)prog->goff_fwd.p,
-                        (int)P.fwd.ops.size(), sa.gates, sa.cmats, sa.theta, P.n_params, 0, ctx->gmat.p,
-                        sa.gmat_stride, 0, 1, s));
-    sa.phases = (const DevPhase*)prog->fwd.phases.p;
-    sa.ops = (const DevOp*)prog->fwd.ops.p;
-    for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
-        sa.sw = P.fwd.sweeps[i];
-        sa.from_zero = (i == 0 && !prog->has_init) ? 1 : 0;
-        if (prog->use_jit)
-            QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), 1, s));
-        else
-            QF_CUDA(launch_sweep(P.prec, false, sa, 1, P.fwd.max_mat, 0, s));
-        ctx->launches++;
-    }
     // Shear-form rotations (DK_RS) may apply -R: a global sign, irrelevant to
     // energies and gradients but not to the state itself -- undo it here.
     double sign = 1.0;
@@ -992,6 +1003,61 @@ int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int 
         QF_CUDA(cudaStreamSynchronize(s));
         for (size_t i = 0; i < 2 * N; ++i) amps_out[i] = sign * f[i];
     }
+    return QF_OK;
+}
+
+int qf_sparse_energy(qf_ctx* ctx, const qf_program* cprog, int batch, const double* thetas, int64_t dim, int64_t nnz,
+                     const int64_t* rows, const int64_t* cols, const double* vals, int coo_on_device,
+                     double* energies) {
+    // reference variational.cpp:45-52 (energy(ansatz, theta, SparseCOO)) and sparse.cpp:44-51
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    if (!ctx || !prog || batch < 0 || nnz < 0 || (batch > 0 && (!energies || (!thetas && prog->plan.n_params))) ||
+        (nnz > 0 && (!rows || !cols || !vals)))
+        return set_err(QF_EINVAL, "qf_sparse_energy: bad arguments");
+    const int n = prog->plan.n;
+    if (dim != ((int64_t)1 << n)) return set_err(QF_EINVAL, "energy: Hamiltonian dimension mismatch");
+    if (batch == 0) return QF_OK;
+    int rc = check_thetas(prog, batch, thetas);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    rc = stage_thetas(ctx, prog, batch, thetas);
+    if (rc) return rc;
+    const int64_t *dr = rows, *dc = cols;
+    const double2* dv = reinterpret_cast<const double2*>(vals);
+    if (!coo_on_device && nnz > 0) {
+        QF_CUDA(ctx->coo_rows.reserve((size_t)nnz * 8));
+        QF_CUDA(ctx->coo_cols.reserve((size_t)nnz * 8));
+        QF_CUDA(ctx->coo_vals.reserve((size_t)nnz * 16));
+        QF_CUDA(cudaMemcpyAsync(ctx->coo_rows.p, rows, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        QF_CUDA(cudaMemcpyAsync(ctx->coo_cols.p, cols, (size_t)nnz * 8, cudaMemcpyHostToDevice, s));
+        QF_CUDA(cudaMemcpyAsync(ctx->coo_vals.p, vals, (size_t)nnz * 16, cudaMemcpyHostToDevice, s));
+        dr = (const int64_t*)ctx->coo_rows.p;
+        dc = (const int64_t*)ctx->coo_cols.p;
+        dv = (const double2*)ctx->coo_vals.p;
+    }
+    const int blocks = coo_energy_blocks(nnz);
+    QF_CUDA(ctx->epart.reserve((size_t)blocks * 8));
+    QF_CUDA(ctx->out.reserve((size_t)batch * 8));
+    double* d_out = (double*)ctx->out.p;
+    for (int b = 0; b < batch; ++b) {
+        rc = forward_one(ctx, prog, (const double*)ctx->thetas.p + (size_t)b * prog->plan.n_params);
+        if (rc) return rc;
+        if (nnz > 0) {
+            QF_CUDA(launch_coo_energy(prog->plan.prec, dr, dc, dv, nnz, ctx->psi.p, (double*)ctx->epart.p, s));
+            ReduceArgs ra{};
+            ra.part = (const double*)ctx->epart.p;
+            ra.count = 1;
+            ra.tiles = blocks;
+            ra.out = d_out + b;
+            QF_CUDA(launch_reduce(ra, 1, s));
+            ctx->launches += 2;
+        } else {
+            QF_CUDA(cudaMemsetAsync(d_out + b, 0, 8, s));
+        }
+    }
+    QF_CUDA(cudaMemcpyAsync(energies, d_out, (size_t)batch * 8, cudaMemcpyDeviceToHost, s));
+    QF_CUDA(cudaStreamSynchronize(s));
     return QF_OK;
 }
 

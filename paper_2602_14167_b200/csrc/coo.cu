@@ -235,7 +235,46 @@ __global__ void coo_write_block_kernel(const CooGroup* g, int n_groups, const Co
     }
 }
 
+template <typename V>
+__global__ void __launch_bounds__(256) coo_energy_kernel(const int64_t* rows, const int64_t* cols, const double2* vals,
+                                                         int64_t nnz, int64_t chunk, const V* psi, double* part) {
+    __shared__ double red[8];
+    const int64_t k0 = (int64_t)blockIdx.x * chunk;
+    const int64_t k1 = min(k0 + chunk, nnz);
+    double acc = 0.0;
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const V a = psi[rows[k]], c = psi[cols[k]];
+        const double2 v = vals[k];
+        const double vr = v.x * (double)c.x - v.y * (double)c.y;  // v psi[c]
+        const double vi = v.x * (double)c.y + v.y * (double)c.x;
+        acc += (double)a.x * vr + (double)a.y * vi;              // Re(conj(psi[r]) v psi[c])
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        part[blockIdx.x] = t;
+    }
+}
+
 }  // namespace
+
+int coo_energy_blocks(int64_t nnz) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((nnz + 8191) / 8192, 148 * 16));
+}
+
+cudaError_t launch_coo_energy(int prec, const int64_t* rows, const int64_t* cols, const double2* vals, int64_t nnz,
+                              const void* psi, double* part, cudaStream_t s) {
+    const int blocks = coo_energy_blocks(nnz);
+    const int64_t chunk = (nnz + blocks - 1) / blocks;
+    if (prec == 1)  // QF_C128
+        coo_energy_kernel<double2><<<blocks, 256, 0, s>>>(rows, cols, vals, nnz, chunk, (const double2*)psi, part);
+    else
+        coo_energy_kernel<float2><<<blocks, 256, 0, s>>>(rows, cols, vals, nnz, chunk, (const float2*)psi, part);
+    return cudaGetLastError();
+}
 
 bool coo_tile_ok(int n, int n_groups, int n_terms) { return n <= 31 && n_groups <= 32 && n_terms <= kTileMaxTerms; }
 

@@ -64,6 +64,12 @@ cudaError_t launch_coo_count(const CooGroup* g, int n_groups, const CooTerm* t, 
 // exclusive scan counts -> offsets (offsets[dim] = nnz); scratch via cub
 cudaError_t coo_scan(const int64_t* counts, int64_t* offsets, int64_t dim, void* scratch, size_t* scratch_bytes,
                      cudaStream_t s);
+// E partials of <psi|H|psi> for a COO H (sparse.cpp:44-51 + variational.cpp:45-52):
+// block j sums Re(conj(psi[r_k]) v_k psi[c_k]) over its contiguous nnz range,
+// fixed order; launch_reduce(count 1, tiles = blocks) finishes.  Returns blocks.
+int coo_energy_blocks(int64_t nnz);
+cudaError_t launch_coo_energy(int prec, const int64_t* rows, const int64_t* cols, const double2* vals, int64_t nnz,
+                              const void* psi, double* part, cudaStream_t s);
 // rows / cols ascending per row, complex128 values
 cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n_terms, const CooEvent* ev,
                              int n_ev, int n, const int64_t* offsets,

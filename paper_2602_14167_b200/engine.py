@@ -296,6 +296,33 @@ def pauli_sum_to_coo(ctx: Context, obs: Observable, n_guard: int = 26, device: b
     return rows, cols, vals
 
 
+def sparse_energy(ctx: Context, prog: Program, thetas, dim: int, rows, cols, vals) -> np.ndarray:
+    """energy(ansatz, theta, SparseCOO) for each parameter row (qf_sparse_energy,
+    variational.cpp:45-52).  rows/cols/vals: numpy (int64, int64, complex128), or
+    torch CUDA tensors of the same dtypes (used in place, e.g. the output of
+    pauli_sum_to_coo(..., device=True))."""
+    th = np.asarray(thetas, dtype=np.float64)
+    th = np.ascontiguousarray(th.reshape(-1, prog.n_params) if prog.n_params
+                              else np.zeros((th.shape[0] if th.ndim == 2 else 1, 0)))
+    B = th.shape[0]
+    out = np.zeros(B)
+    on_dev = hasattr(vals, "is_cuda") and vals.is_cuda
+    if on_dev:
+        import torch
+        assert rows.dtype == torch.int64 and cols.dtype == torch.int64 and vals.dtype == torch.complex128
+        nnz = int(vals.numel())
+        ptrs = [ctypes.c_void_p(t.data_ptr()) if nnz else None for t in (rows, cols, vals)]
+    else:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        vals = np.ascontiguousarray(vals, dtype=np.complex128)
+        nnz = int(vals.size)
+        ptrs = [ctypes.c_void_p(a.ctypes.data) if nnz else None for a in (rows, cols, vals)]
+    check(ctx.lib.qf_sparse_energy(ctx.handle, prog.handle, B, dptr(th), int(dim), nnz, *ptrs, 1 if on_dev else 0,
+                                   dptr(out)))
+    return out
+
+
 def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
                      eps=1e-8) -> None:
     B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))

@@ -617,10 +617,14 @@ def energy_gradient_batch(ansatz: AnsatzSpec, thetas, h: PauliSum, grads: bool =
     return _eng.energy_grad_batch(ctx, prog, h.observable(ctx), th, grads)
 
 
-def energy(ansatz: AnsatzSpec, theta, h: PauliSum) -> float:  # variational.cpp:38-43
+def energy(ansatz: AnsatzSpec, theta, h) -> float:  # variational.cpp:38-43 (PauliSum), :45-52 (SparseCOO)
     ansatz.validate()
     theta = np.asarray(theta, dtype=np.float64).reshape(-1)
     _require(theta.size == ansatz.n_params, "energy: parameter count mismatch")
+    if isinstance(h, SparseCOO):
+        ctx = _eng.default_context()
+        E = _eng.sparse_energy(ctx, ansatz.program(None, ctx), theta[None, :], h.dim, h.rows, h.cols, h.vals)
+        return float(E[0])
     E, _ = energy_gradient_batch(ansatz, theta[None, :], h, grads=False)
     return float(E[0])
 

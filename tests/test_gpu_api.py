@@ -73,6 +73,8 @@ def test_energy_evaluation_subcases(ctx):
     assert e1 == e2  # pure pipeline: bitwise repeatable
     ref = po.energy(po.Ansatz(*po.tca_template(5, 2)), th, po.tfim(5, 1.3))
     assert e1 == pytest.approx(ref, rel=1e-12)
+    e3 = qf.energy(a, th, qf.pauli_sum_to_coo(h))  # operator-format agreement (SparseCOO)
+    assert e1 == pytest.approx(e3, rel=1e-12)
     h5 = chain(5, 1.0)
     ground = po.energy(po.Ansatz(5, [], 0), np.zeros(0), po.tfim(5, 1.0))  # noqa: F841 (sanity)
     r = RngStream(8)
@@ -270,3 +272,29 @@ def test_nccl_single_rank_collective_path(ctx):
     E2, G2 = engine.energy_grad_batch(c2, prog, obs, th)
     assert np.array_equal(E0, E2) and np.array_equal(G0, G2)
     c2.set_comm(0, 1, None)
+
+
+def test_sparse_energy_paths(ctx):
+    """energy(ansatz, theta, SparseCOO) (variational.cpp:45-52): host and device
+    COO agree with the Pauli-sum energy for batches, c64 and c128; dimension
+    mismatch is rejected with the reference message."""
+    from paper_2602_14167_b200 import engine
+    from paper_2602_14167_b200.rng import RngStream
+    h = po.heisenberg(9, 1.0, 0.7, 0.4)
+    _, ops, P = po.hea_template(9, 2)
+    streams = RngStream(11).split(5)
+    th = np.array([[s.normal() for _ in range(P)] for s in streams])
+    obs = engine.Observable(ctx, 9, h.codes, h.wr + 1j * h.wi)
+    rows, cols, vals = engine.pauli_sum_to_coo(ctx, obs)
+    drows, dcols, dvals = engine.pauli_sum_to_coo(ctx, obs, device=True)
+    for prec, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        prog = engine.Program(ctx, 9, ops, P, prec)
+        E, _ = engine.energy_grad_batch(ctx, prog, obs, th, grads=False)
+        Es = engine.sparse_energy(ctx, prog, th, 1 << 9, rows, cols, vals)
+        Ed = engine.sparse_energy(ctx, prog, th, 1 << 9, drows, dcols, dvals)
+        assert np.array_equal(Es, Ed)
+        assert np.abs(Es - E).max() <= tol * np.abs(E).max()
+    ref = [po.energy(po.Ansatz(9, ops, P), t, h) for t in th]
+    assert np.abs(Es - ref).max() <= 1e-5 * np.abs(ref).max()
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        engine.sparse_energy(ctx, prog, th[:1], 1 << 8, rows, cols, vals)
