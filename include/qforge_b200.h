@@ -188,6 +188,18 @@ int qf_sparse_energy(qf_ctx* ctx, const qf_program* prog, int batch, const doubl
                      int64_t nnz, const int64_t* rows, const int64_t* cols, const double* vals, int coo_on_device,
                      double* energies);
 
+/* Trajectory workload (reference experiments.cpp:210-250, exp_mipt_haar): for
+ * each of `trajectories` streams RngStream(seed).split(trajectories)[t], depth
+ * brickwork layers of haar_su4 gates on (i, i+1), i = layer % 2, 2, ..., each
+ * qubit measured with probability p (measure_collapse, circuit.cpp:391-429),
+ * then entropies[t] = subsystem_entropy(psi, {0 .. n/2 - 1}) in bits.  Gates run
+ * as batched sweeps with per-trajectory matrices, measurements as batched
+ * histogram / collapse passes; the entropy spectrum uses cuBLAS + cuSOLVER
+ * (loaded at run time).  n in [2, 20], p in [0, 1], trajectories >= 1.
+ * n_measurements (optional) receives the total number of collapses. */
+int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint64_t seed, int precision,
+                 double* entropies, long long* n_measurements);
+
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
  * float64 device pointers.  Single-GPU semantics (no collective). */

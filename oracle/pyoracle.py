@@ -266,3 +266,82 @@ def vqe_run(a: Ansatz, theta0, h: Hamil, steps, lr, mode="parameter_shift", work
     _check(lib().qo_vqe_run(ctypes.byref(a.s), B, _d(th), ctypes.byref(h.s), steps, lr, MODES[mode], workers,
                             _d(traces), _d(fin), _d(be), ctypes.byref(bi)))
     return traces, fin, float(be[0]), bi.value
+
+
+# ------------------------------------------------------------------ trajectories
+# TEST INFRASTRUCTURE ONLY: numpy restatement of the MIPT-Haar experiment
+# (reference proj/src/experiments.cpp:210-250) for parity tests at small n.
+def haar_su4(rng: Rng) -> np.ndarray:
+    """circuit.cpp:472-489: QR of a complex Gaussian 4x4, R-diagonal phases moved
+    into Q, Q *= det(Q)^(-1/4).  cplx(rng.normal(), rng.normal()) draws the
+    imaginary part first (gcc argument order, pinned with the RNG fixtures)."""
+    g = np.zeros((4, 4), complex)
+    for r in range(4):
+        for c in range(4):
+            im = rng.normal()
+            re = rng.normal()
+            g[r, c] = re + 1j * im
+    q, rr = np.linalg.qr(g)
+    d = np.diag(rr)
+    ph = np.where(np.abs(d) > 0, d / np.where(np.abs(d) > 0, np.abs(d), 1), 1.0)
+    q = q * ph[None, :]
+    q = q * np.exp(-1j * np.angle(np.linalg.det(q)) / 4.0)
+    return q
+
+
+def apply_2q(psi: np.ndarray, n: int, u: np.ndarray, a: int, b: int) -> np.ndarray:
+    """apply_local_unitary(psi, u, {a, b}) with wire a the most significant local bit."""
+    t = psi.reshape([2] * n)
+    t = np.moveaxis(t, [a, b], [0, 1]).reshape(4, -1)
+    t = (u @ t).reshape([2, 2] + [2] * (n - 2))
+    return np.moveaxis(t, [0, 1], [a, b]).reshape(-1)
+
+
+def measure_collapse(psi: np.ndarray, n: int, wire: int, u: float) -> np.ndarray:
+    """circuit.cpp:391-429 for d = 2 with the uniform already drawn."""
+    t = psi.reshape([2] * n)
+    sel = [slice(None)] * n
+    probs = []
+    for o in range(2):
+        sel[wire] = o
+        probs.append(float(np.sum(np.abs(t[tuple(sel)]) ** 2)))
+    outcome, acc = 1, 0.0
+    for o in range(2):
+        acc += probs[o]
+        if u < acc:
+            outcome = o
+            break
+    out = np.zeros_like(t)
+    sel[wire] = outcome
+    out[tuple(sel)] = t[tuple(sel)] / np.sqrt(probs[outcome])
+    return out.reshape(-1)
+
+
+def subsystem_entropy_half(psi: np.ndarray, n: int) -> float:
+    """circuit.cpp:431-470 with keep = {0 .. n/2 - 1} (the leading wires)."""
+    k = n // 2
+    s = np.linalg.svd(psi.reshape(1 << k, 1 << (n - k)), compute_uv=False)
+    ent = 0.0
+    for v in s:
+        p = min(max(v * v, 0.0), 1.0)
+        if p > 1e-15:
+            ent -= p * np.log2(p)
+    return max(ent, 0.0)
+
+
+def mipt_haar(n: int, depth: int, p: float, trajectories: int, seed: int):
+    """exp_mipt_haar (experiments.cpp:210-250): per-trajectory half-chain entropies."""
+    streams = Rng(seed).split(trajectories)
+    ents = []
+    for tr in range(trajectories):
+        rs = streams[tr]
+        psi = np.zeros(1 << n, complex)
+        psi[0] = 1.0
+        for layer in range(depth):
+            for i in range(layer % 2, n - 1, 2):
+                psi = apply_2q(psi, n, haar_su4(rs), i, i + 1)
+            for q in range(n):
+                if rs.uniform() < p:
+                    psi = measure_collapse(psi, n, q, rs.uniform())
+        ents.append(subsystem_entropy_half(psi, n))
+    return np.array(ents)

@@ -21,7 +21,14 @@
 #include <string>
 #include <vector>
 
+#include <complex>
+#include <thread>
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include "../../include/qforge_b200.h"
+#include "../../include/qforge/rng.hpp"
 #include "kernels.cuh"
 #include "jit.hpp"
 #include "plan.hpp"
@@ -62,6 +69,10 @@ struct DevBuf {
         p = nullptr;
         cap = 0;
     }
+};
+
+struct LocalBuf : DevBuf {  // function-scoped device scratch
+    ~LocalBuf() { release(); }
 };
 
 struct HostBuf {
@@ -488,6 +499,106 @@ int check_thetas(const qf_program* prog, int batch, const double* thetas) {
     }
     return QF_OK;
 }
+
+// ------------------------------------------------------------------ trajectories
+// haar_su4 (reference circuit.cpp:472-489): QR of a complex Gaussian 4x4 with the
+// phases of R's diagonal moved into Q (the unique QR with positive diagonal,
+// computed here by modified Gram-Schmidt), then Q *= det(Q)^(-1/4).  Entries are
+// drawn as cplx(rng.normal(), rng.normal()); gcc evaluates those arguments right
+// to left, so the imaginary part is drawn first (pinned by
+// tests/golden/rng_known_answers.txt through the same convention).
+using cd = std::complex<double>;
+void haar_su4(qforge::RngStream& rng, cd q[4][4]) {
+    cd g[4][4];
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            const double im = rng.normal();
+            const double re = rng.normal();
+            g[r][c] = cd(re, im);
+        }
+    for (int j = 0; j < 4; ++j) {
+        cd v[4] = {g[0][j], g[1][j], g[2][j], g[3][j]};
+        for (int i = 0; i < j; ++i) {
+            cd d = 0;
+            for (int r = 0; r < 4; ++r) d += std::conj(q[r][i]) * v[r];
+            for (int r = 0; r < 4; ++r) v[r] -= d * q[r][i];
+        }
+        double nr = 0;
+        for (int r = 0; r < 4; ++r) nr += std::norm(v[r]);
+        nr = std::sqrt(nr);
+        for (int r = 0; r < 4; ++r) q[r][j] = v[r] / nr;
+    }
+    // det by Gaussian elimination with partial pivoting
+    cd a[4][4];
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) a[r][c] = q[r][c];
+    cd det = 1.0;
+    for (int c = 0; c < 4; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < 4; ++r)
+            if (std::abs(a[r][c]) > std::abs(a[piv][c])) piv = r;
+        if (piv != c) {
+            for (int k = 0; k < 4; ++k) std::swap(a[piv][k], a[c][k]);
+            det = -det;
+        }
+        det *= a[c][c];
+        for (int r = c + 1; r < 4; ++r) {
+            const cd f = a[r][c] / a[c][c];
+            for (int k = c; k < 4; ++k) a[r][k] -= f * a[c][k];
+        }
+    }
+    const cd ph = std::polar(1.0, -std::arg(det) / 4.0);
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) q[r][c] *= ph;
+}
+
+// cuBLAS / cuSOLVER, loaded at run time (only the trajectory entropy needs them)
+struct LinAlg {
+    void *hb = nullptr, *hs = nullptr;
+    cublasHandle_t cb = nullptr;
+    cusolverDnHandle_t cs = nullptr;
+    decltype(&cublasCreate_v2) bcreate = nullptr;
+    decltype(&cublasSetStream_v2) bstream = nullptr;
+    decltype(&cublasZherk_v2) zherk = nullptr;
+    decltype(&cusolverDnCreate) screate = nullptr;
+    decltype(&cusolverDnSetStream) sstream = nullptr;
+    decltype(&cusolverDnZheevd_bufferSize) zheevd_ws = nullptr;
+    decltype(&cusolverDnZheevd) zheevd = nullptr;
+    std::string err;
+    bool load() {
+        if (cb && cs) return true;
+        const char* bl[] = {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12",
+                            "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12"};
+        const char* sl[] = {"libcusolver.so.11", "libcusolver.so", "/usr/local/cuda/lib64/libcusolver.so.11",
+                            "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cusolver/lib/libcusolver.so.11"};
+        for (const char* nm : bl)
+            if ((hb = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+        for (const char* nm : sl)
+            if ((hs = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!hb || !hs) {
+            err = "cuBLAS / cuSOLVER unavailable (libcublas.so.12 / libcusolver.so.11)";
+            return false;
+        }
+        bcreate = (decltype(bcreate))dlsym(hb, "cublasCreate_v2");
+        bstream = (decltype(bstream))dlsym(hb, "cublasSetStream_v2");
+        zherk = (decltype(zherk))dlsym(hb, "cublasZherk_v2");
+        screate = (decltype(screate))dlsym(hs, "cusolverDnCreate");
+        sstream = (decltype(sstream))dlsym(hs, "cusolverDnSetStream");
+        zheevd_ws = (decltype(zheevd_ws))dlsym(hs, "cusolverDnZheevd_bufferSize");
+        zheevd = (decltype(zheevd))dlsym(hs, "cusolverDnZheevd");
+        if (!bcreate || !bstream || !zherk || !screate || !sstream || !zheevd_ws || !zheevd) {
+            err = "cuBLAS / cuSOLVER lack required symbols";
+            return false;
+        }
+        if (bcreate(&cb) != CUBLAS_STATUS_SUCCESS || screate(&cs) != CUSOLVER_STATUS_SUCCESS) {
+            err = "cuBLAS / cuSOLVER handle creation failed";
+            return false;
+        }
+        return true;
+    }
+};
+LinAlg g_linalg;
+std::mutex g_linalg_mu;
 
 }  // namespace
 
@@ -1210,6 +1321,228 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
         QF_CUDA(cudaMemcpyAsync(vals, dv, (size_t)total * 16, cudaMemcpyDeviceToHost, s));
     }
     QF_CUDA(cudaStreamSynchronize(s));
+    return QF_OK;
+}
+
+int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint64_t seed, int precision,
+                 double* entropies, long long* n_measurements) {
+    // reference experiments.cpp:210-250 (exp_mipt_haar) with circuit.cpp:391-429 (measure_collapse),
+    // :431-470 (subsystem_entropy of qubits [0, n/2)) and :472-489 (haar_su4)
+    if (!ctx || !entropies) return set_err(QF_EINVAL, "qf_mipt_haar: null argument");
+    if (n < 2 || n > 20) return set_err(QF_EINVAL, "mipt-haar: N must lie in [2, 20]");
+    if (!(p >= 0.0 && p <= 1.0)) return set_err(QF_EINVAL, "mipt-haar: p must lie in [0, 1]");
+    if (trajectories < 1) return set_err(QF_EINVAL, "mipt-haar: trajectories must be >= 1");
+    if (precision != QF_C64 && precision != QF_C128) return set_err(QF_EINVAL, "qf_mipt_haar: bad precision");
+    depth = std::max(depth, 0);
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const int npmax = n / 2;
+    const size_t mat_doubles = (size_t)npmax * 32;  // per state and layer
+
+    // ---- host randomness, in the reference's draw order (per trajectory stream)
+    struct Meas {
+        int layer, pos;
+        double u;
+    };
+    std::vector<double> mats((size_t)std::max(depth, 1) * trajectories * mat_doubles, 0.0);
+    std::vector<std::vector<Meas>> meas(trajectories);
+    {
+        const auto streams = qforge::RngStream(seed).split((size_t)trajectories);
+        auto work = [&](int t0, int t1) {
+            for (int tr = t0; tr < t1; ++tr) {
+                qforge::RngStream rs = streams[tr];
+                for (int layer = 0; layer < depth; ++layer) {
+                    int j = 0;
+                    for (int i = layer % 2; i + 1 < n; i += 2, ++j) {
+                        cd q[4][4];
+                        haar_su4(rs, q);
+                        double* m = mats.data() + ((size_t)layer * trajectories + tr) * mat_doubles + (size_t)j * 32;
+                        for (int r = 0; r < 4; ++r)
+                            for (int c = 0; c < 4; ++c) {
+                                m[(r * 4 + c) * 2] = q[r][c].real();
+                                m[(r * 4 + c) * 2 + 1] = q[r][c].imag();
+                            }
+                    }
+                    for (int qb = 0; qb < n; ++qb)
+                        if (rs.uniform() < p) meas[tr].push_back({layer, n - 1 - qb, rs.uniform()});
+                }
+            }
+        };
+        const int nthr = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), trajectories));
+        std::vector<std::thread> pool;
+        for (int t = 0; t < nthr; ++t)
+            pool.emplace_back(work, (int)((long long)trajectories * t / nthr),
+                              (int)((long long)trajectories * (t + 1) / nthr));
+        for (auto& th : pool) th.join();
+    }
+    long long total_meas = 0;
+    for (auto& v : meas) total_meas += (long long)v.size();
+    if (n_measurements) *n_measurements = total_meas;
+
+    // ---- layer programs: brickwork of dense two-qubit gates, matrices per state
+    qf_program* progs[2] = {nullptr, nullptr};
+    struct ProgGuard {
+        qf_program** p;
+        ~ProgGuard() {
+            for (int i = 0; i < 2; ++i)
+                if (p[i]) qf_program_destroy(p[i]);
+        }
+    } guard{progs};
+    std::vector<double> dummy;
+    for (int k = 0; k < 4; ++k)  // a dense unitary (classified as a general gate; replaced per state)
+        for (int l = 0; l < 4; ++l) {
+            const double ang = 2.0 * M_PI * k * l / 4.0;
+            dummy.push_back(0.5 * std::cos(ang));
+            dummy.push_back(0.5 * std::sin(ang));
+        }
+    for (int par = 0; par < 2; ++par) {
+        std::vector<qf_op> ops;
+        std::vector<double> ms;
+        int j = 0;
+        for (int i = par; i + 1 < n; i += 2, ++j) {
+            qf_op o{};
+            o.kind = QF_UNITARY;
+            o.q0 = i;
+            o.q1 = i + 1;
+            o.slot = -1;
+            o.coef = 1.0;
+            o.mat = j;
+            ops.push_back(o);
+            ms.insert(ms.end(), dummy.begin(), dummy.end());
+        }
+        if (ops.empty()) continue;
+        int rc = qf_program_create(ctx, n, (int)ops.size(), ops.data(), ms.data(), j, 0, precision, &progs[par]);
+        if (rc) return rc;
+    }
+
+    // ---- chunks of trajectories
+    const size_t N = size_t(1) << n;
+    const size_t vs = vsize(precision);
+    const int keep = n / 2;
+    const int64_t dk = (int64_t)1 << keep, de = (int64_t)1 << (n - keep);
+    size_t fr = 0, tot = 0;
+    QF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t budget = (size_t)(0.5 * (double)(fr + ctx->psi.cap));
+    const size_t per_state = N * vs + (size_t)depth * mat_doubles * 8 + (1u << kMeasMax) * 8 + 256;
+    int bc = (int)std::max<size_t>(1, std::min<size_t>(budget / per_state, (size_t)trajectories));
+    bc = std::min(bc, 65535);
+    QF_CUDA(ctx->psi.reserve((size_t)bc * N * vs));
+    LocalBuf d_mats, d_rounds, d_hist, d_mask, d_bits, d_scale, d_out, d_conv, d_rho, d_w, d_work, d_info;
+    QF_CUDA(d_mats.reserve(std::max<size_t>(16, (size_t)depth * bc * mat_doubles * 8)));
+    QF_CUDA(d_rounds.reserve((size_t)bc * sizeof(MeasRound)));
+    QF_CUDA(d_hist.reserve((size_t)bc * (1u << kMeasMax) * 8));
+    QF_CUDA(d_mask.reserve((size_t)bc * 4));
+    QF_CUDA(d_bits.reserve((size_t)bc * 4));
+    QF_CUDA(d_scale.reserve((size_t)bc * 8));
+    QF_CUDA(d_out.reserve((size_t)bc * kMeasMax * 4));
+    QF_CUDA(d_conv.reserve(N * 16));
+    QF_CUDA(d_rho.reserve((size_t)dk * dk * 16));
+    QF_CUDA(d_w.reserve((size_t)bc * dk * 8));
+    QF_CUDA(d_info.reserve(16));
+    {
+        std::lock_guard<std::mutex> lk(g_linalg_mu);
+        if (!g_linalg.load()) return set_err(QF_ERUNTIME, g_linalg.err);
+    }
+    LinAlg& la = g_linalg;
+    int lwork = 0;
+    if (la.zheevd_ws(la.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk, (const cuDoubleComplex*)d_rho.p,
+                     (int)dk, (const double*)d_w.p, &lwork) != CUSOLVER_STATUS_SUCCESS)
+        return set_err(QF_ERUNTIME, "cusolverDnZheevd_bufferSize failed");
+    QF_CUDA(d_work.reserve(std::max<size_t>(16, (size_t)lwork * 16)));
+    std::vector<double> w_host((size_t)bc * dk);
+    std::vector<MeasRound> rounds(bc);
+    for (int t0 = 0; t0 < trajectories; t0 += bc) {
+        const int nb = std::min(bc, trajectories - t0);
+        // matrices of this chunk, layer-major [depth][nb][npmax][32]
+        for (int layer = 0; layer < depth; ++layer)
+            QF_CUDA(cudaMemcpyAsync((double*)d_mats.p + (size_t)layer * nb * mat_doubles,
+                                    mats.data() + ((size_t)layer * trajectories + t0) * mat_doubles,
+                                    (size_t)nb * mat_doubles * 8, cudaMemcpyHostToDevice, s));
+        QF_CUDA(launch_set_basis0(precision, ctx->psi.p, n, nb, s));
+        std::vector<size_t> cursor(nb, 0);
+        for (int layer = 0; layer < depth; ++layer) {
+            qf_program* prog = progs[layer % 2];
+            if (prog) {
+                const ProgramPlan& P = prog->plan;
+                SweepArgs sa{};
+                sa.psi = ctx->psi.p;
+                sa.n = n;
+                sa.gates = (const DevGate*)prog->gates.p;
+                sa.cmats = (const double*)d_mats.p + (size_t)layer * nb * mat_doubles;
+                QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, (size_t)nb * P.fwd.total_mat * vs)));
+                sa.gmat = ctx->gmat.p;
+                sa.gmat_stride = P.fwd.total_mat;
+                QF_CUDA(launch_mats(precision, false, (const DevOp*)prog->fwd.ops.p, (const int*)prog->goff_fwd.p,
+                                    (int)P.fwd.ops.size(), sa.gates, sa.cmats, nullptr, 0, 0, ctx->gmat.p,
+                                    sa.gmat_stride, 0, nb, s, mat_doubles));
+                sa.phases = (const DevPhase*)prog->fwd.phases.p;
+                sa.ops = (const DevOp*)prog->fwd.ops.p;
+                for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
+                    sa.sw = P.fwd.sweeps[i];
+                    if (prog->use_jit)
+                        QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), nb, s));
+                    else
+                        QF_CUDA(launch_sweep(precision, false, sa, nb, P.fwd.max_mat, 0, s));
+                    ctx->launches++;
+                }
+            }
+            // measurements of this layer, in rounds of up to kMeasMax per trajectory
+            for (;;) {
+                int maxc = 0;
+                for (int b = 0; b < nb; ++b) {
+                    const auto& v = meas[t0 + b];
+                    MeasRound& r = rounds[b];
+                    r.count = 0;
+                    while (cursor[b] < v.size() && v[cursor[b]].layer == layer && r.count < kMeasMax) {
+                        r.pos[r.count] = v[cursor[b]].pos;
+                        r.u[r.count] = v[cursor[b]].u;
+                        ++r.count;
+                        ++cursor[b];
+                    }
+                    maxc = std::max(maxc, r.count);
+                }
+                if (maxc == 0) break;
+                QF_CUDA(cudaMemcpyAsync(d_rounds.p, rounds.data(), (size_t)nb * sizeof(MeasRound),
+                                        cudaMemcpyHostToDevice, s));
+                QF_CUDA(launch_meas_hist(precision, ctx->psi.p, n, nb, (const MeasRound*)d_rounds.p, maxc,
+                                         (double*)d_hist.p, s));
+                QF_CUDA(launch_meas_decide((const MeasRound*)d_rounds.p, (const double*)d_hist.p, nb,
+                                           (uint32_t*)d_mask.p, (uint32_t*)d_bits.p, (double*)d_scale.p,
+                                           (int*)d_out.p, s));
+                QF_CUDA(launch_meas_project(precision, ctx->psi.p, n, nb, (const MeasRound*)d_rounds.p,
+                                            (const uint32_t*)d_mask.p, (const uint32_t*)d_bits.p,
+                                            (const double*)d_scale.p, s));
+                QF_CUDA(cudaStreamSynchronize(s));  // rounds[] is reused by the next upload
+                ctx->launches += 3;
+            }
+        }
+        // half-chain entropy: eigenvalues of A^H A, A = psi as a (de x dk) column-major matrix
+        if (la.bstream(la.cb, s) != CUBLAS_STATUS_SUCCESS || la.sstream(la.cs, s) != CUSOLVER_STATUS_SUCCESS)
+            return set_err(QF_ERUNTIME, "cuBLAS / cuSOLVER stream binding failed");
+        const double one = 1.0, zero = 0.0;
+        for (int b = 0; b < nb; ++b) {
+            QF_CUDA(launch_convert_state(precision, (const unsigned char*)ctx->psi.p + (size_t)b * N * vs,
+                                         (double*)d_conv.p, (int64_t)N, s));
+            if (la.zherk(la.cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, (int)dk, (int)de, &one,
+                         (const cuDoubleComplex*)d_conv.p, (int)de, &zero, (cuDoubleComplex*)d_rho.p,
+                         (int)dk) != CUBLAS_STATUS_SUCCESS)
+                return set_err(QF_ERUNTIME, "cublasZherk failed");
+            if (la.zheevd(la.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
+                          (cuDoubleComplex*)d_rho.p, (int)dk, (double*)d_w.p + (size_t)b * dk,
+                          (cuDoubleComplex*)d_work.p, lwork, (int*)d_info.p) != CUSOLVER_STATUS_SUCCESS)
+                return set_err(QF_ERUNTIME, "cusolverDnZheevd failed");
+        }
+        QF_CUDA(cudaMemcpyAsync(w_host.data(), d_w.p, (size_t)nb * dk * 8, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < nb; ++b) {
+            double ent = 0.0;
+            for (int64_t i = dk - 1; i >= 0; --i) {  // descending, as the reference's singular values
+                const double pr = std::clamp(w_host[(size_t)b * dk + i], 0.0, 1.0);
+                if (pr > 1e-15) ent -= pr * std::log2(pr);
+            }
+            entropies[t0 + b] = std::max(ent, 0.0);
+        }
+    }
     return QF_OK;
 }
 

@@ -136,12 +136,14 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
 template <typename RT, bool ADJ>
 __global__ void mats_kernel(const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
                             const double* cmats, const double* theta, int P, int batch_offset,
-                            typename CxT<RT>::T* out, int stride, int pass_base) {
+                            typename CxT<RT>::T* out, int stride, int pass_base, size_t cmats_stride) {
     const int b = blockIdx.y;
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= n_ops || goff[o] < 0) return;
     const DevOp op = ops[o];
-    build_matrix<typename CxT<RT>::T, ADJ>(op, gates[op.gate], theta + (size_t)(b + batch_offset) * P, cmats,
+    // cmats_stride > 0: every state has its own constant matrices (trajectories)
+    build_matrix<typename CxT<RT>::T, ADJ>(op, gates[op.gate], theta + (size_t)(b + batch_offset) * P,
+                                           cmats + (size_t)(b + batch_offset) * cmats_stride,
                                            out + (size_t)b * stride + pass_base + goff[o]);
 }
 
@@ -263,15 +265,15 @@ cudaError_t launch_hpsi(int prec, const HArgs& a, int batch, cudaStream_t s) {
 
 cudaError_t launch_mats(int prec, bool adj, const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
                         const double* cmats, const double* theta, int P, int batch_offset, void* out, int stride,
-                        int pass_base, int batch, cudaStream_t s) {
+                        int pass_base, int batch, cudaStream_t s, size_t cmats_stride) {
     if (n_ops == 0) return cudaSuccess;
     dim3 grid((n_ops + 127) / 128, batch);
     if (prec == QF_C128) {
-        if (adj) mats_kernel<double, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base);
-        else mats_kernel<double, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base);
+        if (adj) mats_kernel<double, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base, cmats_stride);
+        else mats_kernel<double, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (double2*)out, stride, pass_base, cmats_stride);
     } else {
-        if (adj) mats_kernel<float, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base);
-        else mats_kernel<float, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base);
+        if (adj) mats_kernel<float, true><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base, cmats_stride);
+        else mats_kernel<float, false><<<grid, 128, 0, s>>>(ops, goff, n_ops, gates, cmats, theta, P, batch_offset, (float2*)out, stride, pass_base, cmats_stride);
     }
     return cudaGetLastError();
 }

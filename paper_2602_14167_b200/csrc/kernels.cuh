@@ -22,7 +22,8 @@ cudaError_t launch_sweep(int prec, bool bwd, const SweepArgs& a, int batch, int 
 cudaError_t launch_hpsi(int prec, const HArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_mats(int prec, bool adj, const DevOp* ops, const int* goff, int n_ops, const DevGate* gates,
                         const double* cmats, const double* theta, int P, int batch_offset, void* out, int stride,
-                        int pass_base, int batch, cudaStream_t s);
+                        int pass_base, int batch, cudaStream_t s,
+                        size_t cmats_stride = 0);
 cudaError_t launch_init_state(int prec, void* psi, const void* init, int n, int batch,
                               cudaStream_t s);
 cudaError_t launch_reduce(const ReduceArgs& a, int batch, cudaStream_t s);
@@ -70,6 +71,25 @@ cudaError_t coo_scan(const int64_t* counts, int64_t* offsets, int64_t dim, void*
 int coo_energy_blocks(int64_t nnz);
 cudaError_t launch_coo_energy(int prec, const int64_t* rows, const int64_t* cols, const double2* vals, int64_t nnz,
                               const void* psi, double* part, cudaStream_t s);
+// ---- trajectories (reference experiments.cpp:210-250, circuit.cpp:391-429) ----
+// Up to kMeasMax projective measurements per state and round: hist[b][beta] =
+// sum |psi|^2 over amplitudes whose measured bits equal beta (fixed order);
+// mipt_decide replays measure_collapse sequentially on the histogram; project
+// zeroes the rejected amplitudes and rescales the rest.
+constexpr int kMeasMax = 8;
+struct MeasRound {
+    int count;                   // measurements of this state in this round
+    int pos[kMeasMax];           // memory bit positions (n - 1 - wire), in order
+    double u[kMeasMax];          // the uniform drawn by measure_collapse
+};
+cudaError_t launch_meas_hist(int prec, const void* psi, int n, int batch, const MeasRound* rounds, int max_count,
+                             double* hist, cudaStream_t s);
+cudaError_t launch_meas_decide(const MeasRound* rounds, const double* hist, int batch, uint32_t* mask, uint32_t* bits,
+                               double* scale, int* outcomes, cudaStream_t s);
+cudaError_t launch_meas_project(int prec, void* psi, int n, int batch, const MeasRound* rounds, const uint32_t* mask,
+                                const uint32_t* bits, const double* scale, cudaStream_t s);
+cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);
+
 // rows / cols ascending per row, complex128 values
 cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n_terms, const CooEvent* ev,
                              int n_ev, int n, const int64_t* offsets,

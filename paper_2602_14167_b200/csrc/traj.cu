@@ -1,0 +1,169 @@
+// traj.cu -- projective measurements of batched trajectories (measure_collapse,
+// reference circuit.cpp:391-429) for the trajectory workloads of SURVEY.md 8f
+// row 4 (MIPT-Haar, experiments.cpp:210-250).  All reductions are fixed order.
+#include "kernels.cuh"
+
+namespace qfb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t pdep32(uint32_t t, uint32_t m) {
+    uint32_t r = 0;
+    while (m) {
+        const uint32_t low = m & (0u - m);
+        if (t & 1) r |= low;
+        t >>= 1;
+        m ^= low;
+    }
+    return r;
+}
+
+// block (beta, b): sum of |psi[x]|^2 over x whose measured bits spell beta
+template <typename V>
+__global__ void __launch_bounds__(256) meas_hist_kernel(const V* psi, int n, const MeasRound* rounds, double* hist) {
+    __shared__ double red[8];
+    const int b = blockIdx.y;
+    const uint32_t beta = blockIdx.x;
+    const MeasRound r = rounds[b];
+    if (r.count == 0 || beta >= (1u << r.count)) return;
+    uint32_t mask = 0, dep = 0;
+    for (int k = 0; k < r.count; ++k) {
+        mask |= 1u << r.pos[k];
+        if ((beta >> k) & 1) dep |= 1u << r.pos[k];
+    }
+    const uint32_t N = 1u << n, free = (N - 1) & ~mask;
+    const uint32_t rest = 1u << (n - r.count);
+    const V* ps = psi + (size_t)b * N;
+    // walk the free bits as a counter: x -> ((x | mask) + step) & free, step = pdep(T)
+    const uint32_t step = pdep32(blockDim.x, free);
+    uint32_t x = pdep32(threadIdx.x, free);
+    double acc = 0.0;
+    for (uint32_t i = threadIdx.x; i < rest; i += blockDim.x) {
+        const V a = ps[x | dep];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+        x = ((x | mask) + step) & free;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        hist[(size_t)b * (1u << kMeasMax) + beta] = t;
+    }
+}
+
+// thread per state: measure_collapse (d = 2) for each measurement in order
+__global__ void meas_decide_kernel(const MeasRound* rounds, const double* hist, int batch, uint32_t* mask,
+                                   uint32_t* bits, double* scale, int* outcomes) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const MeasRound r = rounds[b];
+    const double* h = hist + (size_t)b * (1u << kMeasMax);
+    uint32_t m = 0, o_bits = 0;
+    double cum = 1.0, sc = 1.0;  // cum = product of the outcome probabilities so far
+    for (int k = 0; k < r.count; ++k) {
+        double a[2] = {0.0, 0.0};
+        const uint32_t lowmask = (1u << k) - 1;
+        for (uint32_t beta = 0; beta < (1u << r.count); ++beta)
+            if ((beta & lowmask) == (o_bits & lowmask)) a[(beta >> k) & 1] += h[beta];
+        const double probs[2] = {k ? a[0] / cum : a[0], k ? a[1] / cum : a[1]};
+        int outcome = 1;
+        double acc = 0.0;
+        for (int o = 0; o < 2; ++o) {
+            acc += probs[o];
+            if (r.u[k] < acc) {
+                outcome = o;
+                break;
+            }
+        }
+        const double p = probs[outcome];
+        sc *= 1.0 / sqrt(p);
+        cum *= p;
+        o_bits |= (uint32_t)outcome << k;
+        m |= 1u << r.pos[k];
+        outcomes[(size_t)b * kMeasMax + k] = outcome;
+    }
+    uint32_t bb = 0;
+    for (int k = 0; k < r.count; ++k)
+        if ((o_bits >> k) & 1) bb |= 1u << r.pos[k];
+    mask[b] = m;
+    bits[b] = bb;
+    scale[b] = sc;
+}
+
+template <typename V>
+__global__ void meas_project_kernel(V* psi, int n, const MeasRound* rounds, const uint32_t* mask, const uint32_t* bits,
+                                    const double* scale) {
+    const int b = blockIdx.y;
+    if (rounds[b].count == 0) return;
+    const uint32_t N = 1u << n, m = mask[b], want = bits[b];
+    const double sc = scale[b];
+    V* ps = psi + (size_t)b * N;
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+        V a = ps[x];
+        if ((x & m) == want) {
+            a.x = (decltype(a.x))((double)a.x * sc);
+            a.y = (decltype(a.y))((double)a.y * sc);
+        } else {
+            a.x = 0;
+            a.y = 0;
+        }
+        ps[x] = a;
+    }
+}
+
+template <typename V>
+__global__ void set_basis0_kernel(V* psi, int n, int batch) {
+    const uint32_t N = 1u << n;
+    const size_t total = (size_t)batch * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        V a;
+        a.x = (i % N) == 0 ? 1 : 0;
+        a.y = 0;
+        psi[i] = a;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_meas_hist(int prec, const void* psi, int n, int batch, const MeasRound* rounds, int max_count,
+                             double* hist, cudaStream_t s) {
+    if (batch == 0 || max_count == 0) return cudaSuccess;
+    dim3 grid(1u << max_count, batch);
+    if (prec == 1)
+        meas_hist_kernel<double2><<<grid, 256, 0, s>>>((const double2*)psi, n, rounds, hist);
+    else
+        meas_hist_kernel<float2><<<grid, 256, 0, s>>>((const float2*)psi, n, rounds, hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_meas_decide(const MeasRound* rounds, const double* hist, int batch, uint32_t* mask, uint32_t* bits,
+                               double* scale, int* outcomes, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    meas_decide_kernel<<<(batch + 127) / 128, 128, 0, s>>>(rounds, hist, batch, mask, bits, scale, outcomes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_meas_project(int prec, void* psi, int n, int batch, const MeasRound* rounds, const uint32_t* mask,
+                                const uint32_t* bits, const double* scale, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    const uint32_t N = 1u << n;
+    dim3 grid(std::max(1u, std::min<uint32_t>(N / 1024, 256)), batch);
+    if (prec == 1)
+        meas_project_kernel<double2><<<grid, 256, 0, s>>>((double2*)psi, n, rounds, mask, bits, scale);
+    else
+        meas_project_kernel<float2><<<grid, 256, 0, s>>>((float2*)psi, n, rounds, mask, bits, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    if (prec == 1)
+        set_basis0_kernel<double2><<<148 * 8, 256, 0, s>>>((double2*)psi, n, batch);
+    else
+        set_basis0_kernel<float2><<<148 * 8, 256, 0, s>>>((float2*)psi, n, batch);
+    return cudaGetLastError();
+}
+
+}  // namespace qfb

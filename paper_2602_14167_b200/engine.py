@@ -323,6 +323,16 @@ def sparse_energy(ctx: Context, prog: Program, thetas, dim: int, rows, cols, val
     return out
 
 
+def mipt_haar(ctx: Context, n: int, depth: int, p: float, trajectories: int, seed: int, precision="c64"):
+    """Half-chain entropies of MIPT-Haar trajectories (qf_mipt_haar, reference
+    experiments.cpp:210-250); returns (entropies[trajectories], measurement count)."""
+    out = np.zeros(int(trajectories))
+    cnt = ctypes.c_longlong()
+    check(ctx.lib.qf_mipt_haar(ctx.handle, int(n), int(depth), float(p), int(trajectories), int(seed),
+                               PRECISIONS[precision], dptr(out), ctypes.byref(cnt)))
+    return out, int(cnt.value)
+
+
 def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
                      eps=1e-8) -> None:
     B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))

@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""MIPT-Haar trajectories on the GPU (qf_mipt_haar) against the paper's Table IV
+(20 qubits x 40 layers, batch 1000, complex64: 84.16 s on
+H200 = 0.084 s/trajectory; 1097 s on the M4 Pro CPU).  p = 0.1 (the reference's
+default, experiments.cpp:213).  Wall clock of the whole call (host RNG + Haar
+matrices, batched sweeps, measurement passes, entropy spectra), best of reps;
+CPU baseline: the numpy oracle restatement on a bounded sample."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2602_14167_b200 import engine  # noqa: E402
+
+n = int(os.environ.get("MIPT_N", 20))
+D = int(os.environ.get("MIPT_D", 40))
+T = int(os.environ.get("MIPT_T", 1000))
+p = float(os.environ.get("MIPT_P", 0.1))
+prec = os.environ.get("MIPT_PREC", "c64")
+ctx = engine.default_context(0)
+engine.mipt_haar(ctx, n, 2, p, 4, 7, prec)  # warm-up: JIT kernels, cuBLAS / cuSOLVER handles
+best = None
+for rep in range(2):
+    t0 = time.perf_counter()
+    ent, nmeas = engine.mipt_haar(ctx, n, D, p, T, 2026 + rep, prec)
+    dt = time.perf_counter() - t0
+    best = dt if best is None else min(best, dt)
+rec = {"n": n, "depth": D, "trajectories": T, "p": p, "precision": prec, "seconds": best,
+       "s_per_traj": best / T, "mean_entropy_bits": float(ent.mean()), "measurements": nmeas,
+       "paper_h200_s_per_traj": 0.08416 if (n, D, T) == (20, 40, 1000) else None}
+if rec["paper_h200_s_per_traj"]:
+    rec["speedup_vs_paper"] = rec["paper_h200_s_per_traj"] / rec["s_per_traj"]
+if os.environ.get("MIPT_CPU", "1") == "1":
+    from oracle import pyoracle as po
+    t0 = time.perf_counter()
+    po.mipt_haar(n, D, p, 1, 5)
+    rec["cpu_oracle_s_per_traj"] = time.perf_counter() - t0
+    rec["cpu_sample"] = "1 trajectory, numpy restatement (oracle/pyoracle.py), single process"
+print(json.dumps(rec), flush=True)
