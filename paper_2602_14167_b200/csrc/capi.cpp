@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
 #include <complex>
 #include <thread>
 
@@ -599,6 +600,49 @@ struct LinAlg {
 };
 LinAlg g_linalg;
 std::mutex g_linalg_mu;
+
+// One ZHEEVD of a 1024 x 1024 matrix is latency bound (~12 ms on one stream);
+// spectra run concurrently on kEigLanes host threads, each with its own stream,
+// cuBLAS / cuSOLVER handles and scratch.
+constexpr int kEigLanes = 8;
+struct EigLane {
+    int device = -1;
+    cudaStream_t st = nullptr;
+    cublasHandle_t cb = nullptr;
+    cusolverDnHandle_t cs = nullptr;
+    DevBuf conv, rho, work, info;
+    int64_t dk = 0;
+    int lwork = 0;
+};
+EigLane g_lanes[kEigLanes];
+
+int lane_setup(EigLane& L, const LinAlg& la, int device, int64_t dk, size_t N) {
+    if (L.device != device) {
+        if (L.st) {
+            cudaStreamDestroy(L.st);
+            L.st = nullptr;
+        }
+        L.cb = nullptr;
+        L.cs = nullptr;
+        L.device = device;
+    }
+    if (!L.st) QF_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    if (!L.cb && la.bcreate(&L.cb) != CUBLAS_STATUS_SUCCESS) return set_err(QF_ERUNTIME, "cublasCreate failed");
+    if (!L.cs && la.screate(&L.cs) != CUSOLVER_STATUS_SUCCESS) return set_err(QF_ERUNTIME, "cusolverDnCreate failed");
+    if (la.bstream(L.cb, L.st) != CUBLAS_STATUS_SUCCESS || la.sstream(L.cs, L.st) != CUSOLVER_STATUS_SUCCESS)
+        return set_err(QF_ERUNTIME, "cuBLAS / cuSOLVER stream binding failed");
+    QF_CUDA(L.conv.reserve(N * 16));
+    QF_CUDA(L.rho.reserve((size_t)dk * dk * 16));
+    QF_CUDA(L.info.reserve(16));
+    if (L.dk != dk) {
+        if (la.zheevd_ws(L.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
+                         (const cuDoubleComplex*)L.rho.p, (int)dk, nullptr, &L.lwork) != CUSOLVER_STATUS_SUCCESS)
+            return set_err(QF_ERUNTIME, "cusolverDnZheevd_bufferSize failed");
+        L.dk = dk;
+    }
+    QF_CUDA(L.work.reserve(std::max<size_t>(16, (size_t)L.lwork * 16)));
+    return QF_OK;
+}
 
 }  // namespace
 
@@ -1336,6 +1380,11 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     depth = std::max(depth, 0);
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->stream;
+    const bool tm = std::getenv("QF_MIPT_TIMING") != nullptr;  // development: phase timings on stderr
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    double t_gen = 0, t_circ = 0, t_ent = 0;
+    auto T0 = now();
     const int npmax = n / 2;
     const size_t mat_doubles = (size_t)npmax * 32;  // per state and layer
 
@@ -1377,6 +1426,7 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     }
     long long total_meas = 0;
     for (auto& v : meas) total_meas += (long long)v.size();
+    t_gen = secs(T0, now());
     if (n_measurements) *n_measurements = total_meas;
 
     // ---- layer programs: brickwork of dense two-qubit gates, matrices per state
@@ -1427,7 +1477,7 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     int bc = (int)std::max<size_t>(1, std::min<size_t>(budget / per_state, (size_t)trajectories));
     bc = std::min(bc, 65535);
     QF_CUDA(ctx->psi.reserve((size_t)bc * N * vs));
-    LocalBuf d_mats, d_rounds, d_hist, d_mask, d_bits, d_scale, d_out, d_conv, d_rho, d_w, d_work, d_info;
+    LocalBuf d_mats, d_rounds, d_hist, d_mask, d_bits, d_scale, d_out, d_w;
     QF_CUDA(d_mats.reserve(std::max<size_t>(16, (size_t)depth * bc * mat_doubles * 8)));
     QF_CUDA(d_rounds.reserve((size_t)bc * sizeof(MeasRound)));
     QF_CUDA(d_hist.reserve((size_t)bc * (1u << kMeasMax) * 8));
@@ -1435,20 +1485,15 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     QF_CUDA(d_bits.reserve((size_t)bc * 4));
     QF_CUDA(d_scale.reserve((size_t)bc * 8));
     QF_CUDA(d_out.reserve((size_t)bc * kMeasMax * 4));
-    QF_CUDA(d_conv.reserve(N * 16));
-    QF_CUDA(d_rho.reserve((size_t)dk * dk * 16));
     QF_CUDA(d_w.reserve((size_t)bc * dk * 8));
-    QF_CUDA(d_info.reserve(16));
-    {
-        std::lock_guard<std::mutex> lk(g_linalg_mu);
-        if (!g_linalg.load()) return set_err(QF_ERUNTIME, g_linalg.err);
-    }
+    std::lock_guard<std::mutex> linalg_lock(g_linalg_mu);  // the eigen lanes are process-wide
+    if (!g_linalg.load()) return set_err(QF_ERUNTIME, g_linalg.err);
     LinAlg& la = g_linalg;
-    int lwork = 0;
-    if (la.zheevd_ws(la.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk, (const cuDoubleComplex*)d_rho.p,
-                     (int)dk, (const double*)d_w.p, &lwork) != CUSOLVER_STATUS_SUCCESS)
-        return set_err(QF_ERUNTIME, "cusolverDnZheevd_bufferSize failed");
-    QF_CUDA(d_work.reserve(std::max<size_t>(16, (size_t)lwork * 16)));
+    const int lanes = std::max(1, std::min(kEigLanes, bc));
+    for (int l = 0; l < lanes; ++l) {
+        int rc = lane_setup(g_lanes[l], la, ctx->device, dk, N);
+        if (rc) return rc;
+    }
     std::vector<double> w_host((size_t)bc * dk);
     std::vector<MeasRound> rounds(bc);
     for (int t0 = 0; t0 < trajectories; t0 += bc) {
@@ -1516,21 +1561,55 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
                 ctx->launches += 3;
             }
         }
-        // half-chain entropy: eigenvalues of A^H A, A = psi as a (de x dk) column-major matrix
-        if (la.bstream(la.cb, s) != CUBLAS_STATUS_SUCCESS || la.sstream(la.cs, s) != CUSOLVER_STATUS_SUCCESS)
-            return set_err(QF_ERUNTIME, "cuBLAS / cuSOLVER stream binding failed");
-        const double one = 1.0, zero = 0.0;
-        for (int b = 0; b < nb; ++b) {
-            QF_CUDA(launch_convert_state(precision, (const unsigned char*)ctx->psi.p + (size_t)b * N * vs,
-                                         (double*)d_conv.p, (int64_t)N, s));
-            if (la.zherk(la.cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, (int)dk, (int)de, &one,
-                         (const cuDoubleComplex*)d_conv.p, (int)de, &zero, (cuDoubleComplex*)d_rho.p,
-                         (int)dk) != CUBLAS_STATUS_SUCCESS)
-                return set_err(QF_ERUNTIME, "cublasZherk failed");
-            if (la.zheevd(la.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
-                          (cuDoubleComplex*)d_rho.p, (int)dk, (double*)d_w.p + (size_t)b * dk,
-                          (cuDoubleComplex*)d_work.p, lwork, (int*)d_info.p) != CUSOLVER_STATUS_SUCCESS)
-                return set_err(QF_ERUNTIME, "cusolverDnZheevd failed");
+        if (tm) {
+            QF_CUDA(cudaStreamSynchronize(s));
+            t_circ += secs(T0, now());
+            T0 = now();
+        }
+        // half-chain entropy: eigenvalues of A^H A, A = psi as a (de x dk) column-major
+        // matrix (same spectrum as the reference's SVD of psi reshaped to dk x de)
+        QF_CUDA(cudaStreamSynchronize(s));
+        {
+            std::vector<std::thread> pool;
+            std::vector<int> lane_rc(lanes, QF_OK);
+            std::vector<std::string> lane_err(lanes);
+            for (int l = 0; l < lanes; ++l)
+                pool.emplace_back([&, l] {
+                    EigLane& L = g_lanes[l];
+                    cudaSetDevice(ctx->device);
+                    const double one = 1.0, zero = 0.0;
+                    // double-precision spectrum for both state precisions: a complex64 CHEEVD
+                    // loses the small Schmidt values (n = 20: -0.22 bits of mean entropy)
+                    for (int b = l; b < nb; b += lanes) {
+                        cudaError_t e = launch_convert_state(
+                            precision, (const unsigned char*)ctx->psi.p + (size_t)b * N * vs, (double*)L.conv.p,
+                            (int64_t)N, L.st);
+                        if (e != cudaSuccess) {
+                            lane_rc[l] = QF_ECUDA;
+                            lane_err[l] = cudaGetErrorString(e);
+                            return;
+                        }
+                        if (la.zherk(L.cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, (int)dk, (int)de, &one,
+                                     (const cuDoubleComplex*)L.conv.p, (int)de, &zero, (cuDoubleComplex*)L.rho.p,
+                                     (int)dk) != CUBLAS_STATUS_SUCCESS ||
+                            la.zheevd(L.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
+                                      (cuDoubleComplex*)L.rho.p, (int)dk, (double*)d_w.p + (size_t)b * dk,
+                                      (cuDoubleComplex*)L.work.p, L.lwork, (int*)L.info.p) !=
+                                CUSOLVER_STATUS_SUCCESS) {
+                            lane_rc[l] = QF_ERUNTIME;
+                            lane_err[l] = "cuBLAS ZHERK / cuSOLVER ZHEEVD failed";
+                            return;
+                        }
+                    }
+                    cudaError_t e = cudaStreamSynchronize(L.st);
+                    if (e != cudaSuccess) {
+                        lane_rc[l] = QF_ECUDA;
+                        lane_err[l] = cudaGetErrorString(e);
+                    }
+                });
+            for (auto& th : pool) th.join();
+            for (int l = 0; l < lanes; ++l)
+                if (lane_rc[l]) return set_err(lane_rc[l], "qf_mipt_haar: " + lane_err[l]);
         }
         QF_CUDA(cudaMemcpyAsync(w_host.data(), d_w.p, (size_t)nb * dk * 8, cudaMemcpyDeviceToHost, s));
         QF_CUDA(cudaStreamSynchronize(s));
@@ -1542,7 +1621,12 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
             }
             entropies[t0 + b] = std::max(ent, 0.0);
         }
+        if (tm) {
+            t_ent += secs(T0, now());
+            T0 = now();
+        }
     }
+    if (tm) fprintf(stderr, "qf_mipt_haar: host randomness %.3f s, circuits %.3f s, entropy %.3f s\n", t_gen, t_circ, t_ent);
     return QF_OK;
 }
 

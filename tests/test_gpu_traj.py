@@ -31,3 +31,12 @@ def test_mipt_haar_deterministic_and_validated(ctx):
                      ((6, 4, 0.1, 0), "trajectories")]:
         with pytest.raises(ValueError, match=msg):
             engine.mipt_haar(ctx, *bad, 1, "c64")
+
+
+def test_mipt_haar_precisions_agree_at_size(ctx):
+    """n = 16 (256 x 256 Schmidt problem, many tiny Schmidt values): complex64
+    trajectories give the complex128 entropies to 1e-4 (the spectrum is always
+    computed in double precision)."""
+    a, na = engine.mipt_haar(ctx, 16, 12, 0.1, 4, 31, "c64")
+    b, nb_ = engine.mipt_haar(ctx, 16, 12, 0.1, 4, 31, "c128")
+    assert na == nb_ and np.abs(a - b).max() < 1e-4, (a, b)
