@@ -1,7 +1,7 @@
-"""`qforge`-compatible command line for the GPU-backed VQE experiment
-(SURVEY.md 8f row 2).
+"""`qforge`-compatible command line for the GPU-backed experiments on the hot
+path: vqe-tfim and mipt-haar (8f row 4).
 
-    python -m paper_2602_14167_b200.cli vqe-tfim [--config F] [--seed S] [--workers W]
+    python -m paper_2602_14167_b200.cli {vqe-tfim,mipt-haar} [--config F] [--seed S] [--workers W]
                                                   [--out DIR] [--set key=value ...]
     python -m paper_2602_14167_b200.cli emit-summary DIR
 
@@ -21,7 +21,7 @@ import os
 import sys
 import time
 
-EXPERIMENTS = ["vqe-tfim"]
+EXPERIMENTS = ["vqe-tfim", "mipt-haar"]
 
 
 class ConfigError(Exception):
@@ -117,6 +117,32 @@ def exp_vqe_tfim(cfg, out, base, seed, workers):  # experiments.cpp:83-141
     return {"best_energy": res.best_energy, "best_index": res.best_index, "n": n, "g": g, "layers": layers}
 
 
+def exp_mipt_haar(cfg, out, base, seed, workers):  # experiments.cpp:210-250
+    from . import engine
+
+    n = _get(cfg, "N", 12, int)
+    depth = _get(cfg, "D", 24, int)
+    p = _get(cfg, "p", 0.1, float)
+    trajectories = _get(cfg, "trajectories", 100, int)
+    precision = _get(cfg, "precision", "c128", str)
+    if n < 2 or n > 20:
+        raise ConfigError("mipt-haar: N must lie in [2, 20]")
+    if p < 0.0 or p > 1.0:
+        raise ConfigError("mipt-haar: p must lie in [0, 1]")
+    if trajectories < 1:
+        raise ConfigError("mipt-haar: trajectories must be >= 1")
+    if precision not in ("c64", "c128"):
+        raise ConfigError("mipt-haar: precision must be c64 or c128")
+    ent, _ = engine.mipt_haar(engine.default_context(), n, depth, p, trajectories, seed, precision)
+    mean = 0.0
+    with open(os.path.join(out, base + ".csv"), "w") as f:
+        f.write("L,p,trajectory,entropy_bits\n")
+        for tr in range(trajectories):
+            f.write(f"{n},{_fmt(p)},{tr},{_fmt(ent[tr])}\n")
+            mean += float(ent[tr])
+    return {"mean_entropy": {str(n): mean / trajectories}, "p": p, "trajectories": trajectories, "N": n, "D": depth}
+
+
 def run_experiment(name, cfg, out_dir, seed, workers):  # experiments.cpp:434-467
     if not isinstance(cfg, dict):
         raise ConfigError("config must be a JSON object")
@@ -125,7 +151,7 @@ def run_experiment(name, cfg, out_dir, seed, workers):  # experiments.cpp:434-46
     os.makedirs(out_dir, exist_ok=True)
     base = name + "_" + config_digest(name, cfg, seed)
     t0 = time.monotonic()
-    extra = exp_vqe_tfim(cfg, out_dir, base, seed, workers)
+    extra = (exp_vqe_tfim if name == "vqe-tfim" else exp_mipt_haar)(cfg, out_dir, base, seed, workers)
     wall = time.monotonic() - t0
     meta = {"experiment": name, "seed": seed, "config": cfg, "workers": workers, "wall_time_s": wall,
             "data": base + ".csv"}
