@@ -200,6 +200,15 @@ int qf_sparse_energy(qf_ctx* ctx, const qf_program* prog, int batch, const doubl
 int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint64_t seed, int precision,
                  double* entropies, long long* n_measurements);
 
+/* Classical-shadow snapshots (reference shadows.cpp:50-85): the state of `prep`
+ * (at theta) rotated, per snapshot r, into bases[r][0..n) (1 = X, 2 = Y, 3 = Z;
+ * basis_rotation, shadows.cpp:33-44) and sampled once by inverse CDF with u[r]
+ * (the reference draws u[r] = rng.split(m)[r].uniform()); outcomes[r][q] =
+ * bit of qubit q (0 = most significant).  Snapshots run as one batched sweep
+ * pass with per-snapshot matrices plus a chunked sampling pass. */
+int qf_shadow_snapshots(qf_ctx* ctx, const qf_program* prep, const double* theta, int m, const int8_t* bases,
+                        const double* u, int8_t* outcomes);
+
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
  * float64 device pointers.  Single-GPU semantics (no collective). */

@@ -345,3 +345,40 @@ def mipt_haar(n: int, depth: int, p: float, trajectories: int, seed: int):
                     psi = measure_collapse(psi, n, q, rs.uniform())
         ents.append(subsystem_entropy_half(psi, n))
     return np.array(ents)
+
+
+# classical shadows (reference proj/src/shadows.cpp:24-85, experiments.cpp:252-274)
+_S = np.sqrt(0.5)
+BASIS_ROTATION = {1: np.array([[_S, _S], [_S, -_S]], complex), 2: np.array([[_S, -1j * _S], [_S, 1j * _S]]),
+                  3: np.eye(2, dtype=complex)}
+
+
+def shadow_snapshots(psi: np.ndarray, n: int, bases, us) -> np.ndarray:
+    """shadow_snapshots with the per-snapshot uniforms already drawn: rotate, then
+    the first index whose running sum of |a_i|^2 exceeds u (last index if none)."""
+    out = np.zeros((len(bases), n), np.int8)
+    for r, (row, u) in enumerate(zip(bases, us)):
+        t = psi.reshape([2] * n)
+        for q, code in enumerate(row):
+            if code != 3:
+                t = np.moveaxis(np.tensordot(BASIS_ROTATION[int(code)], t, axes=([1], [q])), 0, q)
+        acc = np.cumsum(np.abs(t.reshape(-1)) ** 2)
+        idx = int(np.searchsorted(acc, u, side="right"))
+        idx = min(idx, (1 << n) - 1)
+        out[r] = [(idx >> (n - 1 - q)) & 1 for q in range(n)]
+    return out
+
+
+def shadow_gen_inputs(n: int, m: int, depth: int, seed: int):
+    """exp_shadow_gen randomness: ry angles (streams[0]), bases (streams[1]),
+    per-snapshot uniforms (streams[2].split(m)); returns (ops, bases, us)."""
+    streams = Rng(seed).split(3)
+    ops = []
+    for _ in range(depth):
+        for q in range(n):
+            ops.append((GID["ry"], q, -1, -1, 1.0, 2.0 * 3.14159265358979323846 * streams[0].uniform(), -1))
+        for q in range(n - 1):
+            ops.append((GID["cx"], q, q + 1, -1, 1.0, 0.0, -1))
+    bases = [[1 + streams[1].uniform_below(3) for _ in range(n)] for _ in range(m)]
+    us = [s.uniform() for s in streams[2].split(m)]
+    return ops, np.array(bases, np.int8), np.array(us)

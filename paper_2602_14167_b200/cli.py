@@ -1,7 +1,7 @@
 """`qforge`-compatible command line for the GPU-backed experiments on the hot
-path: vqe-tfim and mipt-haar (8f row 4).
+path: vqe-tfim, mipt-haar and shadow-gen (8f row 4).
 
-    python -m paper_2602_14167_b200.cli {vqe-tfim,mipt-haar} [--config F] [--seed S] [--workers W]
+    python -m paper_2602_14167_b200.cli {vqe-tfim,mipt-haar,shadow-gen} [--config F] [--seed S] [--workers W]
                                                   [--out DIR] [--set key=value ...]
     python -m paper_2602_14167_b200.cli emit-summary DIR
 
@@ -21,7 +21,7 @@ import os
 import sys
 import time
 
-EXPERIMENTS = ["vqe-tfim", "mipt-haar"]
+EXPERIMENTS = ["vqe-tfim", "mipt-haar", "shadow-gen"]
 
 
 class ConfigError(Exception):
@@ -143,6 +143,40 @@ def exp_mipt_haar(cfg, out, base, seed, workers):  # experiments.cpp:210-250
     return {"mean_entropy": {str(n): mean / trajectories}, "p": p, "trajectories": trajectories, "N": n, "D": depth}
 
 
+def exp_shadow_gen(cfg, out, base, seed, workers):  # experiments.cpp:252-274
+    from . import engine
+    from .rng import RngStream
+
+    n = _get(cfg, "n", 20, int)
+    m = _get(cfg, "M", 256, int)
+    depth = _get(cfg, "depth", 0, int)
+    precision = _get(cfg, "precision", "c128", str)
+    if n < 1 or n > 24:
+        raise ConfigError("shadow-gen: n must lie in [1, 24]")
+    if m < 1:
+        raise ConfigError("shadow-gen: M must be >= 1")
+    if precision not in ("c64", "c128"):
+        raise ConfigError("shadow-gen: precision must be c64 or c128")
+    streams = RngStream(seed).split(3)
+    ops = []
+    for _ in range(depth):
+        for q in range(n):
+            ops.append(("ry", q, -1, -1, 1.0, 2.0 * 3.14159265358979323846 * streams[0].uniform(), -1))
+        for q in range(n - 1):
+            ops.append(("cx", q, q + 1, -1, 1.0, 0.0, -1))
+    bases = [[1 + streams[1].uniform_below(3) for _ in range(n)] for _ in range(m)]  # random_bases, shadows.cpp:24-29
+    us = [s.uniform() for s in streams[2].split(m)]
+    ctx = engine.default_context()
+    prep = engine.Program(ctx, n, ops, 0, precision)
+    outcomes = engine.shadow_snapshots(ctx, prep, None, bases, us)
+    name = base + ".dataset.csv"
+    with open(os.path.join(out, name), "w") as f:  # save_dataset, shadows.cpp:124-136
+        f.write(f"{n},{m}\n")
+        for r in range(m):
+            f.write("".join(str(c) for c in bases[r]) + ";" + "".join(str(int(b)) for b in outcomes[r]) + "\n")
+    return {"n": n, "M": m, "depth": depth, "dataset": name}
+
+
 def run_experiment(name, cfg, out_dir, seed, workers):  # experiments.cpp:434-467
     if not isinstance(cfg, dict):
         raise ConfigError("config must be a JSON object")
@@ -151,7 +185,8 @@ def run_experiment(name, cfg, out_dir, seed, workers):  # experiments.cpp:434-46
     os.makedirs(out_dir, exist_ok=True)
     base = name + "_" + config_digest(name, cfg, seed)
     t0 = time.monotonic()
-    extra = (exp_vqe_tfim if name == "vqe-tfim" else exp_mipt_haar)(cfg, out_dir, base, seed, workers)
+    extra = {"vqe-tfim": exp_vqe_tfim, "mipt-haar": exp_mipt_haar, "shadow-gen": exp_shadow_gen}[name](
+        cfg, out_dir, base, seed, workers)
     wall = time.monotonic() - t0
     meta = {"experiment": name, "seed": seed, "config": cfg, "workers": workers, "wall_time_s": wall,
             "data": base + ".csv"}

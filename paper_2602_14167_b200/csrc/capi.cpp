@@ -191,6 +191,7 @@ struct qf_ctx {
     DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init, gmat;
     DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_nodes, coo_rows, coo_cols, coo_vals;
     uint64_t coo_uid = 0;  // observable whose groups/terms/offsets coo_* currently hold (0: none)
+    std::map<std::pair<int, int>, qf_program*> basis_progs;  // (n, precision) -> per-qubit basis rotation program
     int coo_n_groups = 0, coo_n_events = 0, coo_n_terms = 0;
     int64_t coo_total = 0;
     HostBuf pin;
@@ -674,6 +675,7 @@ int qf_ctx_destroy(qf_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.commDestroy(c->comm);
+    for (auto& kv : c->basis_progs) qf_program_destroy(kv.second);
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
                       &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_nodes, &c->coo_rows,
                       &c->coo_cols, &c->coo_vals})
@@ -1627,6 +1629,121 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
         }
     }
     if (tm) fprintf(stderr, "qf_mipt_haar: host randomness %.3f s, circuits %.3f s, entropy %.3f s\n", t_gen, t_circ, t_ent);
+    return QF_OK;
+}
+
+int qf_shadow_snapshots(qf_ctx* ctx, const qf_program* cprep, const double* theta, int m, const int8_t* bases,
+                        const double* u, int8_t* outcomes) {
+    // reference shadows.cpp:50-85 (shadow_snapshots): per snapshot r, the prepared state
+    // rotated into bases[r] (basis_rotation :33-44; 1 = X, 2 = Y, 3 = Z) and one sample
+    // by inverse CDF with the uniform u[r] (= rng.split(m)[r].uniform() in the reference)
+    qf_program* prep = const_cast<qf_program*>(cprep);
+    if (!ctx || !prep || m < 0 || (m > 0 && (!bases || !u || !outcomes)) || (!theta && prep->plan.n_params))
+        return set_err(QF_EINVAL, "qf_shadow_snapshots: bad arguments");
+    const int n = prep->plan.n, prec = prep->plan.prec;
+    for (size_t i = 0; i < (size_t)m * n; ++i)
+        if (bases[i] < 1 || bases[i] > 3) return set_err(QF_EINVAL, "shadow_snapshots: bad basis code");
+    if (m == 0) return QF_OK;
+    int rc = check_thetas(prep, 1, theta);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    rc = stage_thetas(ctx, prep, 1, theta);
+    if (rc) return rc;
+    rc = forward_one(ctx, prep, (const double*)ctx->thetas.p);  // psi -> ctx->psi (global sign irrelevant)
+    if (rc) return rc;
+    // per-qubit basis program (dense single-qubit gates, matrices per snapshot)
+    qf_program*& bp = ctx->basis_progs[{n, prec}];
+    if (!bp) {
+        std::vector<qf_op> ops(n);
+        std::vector<double> ms;
+        const double h = std::sqrt(0.5);
+        for (int q = 0; q < n; ++q) {
+            ops[q] = qf_op{};
+            ops[q].kind = QF_UNITARY;
+            ops[q].q0 = q;
+            ops[q].q1 = -1;
+            ops[q].slot = -1;
+            ops[q].coef = 1.0;
+            ops[q].mat = q;
+            const double hx[8] = {h, 0, h, 0, h, 0, -h, 0};  // placeholder; replaced per snapshot
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) {
+                    ms.push_back(r < 2 && c < 2 ? hx[(r * 2 + c) * 2] : 0.0);
+                    ms.push_back(r < 2 && c < 2 ? hx[(r * 2 + c) * 2 + 1] : 0.0);
+                }
+        }
+        rc = qf_program_create(ctx, n, n, ops.data(), ms.data(), n, 0, prec, &bp);
+        if (rc) {
+            bp = nullptr;
+            return rc;
+        }
+    }
+    const ProgramPlan& P = bp->plan;
+    const size_t N = size_t(1) << n, vs = vsize(prec);
+    size_t fr = 0, tot = 0;
+    QF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t budget = (size_t)(0.5 * (double)(fr + ctx->lam.cap));
+    const int cb = sample_chunk_bits(n);
+    const size_t nc = N >> cb;
+    const size_t per_state = N * vs + (size_t)n * 32 * 8 + nc * 8 + 64;
+    int bc = (int)std::max<size_t>(1, std::min<size_t>(budget / per_state, (size_t)m));
+    bc = std::min(bc, 65535);
+    QF_CUDA(ctx->lam.reserve((size_t)bc * N * vs));
+    QF_CUDA(ctx->gmat.reserve(std::max<size_t>(16, (size_t)bc * P.fwd.total_mat * vs)));
+    LocalBuf d_cm, d_u, d_csum, d_hit;
+    QF_CUDA(d_cm.reserve((size_t)bc * n * 32 * 8));
+    QF_CUDA(d_u.reserve((size_t)bc * 8));
+    QF_CUDA(d_csum.reserve((size_t)bc * nc * 8));
+    QF_CUDA(d_hit.reserve((size_t)bc * 8));
+    const double h = std::sqrt(0.5);
+    // basis_rotation: X -> [[s, s], [s, -s]], Y -> [[s, -i s], [s, i s]], Z -> identity
+    const double rot[4][8] = {{0}, {h, 0, h, 0, h, 0, -h, 0}, {h, 0, 0, -h, h, 0, 0, h}, {1, 0, 0, 0, 0, 0, 1, 0}};
+    std::vector<double> cm((size_t)bc * n * 32);
+    std::vector<int64_t> hits(bc);
+    for (int r0 = 0; r0 < m; r0 += bc) {
+        const int nb = std::min(bc, m - r0);
+        std::fill(cm.begin(), cm.end(), 0.0);
+        for (int b = 0; b < nb; ++b)
+            for (int q = 0; q < n; ++q) {
+                const double* R = rot[bases[(size_t)(r0 + b) * n + q]];
+                double* dst = cm.data() + ((size_t)b * n + q) * 32;
+                for (int rr = 0; rr < 2; ++rr)
+                    for (int c = 0; c < 2; ++c) {
+                        dst[(rr * 4 + c) * 2] = R[(rr * 2 + c) * 2];
+                        dst[(rr * 4 + c) * 2 + 1] = R[(rr * 2 + c) * 2 + 1];
+                    }
+            }
+        QF_CUDA(cudaMemcpyAsync(d_cm.p, cm.data(), (size_t)nb * n * 32 * 8, cudaMemcpyHostToDevice, s));
+        QF_CUDA(cudaMemcpyAsync(d_u.p, u + r0, (size_t)nb * 8, cudaMemcpyHostToDevice, s));
+        QF_CUDA(launch_init_state(prec, ctx->lam.p, ctx->psi.p, n, nb, s));  // nb copies of psi
+        SweepArgs sa{};
+        sa.psi = ctx->lam.p;
+        sa.n = n;
+        sa.gates = (const DevGate*)bp->gates.p;
+        sa.cmats = (const double*)d_cm.p;
+        sa.gmat = ctx->gmat.p;
+        sa.gmat_stride = P.fwd.total_mat;
+        QF_CUDA(launch_mats(prec, false, (const DevOp*)bp->fwd.ops.p, (const int*)bp->goff_fwd.p, (int)P.fwd.ops.size(),
+                            sa.gates, sa.cmats, nullptr, 0, 0, ctx->gmat.p, sa.gmat_stride, 0, nb, s,
+                            (size_t)n * 32));
+        sa.phases = (const DevPhase*)bp->fwd.phases.p;
+        sa.ops = (const DevOp*)bp->fwd.ops.p;
+        for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
+            sa.sw = P.fwd.sweeps[i];
+            if (bp->use_jit)
+                QF_CUDA((cudaError_t)jit_launch(bp->jf.sweeps[i], sa, 1 << (n - sa.sw.k), nb, s));
+            else
+                QF_CUDA(launch_sweep(prec, false, sa, nb, P.fwd.max_mat, 0, s));
+            ctx->launches++;
+        }
+        QF_CUDA(launch_sample(prec, ctx->lam.p, n, nb, (const double*)d_u.p, (double*)d_csum.p, (int64_t*)d_hit.p, s));
+        QF_CUDA(cudaMemcpyAsync(hits.data(), d_hit.p, (size_t)nb * 8, cudaMemcpyDeviceToHost, s));
+        QF_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < nb; ++b)
+            for (int q = 0; q < n; ++q)
+                outcomes[(size_t)(r0 + b) * n + q] = (int8_t)((hits[b] >> (n - 1 - q)) & 1);
+    }
     return QF_OK;
 }
 

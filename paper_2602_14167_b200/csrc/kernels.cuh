@@ -88,6 +88,10 @@ cudaError_t launch_meas_decide(const MeasRound* rounds, const double* hist, int 
                                double* scale, int* outcomes, cudaStream_t s);
 cudaError_t launch_meas_project(int prec, void* psi, int n, int batch, const MeasRound* rounds, const uint32_t* mask,
                                 const uint32_t* bits, const double* scale, cudaStream_t s);
+// one inverse-CDF sample per state (u[b] in [0, 1)); csum: [batch][2^(n - sample_chunk_bits(n))]
+int sample_chunk_bits(int n);
+cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const double* u, double* csum, int64_t* hit,
+                          cudaStream_t s);
 cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);
 
 // rows / cols ascending per row, complex128 values

@@ -125,7 +125,73 @@ __global__ void set_basis0_kernel(V* psi, int n, int batch) {
     }
 }
 
+// inverse-CDF sampling (shadow_snapshots, shadows.cpp:64-78): chunk sums of |psi|^2
+// in fixed order, then one thread per state walks the chunk sums and the hit
+// chunk's amplitudes with a running sum as the reference does (acc += |a_i|^2,
+// first i with u < acc; the last index when none)
+template <typename V>
+__global__ void __launch_bounds__(256) chunk_norms_kernel(const V* psi, int n, int chunk_bits, double* csum) {
+    __shared__ double red[8];
+    const int b = blockIdx.y;
+    const size_t N = size_t(1) << n, C = size_t(1) << chunk_bits;
+    const V* ps = psi + (size_t)b * N + (size_t)blockIdx.x * C;
+    double acc = 0.0;
+    for (size_t i = threadIdx.x; i < C; i += blockDim.x) {
+        const V a = ps[i];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        csum[(size_t)b * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+template <typename V>
+__global__ void sample_pick_kernel(const V* psi, int n, int chunk_bits, const double* csum, const double* u, int batch,
+                                   int64_t* hit) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const size_t N = size_t(1) << n, C = size_t(1) << chunk_bits, nc = N / C;
+    const V* ps = psi + (size_t)b * N;
+    const double* cs = csum + (size_t)b * nc;
+    const double ub = u[b];
+    double acc = 0.0;
+    size_t c = 0;
+    while (c < nc && !(ub < acc + cs[c])) acc += cs[c++];
+    int64_t h = (int64_t)N - 1;
+    for (size_t i = c * C; i < N; ++i) {
+        const V a = ps[i];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+        if (ub < acc) {
+            h = (int64_t)i;
+            break;
+        }
+    }
+    hit[b] = h;
+}
+
 }  // namespace
+
+int sample_chunk_bits(int n) { return n > 10 ? 10 : n; }
+
+cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const double* u, double* csum, int64_t* hit,
+                          cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    const int cb = sample_chunk_bits(n);
+    dim3 grid(1u << (n - cb), batch);
+    if (prec == 1) {
+        chunk_norms_kernel<double2><<<grid, 256, 0, s>>>((const double2*)psi, n, cb, csum);
+        sample_pick_kernel<double2><<<(batch + 127) / 128, 128, 0, s>>>((const double2*)psi, n, cb, csum, u, batch, hit);
+    } else {
+        chunk_norms_kernel<float2><<<grid, 256, 0, s>>>((const float2*)psi, n, cb, csum);
+        sample_pick_kernel<float2><<<(batch + 127) / 128, 128, 0, s>>>((const float2*)psi, n, cb, csum, u, batch, hit);
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_meas_hist(int prec, const void* psi, int n, int batch, const MeasRound* rounds, int max_count,
                              double* hist, cudaStream_t s) {

@@ -333,6 +333,21 @@ def mipt_haar(ctx: Context, n: int, depth: int, p: float, trajectories: int, see
     return out, int(cnt.value)
 
 
+def shadow_snapshots(ctx: Context, prep: Program, theta, bases, u) -> np.ndarray:
+    """Classical-shadow outcomes (qf_shadow_snapshots, shadows.cpp:50-85):
+    bases [m, n] codes 1/2/3, u [m] uniforms -> outcomes [m, n] bits (int8)."""
+    th = np.ascontiguousarray(np.asarray(theta if theta is not None else np.zeros(0), dtype=np.float64).reshape(-1))
+    bases = np.ascontiguousarray(np.asarray(bases, dtype=np.int8).reshape(-1, prep.n))
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64).reshape(-1))
+    m = bases.shape[0]
+    if u.size != m:
+        raise ValueError("shadow_snapshots: one uniform per snapshot")
+    out = np.zeros((m, prep.n), dtype=np.int8)
+    check(ctx.lib.qf_shadow_snapshots(ctx.handle, prep.handle, dptr(th), m, ctypes.c_void_p(bases.ctypes.data), dptr(u),
+                                      ctypes.c_void_p(out.ctypes.data)))
+    return out
+
+
 def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
                      eps=1e-8) -> None:
     B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))

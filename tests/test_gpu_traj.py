@@ -40,3 +40,32 @@ def test_mipt_haar_precisions_agree_at_size(ctx):
     a, na = engine.mipt_haar(ctx, 16, 12, 0.1, 4, 31, "c64")
     b, nb_ = engine.mipt_haar(ctx, 16, 12, 0.1, 4, 31, "c128")
     assert na == nb_ and np.abs(a - b).max() < 1e-4, (a, b)
+
+
+@pytest.mark.parametrize("n,m,depth", [(1, 20, 0), (5, 64, 2), (8, 100, 3), (11, 40, 2)])
+def test_shadow_snapshots_match_oracle(ctx, n, m, depth):
+    """shadow_snapshots (shadows.cpp:50-85) with the shadow-gen randomness
+    (experiments.cpp:252-274): identical outcome bits (complex128)."""
+    ops, bases, us = po.shadow_gen_inputs(n, m, depth, 77 + n)
+    psi = po.run(n, ops)
+    ref = po.shadow_snapshots(psi, n, bases, us)
+    prep = engine.Program(ctx, n, ops, 0, "c128")
+    got = engine.shadow_snapshots(ctx, prep, None, bases, us)
+    assert np.array_equal(got, ref)
+    with pytest.raises(ValueError, match="bad basis code"):
+        engine.shadow_snapshots(ctx, prep, None, np.zeros((2, n), np.int8), us[:2])
+
+
+def test_shadow_gen_cli_dataset(ctx, tmp_path):
+    from paper_2602_14167_b200 import cli
+    args = ["shadow-gen", "--seed", "5", "--set", "n=6", "--set", "M=30", "--set", "depth=2"]
+    assert cli.main(args + ["--out", str(tmp_path)]) == 0
+    ds = [f for f in tmp_path.iterdir() if f.name.endswith(".dataset.csv")][0]
+    lines = ds.read_text().splitlines()
+    assert lines[0] == "6,30" and len(lines) == 31
+    ops, bases, us = po.shadow_gen_inputs(6, 30, 2, 5)
+    ref = po.shadow_snapshots(po.run(6, ops), 6, bases, us)
+    for r, line in enumerate(lines[1:]):
+        b, o = line.split(";")
+        assert b == "".join(str(c) for c in bases[r]) and o == "".join(str(x) for x in ref[r])
+    assert cli.main(["shadow-gen", "--out", str(tmp_path), "--set", "n=25"]) == 2
