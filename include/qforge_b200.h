@@ -209,6 +209,22 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
 int qf_shadow_snapshots(qf_ctx* ctx, const qf_program* prep, const double* theta, int m, const int8_t* bases,
                         const double* u, int8_t* outcomes);
 
+/* Monte-Carlo noise trajectories (reference noise.cpp:162-197, mc_trajectory),
+ * batched: `trajectories` runs of one constant circuit (ops with slot = -1;
+ * angles in offset) from |0..0> or `init`.  After op j the channels
+ * op_chan[op_chan_ptr[j] .. op_chan_ptr[j+1]) fire in order; channel c's Kraus
+ * operators are kraus[chan_kraus_ptr[c] .. chan_kraus_ptr[c+1]) (each 4x4x2
+ * doubles, top-left D x D used, D = 2^wires of op j).  Trajectory t consumes the
+ * uniforms u[t][0 .. n_apps), n_apps = op_chan_ptr[n_ops], one per application:
+ * branch k is picked by u * sum_k p_k against the running sum of
+ * p_k = ||K_k psi||^2, psi <- K psi / sqrt(p), log_prob += log(p/acc) + log(acc).
+ * Outputs (each optional): states [t][2^n][2], log_probs [t], and with obs the
+ * energies Re<psi_t|H|psi_t> in expvals [t]. */
+int qf_noise_trajectories(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, const double* mats, int n_mats,
+                          const int* op_chan_ptr, const int* op_chan, const int* chan_kraus_ptr, const double* kraus,
+                          const double* init, int trajectories, const double* u, int precision, double* states,
+                          double* log_probs, qf_observable* obs, double* expvals);
+
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
  * float64 device pointers.  Single-GPU semantics (no collective). */

@@ -382,3 +382,72 @@ def shadow_gen_inputs(n: int, m: int, depth: int, seed: int):
     bases = [[1 + streams[1].uniform_below(3) for _ in range(n)] for _ in range(m)]
     us = [s.uniform() for s in streams[2].split(m)]
     return ops, np.array(bases, np.int8), np.array(us)
+
+
+# noise trajectories (reference proj/src/noise.cpp:162-197)
+def _gate_matrix_np(kind, offset):
+    """circuit.cpp:202-302 for the constant gates used by the noise tests."""
+    g = GATES[kind]
+    c, s = np.cos(offset / 2), np.sin(offset / 2)
+    h = np.sqrt(0.5)
+    table = {
+        "h": np.array([[h, h], [h, -h]], complex), "x": np.array([[0, 1], [1, 0]], complex),
+        "y": np.array([[0, -1j], [1j, 0]]), "z": np.diag([1.0 + 0j, -1]), "s": np.diag([1.0 + 0j, 1j]),
+        "rx": np.array([[c, -1j * s], [-1j * s, c]]), "ry": np.array([[c, -s], [s, c]], complex),
+        "rz": np.diag([np.exp(-0.5j * offset), np.exp(0.5j * offset)]),
+        "rzz": np.diag([np.exp(-0.5j * offset), np.exp(0.5j * offset), np.exp(0.5j * offset), np.exp(-0.5j * offset)]),
+        "cx": np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], complex),
+        "cz": np.diag([1.0 + 0j, 1, 1, -1]),
+    }
+    return table[g]
+
+
+def _apply_np(psi, n, m, wires):
+    if len(wires) == 1:
+        t = np.moveaxis(np.tensordot(m, psi.reshape([2] * n), axes=([1], [wires[0]])), 0, wires[0])
+        return t.reshape(-1)
+    return apply_2q(psi, n, m, wires[0], wires[1])
+
+
+def mc_trajectory(n, ops, op_channels, channels, u_row):
+    """One trajectory with its uniforms already drawn: (state, log_prob)."""
+    psi = np.zeros(1 << n, complex)
+    psi[0] = 1.0
+    logp, app = 0.0, 0
+    for j, op in enumerate(ops):
+        kind, q0, q1 = op[0], op[1], op[2]
+        wires = [q0] if q1 < 0 else [q0, q1]
+        psi = _apply_np(psi, n, _gate_matrix_np(kind, op[5]), wires)
+        for ch in op_channels[j]:
+            branches = [_apply_np(psi, n, np.asarray(k, complex), wires) for k in channels[ch]]
+            probs = [float(np.sum(np.abs(b) ** 2)) for b in branches]
+            acc = sum(probs)
+            uu = u_row[app] * acc
+            app += 1
+            pick, run = len(probs) - 1, 0.0
+            for i, p in enumerate(probs):
+                run += p
+                if uu < run:
+                    pick = i
+                    break
+            psi = branches[pick] / np.sqrt(probs[pick])
+            logp += np.log(probs[pick] / acc) + np.log(acc)
+    return psi, logp
+
+
+def density_matrix_expect_z0(n, ops, op_channels, channels):
+    """Exact <Z_0> of the channel-averaged state (density_matrix_run, noise.cpp:199-240)."""
+    rho = np.zeros((1 << n, 1 << n), complex)
+    rho[0, 0] = 1.0
+    for j, op in enumerate(ops):
+        wires = [op[1]] if op[2] < 0 else [op[1], op[2]]
+
+        def conj(r, m):
+            cols = np.stack([_apply_np(r[:, c], n, m, wires) for c in range(1 << n)], axis=1)
+            rows = np.stack([_apply_np(cols[i, :].conj(), n, m, wires).conj() for i in range(1 << n)], axis=0)
+            return rows
+        rho = conj(rho, _gate_matrix_np(op[0], op[5]))
+        for ch in op_channels[j]:
+            rho = sum(conj(rho, np.asarray(k, complex)) for k in channels[ch])
+    z0 = np.array([1.0 if ((i >> (n - 1)) & 1) == 0 else -1.0 for i in range(1 << n)])
+    return float(np.real(np.sum(np.diag(rho) * z0)))

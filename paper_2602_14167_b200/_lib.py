@@ -64,6 +64,9 @@ SIGNATURES = {
     "qf_mipt_haar": (_I, [ctypes.c_void_p, _I, _I, ctypes.c_double, _I, ctypes.c_uint64, _I, _D,
                          ctypes.POINTER(ctypes.c_longlong)]),
     "qf_shadow_snapshots": (_I, [ctypes.c_void_p, ctypes.c_void_p, _D, _I, ctypes.c_void_p, _D, ctypes.c_void_p]),
+    "qf_noise_trajectories": (_I, [ctypes.c_void_p, _I, _I, ctypes.POINTER(QfOp), _D, _I, ctypes.POINTER(_I),
+                                  ctypes.POINTER(_I), ctypes.POINTER(_I), _D, _D, _I, _D, _I, _D, _D, ctypes.c_void_p,
+                                  _D]),
     "qf_jit_hpsi_check": (_I, [_I, _I, ctypes.c_void_p, _D, _D, _I, ctypes.POINTER(_I)]),
     "qf_pauli_sum_to_coo": (_I, [_P, _P, _I, _I, _P, _P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "qf_ctx_set_timing": (_I, [_P, _I]),

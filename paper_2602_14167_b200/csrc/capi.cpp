@@ -554,6 +554,42 @@ void haar_su4(qforge::RngStream& rng, cd q[4][4]) {
         for (int c = 0; c < 4; ++c) q[r][c] *= ph;
 }
 
+// gate_matrix (reference circuit.cpp:202-302) on the host for the noise
+// trajectories: D x D row-major (wires[0] most significant), angle = op.offset
+int host_gate_matrix(const qf_op& o, const double* mats, int n_mats, int& D, cd m[16]) {
+    for (int i = 0; i < 16; ++i) m[i] = 0.0;
+    const double t = o.offset, c = std::cos(0.5 * t), sn = std::sin(0.5 * t), h = std::sqrt(0.5);
+    const cd I(0.0, 1.0);
+    D = 2;
+    switch (o.kind) {
+        case QF_H: m[0] = h; m[1] = h; m[2] = h; m[3] = -h; break;
+        case QF_X: m[1] = 1; m[2] = 1; break;
+        case QF_Y: m[1] = -I; m[2] = I; break;
+        case QF_Z: m[0] = 1; m[3] = -1; break;
+        case QF_S: m[0] = 1; m[3] = I; break;
+        case QF_RX: m[0] = c; m[1] = -I * sn; m[2] = -I * sn; m[3] = c; break;
+        case QF_RY: m[0] = c; m[1] = -sn; m[2] = sn; m[3] = c; break;
+        case QF_RZ: m[0] = std::polar(1.0, -0.5 * t); m[3] = std::polar(1.0, 0.5 * t); break;
+        case QF_RZZ:
+            D = 4;
+            m[0] = m[15] = std::polar(1.0, -0.5 * t);
+            m[5] = m[10] = std::polar(1.0, 0.5 * t);
+            break;
+        case QF_CX: D = 4; m[0] = m[5] = m[11] = m[14] = 1; break;
+        case QF_CZ: D = 4; m[0] = m[5] = m[10] = 1; m[15] = -1; break;
+        case QF_SU4: case QF_UNITARY: {
+            if (o.mat < 0 || o.mat >= n_mats || !mats) return set_err(QF_EINVAL, "program: missing gate matrix");
+            D = o.q1 >= 0 ? 4 : 2;
+            const double* src = mats + 32 * (size_t)o.mat;
+            for (int r = 0; r < D; ++r)
+                for (int cc = 0; cc < D; ++cc) m[r * D + cc] = cd(src[(r * 4 + cc) * 2], src[(r * 4 + cc) * 2 + 1]);
+            break;
+        }
+        default: return set_err(QF_EINVAL, "gate_matrix: qudit gates are not supported on the qubit device path");
+    }
+    return QF_OK;
+}
+
 // cuBLAS / cuSOLVER, loaded at run time (only the trajectory entropy needs them)
 struct LinAlg {
     void *hb = nullptr, *hs = nullptr;
@@ -1743,6 +1779,174 @@ int qf_shadow_snapshots(qf_ctx* ctx, const qf_program* cprep, const double* thet
         for (int b = 0; b < nb; ++b)
             for (int q = 0; q < n; ++q)
                 outcomes[(size_t)(r0 + b) * n + q] = (int8_t)((hits[b] >> (n - 1 - q)) & 1);
+    }
+    return QF_OK;
+}
+
+int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const double* mats, int n_mats,
+                          const int* op_chan_ptr, const int* op_chan, const int* chan_kraus_ptr, const double* kraus,
+                          const double* init, int trajectories, const double* u, int precision, double* states,
+                          double* log_probs, qf_observable* obs, double* expvals) {
+    // reference noise.cpp:162-197 (mc_trajectory), batched: trajectory t uses the uniforms
+    // u[t][0 .. n_apps) in channel-application order (the reference draws one per application)
+    if (!ctx || n < 1 || n > 30 || n_ops < 0 || (n_ops > 0 && (!ops || !op_chan_ptr)) || trajectories < 0 ||
+        (precision != QF_C64 && precision != QF_C128) || (obs && !expvals) || (obs && obs->n != n))
+        return set_err(QF_EINVAL, "qf_noise_trajectories: bad arguments");
+    const int n_apps = n_ops ? op_chan_ptr[n_ops] : 0;
+    if (n_apps > 0 && (!op_chan || !chan_kraus_ptr || !kraus || (trajectories > 0 && !u)))
+        return set_err(QF_EINVAL, "qf_noise_trajectories: missing channel data");
+    if (trajectories == 0) return QF_OK;
+    std::vector<int> Dg(n_ops), P0(n_ops), P1(n_ops);
+    std::vector<double2> gm((size_t)std::max(n_ops, 1) * 16);
+    for (int j = 0; j < n_ops; ++j) {
+        const qf_op& o = ops[j];
+        const bool two = o.kind == QF_RZZ || o.kind == QF_CX || o.kind == QF_CZ || o.kind == QF_SU4 ||
+                         (o.kind == QF_UNITARY && o.q1 >= 0);
+        if (o.slot >= 0) return set_err(QF_EINVAL, "qf_noise_trajectories: constant circuits only (slot = -1)");
+        if (o.q0 < 0 || o.q0 >= n || (two && (o.q1 < 0 || o.q1 >= n || o.q1 == o.q0)))
+            return set_err(QF_EINVAL, "Circuit: wire out of range");
+        cd m[16];
+        int rc = host_gate_matrix(o, mats, n_mats, Dg[j], m);
+        if (rc) return rc;
+        P0[j] = n - 1 - o.q0;
+        P1[j] = Dg[j] == 4 ? n - 1 - o.q1 : -1;
+        for (int i = 0; i < 16; ++i) gm[(size_t)j * 16 + i] = make_double2(m[i].real(), m[i].imag());
+    }
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const size_t N = size_t(1) << n, vs = vsize(precision);
+    size_t fr = 0, tot = 0;
+    QF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t budget = (size_t)(0.5 * (double)(fr + ctx->lam.cap));
+    int bc = (int)std::max<size_t>(1, std::min<size_t>(budget / (N * vs + 1024), (size_t)trajectories));
+    bc = std::min(bc, 65535);
+    QF_CUDA(ctx->lam.reserve((size_t)bc * N * vs));
+    LocalBuf d_gm, d_rho, d_k, d_init, d_part, d_E;
+    QF_CUDA(d_gm.reserve(gm.size() * 16));
+    QF_CUDA(cudaMemcpyAsync(d_gm.p, gm.data(), gm.size() * 16, cudaMemcpyHostToDevice, s));
+    QF_CUDA(d_rho.reserve((size_t)bc * 16 * 16));
+    QF_CUDA(d_k.reserve((size_t)bc * 16 * 16));
+    if (init) {
+        QF_CUDA(d_init.reserve(N * vs));
+        if (precision == QF_C128) {
+            QF_CUDA(cudaMemcpyAsync(d_init.p, init, N * 16, cudaMemcpyHostToDevice, s));
+        } else {
+            std::vector<float> f(2 * N);
+            for (size_t i = 0; i < 2 * N; ++i) f[i] = (float)init[i];
+            QF_CUDA(cudaMemcpyAsync(d_init.p, f.data(), N * 8, cudaMemcpyHostToDevice, s));
+            QF_CUDA(cudaStreamSynchronize(s));
+        }
+    }
+    ObsDev* od = nullptr;
+    int tiles_h = 0;
+    if (obs) {
+        const Geometry geo = geometry(precision, n);
+        od = &obs->dev[precision];
+        int rc = ensure_obs_dev(obs, precision, geo.kh, *od, 0, (int)obs->w_re.size());
+        if (rc) return rc;
+        tiles_h = 1 << (n - geo.kh);
+        QF_CUDA(d_part.reserve((size_t)bc * tiles_h * 8));
+        QF_CUDA(d_E.reserve((size_t)bc * 8));
+    }
+    std::vector<double2> rho((size_t)bc * 16), km((size_t)bc * 16);
+    std::vector<double> logp(bc);
+    std::vector<float> fbuf;
+    for (int t0 = 0; t0 < trajectories; t0 += bc) {
+        const int nb = std::min(bc, trajectories - t0);
+        if (init)
+            QF_CUDA(launch_init_state(precision, ctx->lam.p, d_init.p, n, nb, s));
+        else
+            QF_CUDA(launch_set_basis0(precision, ctx->lam.p, n, nb, s));
+        std::fill(logp.begin(), logp.end(), 0.0);
+        int app = 0;
+        for (int j = 0; j < n_ops; ++j) {
+            const int D = Dg[j];
+            QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_gm.p + (size_t)j * 16,
+                                       false, s));
+            ctx->launches++;
+            for (int ci = op_chan_ptr[j]; ci < op_chan_ptr[j + 1]; ++ci, ++app) {
+                const int ch = op_chan[ci];
+                const int k0 = chan_kraus_ptr[ch], k1 = chan_kraus_ptr[ch + 1];
+                if (k1 <= k0) return set_err(QF_EINVAL, "KrausChannel: no operators");
+                QF_CUDA(launch_local_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], (double2*)d_rho.p, s));
+                QF_CUDA(cudaMemcpyAsync(rho.data(), d_rho.p, (size_t)nb * D * D * 16, cudaMemcpyDeviceToHost, s));
+                QF_CUDA(cudaStreamSynchronize(s));
+                for (int b = 0; b < nb; ++b) {
+                    const double2* r = rho.data() + (size_t)b * D * D;
+                    std::vector<double> probs;
+                    double acc = 0.0;
+                    for (int k = k0; k < k1; ++k) {  // p_k = || K_k psi ||^2 = tr(K rho K^dagger)
+                        const double* K = kraus + 32 * (size_t)k;
+                        double pk = 0.0;
+                        for (int a = 0; a < D; ++a) {
+                            cd kr[4];
+                            for (int i = 0; i < D; ++i) kr[i] = cd(K[(a * 4 + i) * 2], K[(a * 4 + i) * 2 + 1]);
+                            cd sa = 0.0;
+                            for (int i = 0; i < D; ++i)
+                                for (int jj = 0; jj < D; ++jj)
+                                    sa += kr[i] * cd(r[i * D + jj].x, r[i * D + jj].y) * std::conj(kr[jj]);
+                            pk += sa.real();
+                        }
+                        probs.push_back(pk);
+                        acc += pk;
+                    }
+                    if (!(acc > 1e-14)) return set_err(QF_EINVAL, "mc_trajectory: all branch probabilities vanish");
+                    const double uu = u[(size_t)(t0 + b) * n_apps + app] * acc;
+                    size_t pick = probs.size() - 1;
+                    double run = 0.0;
+                    for (size_t i = 0; i < probs.size(); ++i) {
+                        run += probs[i];
+                        if (uu < run) {
+                            pick = i;
+                            break;
+                        }
+                    }
+                    const double pp = probs[pick], sc = 1.0 / std::sqrt(pp);
+                    const double* K = kraus + 32 * (size_t)(k0 + pick);
+                    for (int a = 0; a < D; ++a)
+                        for (int i = 0; i < D; ++i)
+                            km[(size_t)b * D * D + a * D + i] =
+                                make_double2(K[(a * 4 + i) * 2] * sc, K[(a * 4 + i) * 2 + 1] * sc);
+                    logp[b] += std::log(pp / acc) + std::log(acc);
+                }
+                QF_CUDA(cudaMemcpyAsync(d_k.p, km.data(), (size_t)nb * D * D * 16, cudaMemcpyHostToDevice, s));
+                QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true, s));
+                ctx->launches += 2;
+            }
+        }
+        if (log_probs)
+            for (int b = 0; b < nb; ++b) log_probs[t0 + b] = logp[b];
+        if (obs) {
+            HArgs ha{};
+            ha.psi = ctx->lam.p;
+            ha.n = n;
+            ha.kh = od->plan.kh;
+            ha.groups = (const DevGroup*)od->groups.p;
+            ha.n_groups = (int)od->plan.groups.size();
+            ha.terms = (const DevTerm*)od->terms.p;
+            ha.write_lam = 0;
+            ha.epart = (double*)d_part.p;
+            QF_CUDA(launch_hpsi(precision, ha, nb, s));
+            ReduceArgs ra{};
+            ra.part = (const double*)d_part.p;
+            ra.count = 1;
+            ra.tiles = tiles_h;
+            ra.out = (double*)d_E.p;
+            QF_CUDA(launch_reduce(ra, nb, s));
+            QF_CUDA(cudaMemcpyAsync(expvals + t0, d_E.p, (size_t)nb * 8, cudaMemcpyDeviceToHost, s));
+        }
+        if (states) {
+            if (precision == QF_C128) {
+                QF_CUDA(cudaMemcpyAsync(states + (size_t)t0 * 2 * N, ctx->lam.p, (size_t)nb * N * 16,
+                                        cudaMemcpyDeviceToHost, s));
+            } else {
+                fbuf.resize((size_t)nb * 2 * N);
+                QF_CUDA(cudaMemcpyAsync(fbuf.data(), ctx->lam.p, (size_t)nb * N * 8, cudaMemcpyDeviceToHost, s));
+                QF_CUDA(cudaStreamSynchronize(s));
+                for (size_t i = 0; i < fbuf.size(); ++i) states[(size_t)t0 * 2 * N + i] = fbuf[i];
+            }
+        }
+        QF_CUDA(cudaStreamSynchronize(s));
     }
     return QF_OK;
 }

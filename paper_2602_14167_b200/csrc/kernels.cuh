@@ -92,6 +92,13 @@ cudaError_t launch_meas_project(int prec, void* psi, int n, int batch, const Mea
 int sample_chunk_bits(int n);
 cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const double* u, double* csum, int64_t* hit,
                           cudaStream_t s);
+// one 1- or 2-qubit operator (memory bit positions p0 = wires[0], p1 = wires[1] or -1)
+// on every state; m = [D][D] complex row-major, shared or one per state
+cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
+                               cudaStream_t s);
+// reduced density matrix of every state on those wires: rho [batch][D][D]
+cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
+                             cudaStream_t s);
 cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);
 
 // rows / cols ascending per row, complex128 values

@@ -174,7 +174,124 @@ __global__ void sample_pick_kernel(const V* psi, int n, int chunk_bits, const do
     hit[b] = h;
 }
 
+// Local operator on wires (w0[, w1]) of every state: amplitude quads / pairs in
+// the local basis (w0 most significant), matrix shared (mstride = 0) or per state.
+// Used by the noise trajectories, where every gate / Kraus branch is its own pass.
+template <typename V, int D>
+__global__ void apply_local_kernel(V* psi, int n, int p0, int p1, const double2* m, int mstride) {
+    const int b = blockIdx.y;
+    const double2* mb = m + (size_t)b * mstride;
+    double2 mm[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) mm[i] = mb[i];
+    const uint32_t N = 1u << n, R = N / D;
+    const uint32_t mask = D == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
+    const uint32_t free = (N - 1) & ~mask;
+    V* ps = psi + (size_t)b * N;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+        const uint32_t base = pdep32(r, free);
+        uint32_t idx[D];
+        double2 a[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            idx[i] = base | (D == 2 ? (i ? (1u << p0) : 0u)
+                                    : (((i >> 1) & 1) ? (1u << p0) : 0u) | ((i & 1) ? (1u << p1) : 0u));
+            const V v = ps[idx[i]];
+            a[i] = make_double2((double)v.x, (double)v.y);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double2 c = mm[i * D + j];
+                re += c.x * a[j].x - c.y * a[j].y;
+                im += c.x * a[j].y + c.y * a[j].x;
+            }
+            V o;
+            o.x = (decltype(o.x))re;
+            o.y = (decltype(o.y))im;
+            ps[idx[i]] = o;
+        }
+    }
+}
+
+// rho[b][i][j] = sum over the other wires of psi_i conj(psi_j) on wires (w0[, w1]):
+// one block per state, fixed order
+template <typename V, int D>
+__global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int p0, int p1, double2* rho) {
+    __shared__ double red[8][2 * D * D];
+    const int b = blockIdx.x;
+    const uint32_t N = 1u << n, R = N / D;
+    const uint32_t mask = D == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
+    const uint32_t free = (N - 1) & ~mask;
+    const V* ps = psi + (size_t)b * N;
+    double acc[2 * D * D];
+#pragma unroll
+    for (int i = 0; i < 2 * D * D; ++i) acc[i] = 0.0;
+    for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
+        const uint32_t base = pdep32(r, free);
+        double2 a[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const uint32_t x = base | (D == 2 ? (i ? (1u << p0) : 0u)
+                                              : (((i >> 1) & 1) ? (1u << p0) : 0u) | ((i & 1) ? (1u << p1) : 0u));
+            const V v = ps[x];
+            a[i] = make_double2((double)v.x, (double)v.y);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                acc[2 * (i * D + j)] += a[i].x * a[j].x + a[i].y * a[j].y;
+                acc[2 * (i * D + j) + 1] += a[i].y * a[j].x - a[i].x * a[j].y;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * D * D; ++i) {
+        double v = acc[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * D * D) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+        reinterpret_cast<double*>(rho + (size_t)b * D * D)[threadIdx.x] = t;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
+                               cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    const int D = p1 >= 0 ? 4 : 2;
+    const uint32_t R = (1u << n) / D;
+    dim3 grid(std::max(1u, std::min<uint32_t>((R + 255) / 256, 512)), batch);
+    const int ms = per_state ? D * D : 0;
+    if (prec == 1) {
+        if (D == 2) apply_local_kernel<double2, 2><<<grid, 256, 0, s>>>((double2*)psi, n, p0, p1, m, ms);
+        else apply_local_kernel<double2, 4><<<grid, 256, 0, s>>>((double2*)psi, n, p0, p1, m, ms);
+    } else {
+        if (D == 2) apply_local_kernel<float2, 2><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms);
+        else apply_local_kernel<float2, 4><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
+                             cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    if (prec == 1) {
+        if (p1 < 0) local_rho_kernel<double2, 2><<<batch, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
+        else local_rho_kernel<double2, 4><<<batch, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
+    } else {
+        if (p1 < 0) local_rho_kernel<float2, 2><<<batch, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
+        else local_rho_kernel<float2, 4><<<batch, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
+    }
+    return cudaGetLastError();
+}
 
 int sample_chunk_bits(int n) { return n > 10 ? 10 : n; }
 

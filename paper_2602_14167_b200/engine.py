@@ -348,6 +348,48 @@ def shadow_snapshots(ctx: Context, prep: Program, theta, bases, u) -> np.ndarray
     return out
 
 
+def noise_trajectories(ctx: Context, n: int, ops: Sequence, mats, op_channels, channels, u, precision="c128",
+                       init=None, obs: Optional["Observable"] = None, want_states: bool = True):
+    """Batched mc_trajectory (qf_noise_trajectories, noise.cpp:162-197).
+    op_channels[j]: channel indices firing after op j; channels[c]: list of D x D
+    Kraus matrices; u: [T, n_apps] uniforms (one per channel application, in
+    order).  Returns (states [T, 2^n] complex or None, log_probs [T], energies [T] or None)."""
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    T = int(u.shape[0])
+    ptr = [0]
+    flat = []
+    for j in range(len(ops)):
+        chs = list(op_channels[j]) if j < len(op_channels) else []
+        flat += chs
+        ptr.append(len(flat))
+    kptr = [0]
+    kr = []
+    for ops_k in channels:
+        for k in ops_k:
+            k = np.asarray(k, dtype=np.complex128)
+            full = np.zeros((4, 4), np.complex128)
+            full[: k.shape[0], : k.shape[1]] = k
+            kr.append(full)
+        kptr.append(len(kr))
+    if u.ndim != 2 or u.shape[1] != ptr[-1]:
+        raise ValueError("noise_trajectories: u must be [trajectories, channel applications]")
+    as_i = lambda v: (ctypes.c_int * max(1, len(v)))(*v)  # noqa: E731
+    kr_v = np.ascontiguousarray(np.array(kr if kr else [np.zeros((4, 4))], np.complex128)).view(np.float64).reshape(-1)
+    arr = _op_array(ops)
+    mv, nm = _mats_array(mats)
+    init_v = None
+    if init is not None:
+        init_v = np.ascontiguousarray(np.asarray(init, np.complex128).reshape(-1)).view(np.float64)
+    states = np.zeros((T, 1 << n), np.complex128) if want_states else None
+    logp = np.zeros(T)
+    ev = np.zeros(T) if obs is not None else None
+    check(ctx.lib.qf_noise_trajectories(
+        ctx.handle, n, len(ops), arr, dptr(mv), nm, as_i(ptr), as_i(flat), as_i(kptr), dptr(kr_v), dptr(init_v), T,
+        dptr(u), PRECISIONS[precision], dptr(states.view(np.float64)) if states is not None else None, dptr(logp),
+        obs.handle if obs is not None else None, dptr(ev) if ev is not None else None))
+    return states, logp, ev
+
+
 def adam_step_device(ctx: Context, theta, m, v, g, t: int, lr: float, beta1=0.9, beta2=0.999,
                      eps=1e-8) -> None:
     B, P = (int(theta.shape[0]), int(theta.shape[1])) if theta.dim() == 2 else (1, int(theta.numel()))

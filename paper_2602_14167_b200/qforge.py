@@ -698,3 +698,146 @@ def vqe_run(ansatz: AnsatzSpec, theta0_batch, h: PauliSum, steps: int, lr: float
     from .vqe import vqe_run_device
 
     return vqe_run_device(ansatz, theta0_batch, h, steps, lr, grad_mode)
+
+
+# ---------------------------------------------------------------- noise (noise.hpp / noise.cpp)
+class KrausChannel:  # noise.hpp:15-23
+    def __init__(self, name: str = "", arity: int = 1, operators=None):
+        self.name = name
+        self.arity = arity
+        self.operators = [np.asarray(k, dtype=np.complex128) for k in (operators or [])]
+
+    def completeness_defect(self) -> float:  # noise.cpp:10-16
+        if not self.operators:
+            return 1.0
+        d = self.operators[0].shape[0]
+        acc = sum(k.conj().T @ k for k in self.operators)
+        return float(np.abs(acc - np.eye(d)).max())
+
+    def validate(self) -> None:  # noise.cpp:18-25
+        _require(bool(self.operators), "KrausChannel: no operators")
+        d = 1 << self.arity
+        for k in self.operators:
+            _require(k.shape == (d, d), "KrausChannel: wrong operator shape")
+        _require(self.completeness_defect() <= 1e-10, "KrausChannel: completeness violated")
+
+
+_PAULI = [np.eye(2, dtype=complex), np.array([[0, 1], [1, 0]], complex), np.array([[0, -1j], [1j, 0]]),
+          np.diag([1.0 + 0j, -1.0])]
+
+
+def depolarizing_channel(p: float, k: int = 1) -> KrausChannel:  # noise.cpp:27-60
+    _require(0.0 <= p <= 1.0, "depolarizing_channel: p out of range")
+    _require(1 <= k <= 3, "depolarizing_channel: arity out of range")
+    words = 4 ** k
+    pw = p / (words - 1)
+    ops = []
+    for w in range(words):
+        weight = 1.0 - p if w == 0 else pw
+        if weight == 0.0:
+            continue
+        op = np.eye(1, dtype=complex)
+        ww = w
+        for _ in range(k):  # site 0 is the least significant Kronecker factor
+            op = np.kron(_PAULI[ww % 4], op)
+            ww //= 4
+        ops.append(np.sqrt(weight) * op)
+    ch = KrausChannel("depolarizing", k, ops)
+    ch.validate()
+    return ch
+
+
+def amplitude_damping_channel(gamma: float) -> KrausChannel:  # noise.cpp:62-72
+    _require(0.0 <= gamma <= 1.0, "amplitude_damping_channel: gamma out of range")
+    ch = KrausChannel("amplitude_damping", 1, [np.array([[1, 0], [0, np.sqrt(1.0 - gamma)]], complex),
+                                               np.array([[0, np.sqrt(gamma)], [0, 0]], complex)])
+    ch.validate()
+    return ch
+
+
+def phase_damping_channel(lam: float) -> KrausChannel:  # noise.cpp:74-84
+    _require(0.0 <= lam <= 1.0, "phase_damping_channel: lambda out of range")
+    ch = KrausChannel("phase_damping", 1, [np.array([[1, 0], [0, np.sqrt(1.0 - lam)]], complex),
+                                           np.array([[0, 0], [0, np.sqrt(lam)]], complex)])
+    ch.validate()
+    return ch
+
+
+def reset_channel(p: float) -> KrausChannel:  # noise.cpp:86-97
+    _require(0.0 <= p <= 1.0, "reset_channel: p out of range")
+    sp, sq = np.sqrt(p), np.sqrt(1.0 - p)
+    ch = KrausChannel("reset", 1, [sq * np.eye(2, dtype=complex), np.array([[sp, 0], [0, 0]], complex),
+                                   np.array([[0, sp], [0, 0]], complex)])
+    ch.validate()
+    return ch
+
+
+def thermal_relaxation_channel(gamma: float, lam: float) -> KrausChannel:  # noise.cpp:99-111
+    ad, pd = amplitude_damping_channel(gamma), phase_damping_channel(lam)
+    ch = KrausChannel("thermal_relaxation", 1, [k2 @ k1 for k2 in pd.operators for k1 in ad.operators])
+    ch.validate()
+    return ch
+
+
+class NoiseConf:  # noise.hpp:37-60, noise.cpp:113-145
+    def __init__(self):
+        self.rules = []  # (gate name or "", wires or None, predicate or None, channel)
+
+    def attach(self, gate: str, channel: KrausChannel) -> None:
+        channel.validate()
+        self.rules.append((gate, None, None, channel))
+
+    def attach_on_wires(self, gate: str, wires, channel: KrausChannel) -> None:
+        channel.validate()
+        _require(channel.arity == len(wires), "NoiseConf: channel arity does not match wire tuple")
+        self.rules.append((gate, list(wires), None, channel))
+
+    def attach_predicate(self, pred, channel: KrausChannel) -> None:
+        channel.validate()
+        self.rules.append(("", None, pred, channel))
+
+    def match(self, instr) -> list:
+        out = []
+        for gate, wires, pred, ch in self.rules:
+            if gate and gate != gate_name(Gate(instr.name)):
+                continue
+            if wires is not None and wires != list(instr.wires):
+                continue
+            if pred is not None and not pred(instr):
+                continue
+            if ch.arity != len(instr.wires):
+                continue
+            out.append(ch)
+        return out
+
+
+class Trajectory:  # noise.hpp:62-65
+    def __init__(self, state: StateVector, log_prob: float):
+        self.state = state
+        self.log_prob = log_prob
+
+
+def mc_trajectories(c: Circuit, conf: NoiseConf, rng, count: int) -> list:
+    """`count` consecutive mc_trajectory(c, conf, rng) calls (noise.cpp:162-197) as
+    one batched GPU run: the uniforms are drawn from `rng` in the same order."""
+    _require(c.d == 2, "mc_trajectory: qubits only")
+    ops, mats = _circuit_ops(c)
+    chans, index, op_channels = [], {}, []
+    for instr in c.ops:
+        ids = []
+        for ch in conf.match(instr):
+            if id(ch) not in index:
+                index[id(ch)] = len(chans)
+                chans.append(ch.operators)
+            ids.append(index[id(ch)])
+        op_channels.append(ids)
+    n_apps = sum(len(x) for x in op_channels)
+    u = np.array([[rng.uniform() for _ in range(n_apps)] for _ in range(count)]).reshape(count, n_apps)
+    ctx = _eng.default_context()
+    states, logp, _ = _eng.noise_trajectories(ctx, c.n, ops, mats, op_channels, chans, u, _precision,
+                                              init=c.initial_state)
+    return [Trajectory(StateVector(c.n, 2, states[t]), float(logp[t])) for t in range(count)]
+
+
+def mc_trajectory(c: Circuit, conf: NoiseConf, rng) -> Trajectory:  # noise.cpp:162-197
+    return mc_trajectories(c, conf, rng, 1)[0]

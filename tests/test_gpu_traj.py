@@ -69,3 +69,76 @@ def test_shadow_gen_cli_dataset(ctx, tmp_path):
         b, o = line.split(";")
         assert b == "".join(str(c) for c in bases[r]) and o == "".join(str(x) for x in ref[r])
     assert cli.main(["shadow-gen", "--out", str(tmp_path), "--set", "n=25"]) == 2
+
+
+def _noisy_circuit(n, depth, rng):
+    ops = []
+    for _ in range(depth):
+        for q in range(n):
+            ops.append((po.GID["h"], q, -1, -1, 1.0, 0.0, -1))
+            ops.append((po.GID["rx"], q, -1, -1, 1.0, 3.0 * rng.uniform() - 1.5, -1))
+        for q in range(n - 1):
+            ops.append((po.GID["cx"], q, q + 1, -1, 1.0, 0.0, -1))
+        ops.append((po.GID["ry"], n - 1, -1, -1, 1.0, rng.uniform(), -1))
+    return ops
+
+
+def _channels_for(ops):
+    from paper_2602_14167_b200 import qforge as qf
+    chans = [qf.depolarizing_channel(0.05, 2).operators, qf.amplitude_damping_channel(0.08).operators,
+             qf.phase_damping_channel(0.1).operators, qf.thermal_relaxation_channel(0.2, 0.3).operators,
+             qf.reset_channel(0.15).operators]
+    by = {po.GID["cx"]: [0], po.GID["h"]: [1], po.GID["rx"]: [2], po.GID["ry"]: [3, 4]}
+    return [by.get(op[0], []) for op in ops], chans
+
+
+@pytest.mark.parametrize("n,depth", [(2, 2), (4, 2), (6, 1)])
+def test_noise_trajectories_match_oracle(ctx, n, depth):
+    """mc_trajectory (noise.cpp:162-197) per trajectory with the same uniforms:
+    states and log-probabilities (complex128), and the energy output path."""
+    rng = po.Rng(40 + n)
+    ops = _noisy_circuit(n, depth, rng)
+    op_ch, chans = _channels_for(ops)
+    T = 12
+    n_apps = sum(len(x) for x in op_ch)
+    u = np.array([[rng.uniform() for _ in range(n_apps)] for _ in range(T)])
+    h = po.tfim(n, 0.7)
+    obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
+    states, logp, ev = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, "c128", obs=obs)
+    for t in range(T):
+        ref_s, ref_l = po.mc_trajectory(n, ops, op_ch, chans, u[t])
+        assert np.abs(states[t] - ref_s).max() < 1e-10 and abs(logp[t] - ref_l) < 1e-10
+        assert abs(ev[t] - po.expectation(n, ref_s, h).real) < 1e-10
+
+
+def test_noise_trajectory_reference_cases(ctx):
+    """test_noise.cpp:175-214: empty configuration = pure run (log_prob 0); certain
+    decay lands in the ground state; the trajectory average of <Z_0> matches the
+    exact channel average within three sigma."""
+    from paper_2602_14167_b200 import qforge as qf
+    from paper_2602_14167_b200.rng import RngStream
+    c = qf.Circuit(4)
+    for q in range(4):
+        c.h(q)
+        c.rx(q, 0.3 + q)
+    c.cx(0, 1).cx(1, 2)
+    t = qf.mc_trajectory(c, qf.NoiseConf(), RngStream(3))
+    assert np.abs(t.state.amps - qf.run(c).amps).max() < 1e-12 and t.log_prob == 0.0
+    conf = qf.NoiseConf()
+    conf.attach("x", qf.amplitude_damping_channel(1.0))
+    one = qf.Circuit(1)
+    one.x(0)
+    for tr in qf.mc_trajectories(one, conf, RngStream(5), 20):
+        assert abs(abs(tr.state.amps[0]) - 1.0) < 1e-12 and abs(tr.log_prob) < 1e-12
+    rng = po.Rng(11)
+    for rep in range(3):
+        ops = _noisy_circuit(4, 2, rng)
+        op_ch, chans = _channels_for(ops)
+        exact = po.density_matrix_expect_z0(4, ops, op_ch, chans)
+        T = 4000
+        n_apps = sum(len(x) for x in op_ch)
+        r2 = po.Rng(100 + rep)
+        u = np.array([[r2.uniform() for _ in range(n_apps)] for _ in range(T)])
+        z0 = engine.Observable(ctx, 4, np.array([[3, 0, 0, 0]], np.int8), np.array([1.0]))
+        _, _, ev = engine.noise_trajectories(ctx, 4, ops, None, op_ch, chans, u, "c128", obs=z0, want_states=False)
+        assert abs(ev.mean() - exact) < 3.0 / np.sqrt(T)
