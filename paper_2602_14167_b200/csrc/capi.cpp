@@ -1824,7 +1824,8 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
     LocalBuf d_gm, d_rho, d_k, d_init, d_part, d_E;
     QF_CUDA(d_gm.reserve(gm.size() * 16));
     QF_CUDA(cudaMemcpyAsync(d_gm.p, gm.data(), gm.size() * 16, cudaMemcpyHostToDevice, s));
-    QF_CUDA(d_rho.reserve((size_t)bc * 16 * 16));
+    const int parts = local_rho_parts(n);
+    QF_CUDA(d_rho.reserve((size_t)bc * parts * 16 * 16));
     QF_CUDA(d_k.reserve((size_t)bc * 16 * 16));
     if (init) {
         QF_CUDA(d_init.reserve(N * vs));
@@ -1848,7 +1849,7 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
         QF_CUDA(d_part.reserve((size_t)bc * tiles_h * 8));
         QF_CUDA(d_E.reserve((size_t)bc * 8));
     }
-    std::vector<double2> rho((size_t)bc * 16), km((size_t)bc * 16);
+    std::vector<double2> rho((size_t)bc * parts * 16), km((size_t)bc * 16);
     std::vector<double> logp(bc);
     std::vector<float> fbuf;
     for (int t0 = 0; t0 < trajectories; t0 += bc) {
@@ -1869,10 +1870,19 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
                 const int k0 = chan_kraus_ptr[ch], k1 = chan_kraus_ptr[ch + 1];
                 if (k1 <= k0) return set_err(QF_EINVAL, "KrausChannel: no operators");
                 QF_CUDA(launch_local_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], (double2*)d_rho.p, s));
-                QF_CUDA(cudaMemcpyAsync(rho.data(), d_rho.p, (size_t)nb * D * D * 16, cudaMemcpyDeviceToHost, s));
+                QF_CUDA(cudaMemcpyAsync(rho.data(), d_rho.p, (size_t)nb * parts * D * D * 16, cudaMemcpyDeviceToHost,
+                                        s));
                 QF_CUDA(cudaStreamSynchronize(s));
                 for (int b = 0; b < nb; ++b) {
-                    const double2* r = rho.data() + (size_t)b * D * D;
+                    double2 r[16];
+                    for (int e = 0; e < D * D; ++e) {  // parts summed in order
+                        double x = 0.0, y = 0.0;
+                        for (int pt = 0; pt < parts; ++pt) {
+                            x += rho[((size_t)b * parts + pt) * D * D + e].x;
+                            y += rho[((size_t)b * parts + pt) * D * D + e].y;
+                        }
+                        r[e] = make_double2(x, y);
+                    }
                     std::vector<double> probs;
                     double acc = 0.0;
                     for (int k = k0; k < k1; ++k) {  // p_k = || K_k psi ||^2 = tr(K rho K^dagger)

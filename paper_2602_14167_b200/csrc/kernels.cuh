@@ -96,7 +96,9 @@ cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const dou
 // on every state; m = [D][D] complex row-major, shared or one per state
 cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                                cudaStream_t s);
-// reduced density matrix of every state on those wires: rho [batch][D][D]
+// reduced density matrix of every state on those wires, as local_rho_parts(n)
+// fixed-order partials: rho [batch][parts][D][D] (the caller sums the parts in order)
+int local_rho_parts(int n);
 cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
                              cudaStream_t s);
 cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);

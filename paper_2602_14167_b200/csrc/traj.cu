@@ -216,12 +216,12 @@ __global__ void apply_local_kernel(V* psi, int n, int p0, int p1, const double2*
     }
 }
 
-// rho[b][i][j] = sum over the other wires of psi_i conj(psi_j) on wires (w0[, w1]):
-// one block per state, fixed order
+// rho partials [b][part][i][j] = sum over part of the other wires' indices of
+// psi_i conj(psi_j) on wires (w0[, w1]); fixed order (the caller sums the parts)
 template <typename V, int D>
 __global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int p0, int p1, double2* rho) {
     __shared__ double red[8][2 * D * D];
-    const int b = blockIdx.x;
+    const int b = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
     const uint32_t N = 1u << n, R = N / D;
     const uint32_t mask = D == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
     const uint32_t free = (N - 1) & ~mask;
@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int
     double acc[2 * D * D];
 #pragma unroll
     for (int i = 0; i < 2 * D * D; ++i) acc[i] = 0.0;
-    for (uint32_t r = threadIdx.x; r < R; r += blockDim.x) {
+    const uint32_t r0 = (uint32_t)((uint64_t)R * part / parts), r1 = (uint32_t)((uint64_t)R * (part + 1) / parts);
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
         const uint32_t base = pdep32(r, free);
         double2 a[D];
 #pragma unroll
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int
     if (threadIdx.x < 2 * D * D) {
         double t = 0.0;
         for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
-        reinterpret_cast<double*>(rho + (size_t)b * D * D)[threadIdx.x] = t;
+        reinterpret_cast<double*>(rho + ((size_t)b * parts + part) * D * D)[threadIdx.x] = t;
     }
 }
 
@@ -280,15 +281,18 @@ cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, in
     return cudaGetLastError();
 }
 
+int local_rho_parts(int n) { return n >= 14 ? 16 : 1; }
+
 cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
                              cudaStream_t s) {
     if (batch == 0) return cudaSuccess;
+    const dim3 grid(local_rho_parts(n), batch);
     if (prec == 1) {
-        if (p1 < 0) local_rho_kernel<double2, 2><<<batch, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
-        else local_rho_kernel<double2, 4><<<batch, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
+        if (p1 < 0) local_rho_kernel<double2, 2><<<grid, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
+        else local_rho_kernel<double2, 4><<<grid, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
     } else {
-        if (p1 < 0) local_rho_kernel<float2, 2><<<batch, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
-        else local_rho_kernel<float2, 4><<<batch, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
+        if (p1 < 0) local_rho_kernel<float2, 2><<<grid, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
+        else local_rho_kernel<float2, 4><<<grid, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
     }
     return cudaGetLastError();
 }
