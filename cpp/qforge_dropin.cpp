@@ -6,6 +6,7 @@
 // /root/reference/proj.
 #include <algorithm>
 #include <cmath>
+#include <fstream>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -15,6 +16,8 @@
 
 #include "qforge/circuit.hpp"
 #include "qforge/lattice.hpp"
+#include "qforge/noise.hpp"
+#include "qforge/shadows.hpp"
 #include "qforge/pauli.hpp"
 #include "qforge/variational.hpp"
 #include "qforge_b200.h"
@@ -467,6 +470,286 @@ SparseCOO SparseCOO::operator+(const SparseCOO& other) const {
     for (size_t k = 0; k < other.vals.size(); ++k) s.push(other.rows[k], other.cols[k], other.vals[k]);
     s.canonicalize();
     return s;
+}
+
+// ------------------------------------------------------------------ shadows (shadows.cpp)
+void ShadowDataset::validate() const {
+    require(n >= 1, "ShadowDataset: n must be >= 1");
+    require(bases.size() == outcomes.size(), "ShadowDataset: row count mismatch");
+    for (size_t r = 0; r < bases.size(); ++r) {
+        require((int)bases[r].size() == n, "ShadowDataset: bad basis row");
+        require((int)outcomes[r].size() == n, "ShadowDataset: bad outcome row");
+        for (int c : bases[r]) require(c >= 1 && c <= 3, "ShadowDataset: bad basis code");
+        for (int b : outcomes[r]) require(b == 0 || b == 1, "ShadowDataset: bad outcome");
+    }
+}
+
+std::vector<std::vector<int>> random_bases(std::size_t m, int n, RngStream& rng) {  // shadows.cpp:24-29
+    std::vector<std::vector<int>> out(m, std::vector<int>(n));
+    for (auto& row : out)
+        for (int& c : row) c = 1 + (int)rng.uniform_below(3);
+    return out;
+}
+
+ShadowDataset shadow_snapshots(const StateVector& psi, const std::vector<std::vector<int>>& bases, RngStream& rng,
+                               int /*workers*/) {  // shadows.cpp:50-85
+    require(psi.d == 2, "shadow_snapshots: qubits only");
+    const size_t m = bases.size();
+    ShadowDataset ds;
+    ds.n = psi.n;
+    ds.bases = bases;
+    ds.outcomes.assign(m, std::vector<int>(psi.n, 0));
+    if (m == 0) return ds;
+    std::vector<int8_t> codes(m * psi.n);
+    for (size_t r = 0; r < m; ++r) {
+        require((int)bases[r].size() == psi.n, "shadow_snapshots: bad basis row");
+        for (int q = 0; q < psi.n; ++q) codes[r * psi.n + q] = (int8_t)bases[r][q];
+    }
+    const std::vector<RngStream> streams = rng.split(m);
+    std::vector<double> u(m);
+    for (size_t r = 0; r < m; ++r) u[r] = RngStream(streams[r]).uniform();
+    Circuit c(psi.n);
+    c.initial_state = psi.amps;
+    auto prog = make_program(circuit_template(c, nullptr), 0);
+    std::vector<int8_t> out(m * psi.n);
+    check(qf_shadow_snapshots(ctx(), prog->p, nullptr, (int)m, codes.data(), u.data(), out.data()));
+    for (size_t r = 0; r < m; ++r)
+        for (int q = 0; q < psi.n; ++q) ds.outcomes[r][q] = out[r * psi.n + q];
+    return ds;
+}
+
+double estimate_pauli(const ShadowDataset& ds, const std::vector<int>& obs_codes, int n_batches) {  // :86-122
+    require((int)obs_codes.size() == ds.n, "estimate_pauli: length mismatch");
+    require(n_batches >= 1, "estimate_pauli: n_batches must be >= 1");
+    std::vector<int> support;
+    for (int q = 0; q < ds.n; ++q) {
+        require(obs_codes[q] >= 0 && obs_codes[q] <= 3, "estimate_pauli: bad code");
+        if (obs_codes[q]) support.push_back(q);
+    }
+    if (support.empty()) return 1.0;
+    const size_t m = ds.size();
+    require(m > 0, "estimate_pauli: empty dataset");
+    require((size_t)n_batches <= m, "estimate_pauli: more batches than snapshots");
+    std::vector<double> mean(n_batches, 0.0);
+    std::vector<size_t> cnt(n_batches, 0);
+    for (size_t r = 0; r < m; ++r) {
+        double v = 1.0;
+        for (int q : support) {
+            if (ds.bases[r][q] != obs_codes[q]) {
+                v = 0.0;
+                break;
+            }
+            v *= 3.0 * (1.0 - 2.0 * ds.outcomes[r][q]);
+        }
+        const size_t b = r * n_batches / m;
+        mean[b] += v;
+        ++cnt[b];
+    }
+    for (int b = 0; b < n_batches; ++b) mean[b] /= (double)cnt[b];
+    std::sort(mean.begin(), mean.end());
+    return n_batches % 2 ? mean[n_batches / 2] : 0.5 * (mean[n_batches / 2 - 1] + mean[n_batches / 2]);
+}
+
+void save_dataset(const ShadowDataset& ds, const std::string& path) {  // :124-136
+    ds.validate();
+    std::ofstream f(path);
+    require(f.good(), ("save_dataset: cannot open " + path).c_str());
+    f << ds.n << "," << ds.size() << "\n";
+    for (size_t r = 0; r < ds.size(); ++r) {
+        for (int c : ds.bases[r]) f << c;
+        f << ";";
+        for (int b : ds.outcomes[r]) f << b;
+        f << "\n";
+    }
+    require(f.good(), "save_dataset: write failed");
+}
+
+ShadowDataset load_dataset(const std::string& path) {  // :138-170
+    std::ifstream f(path);
+    require(f.good(), ("load_dataset: cannot open " + path).c_str());
+    std::string line;
+    require((bool)std::getline(f, line), "load_dataset: missing header");
+    const size_t comma = line.find(',');
+    require(comma != std::string::npos, "load_dataset: bad header");
+    ShadowDataset ds;
+    ds.n = std::stoi(line.substr(0, comma));
+    const size_t m = std::stoul(line.substr(comma + 1));
+    while (std::getline(f, line)) {
+        if (line.empty()) continue;
+        const size_t semi = line.find(';');
+        require(semi != std::string::npos, "load_dataset: bad row");
+        const std::string bs = line.substr(0, semi), os = line.substr(semi + 1);
+        require(bs.size() == (size_t)ds.n && os.size() == bs.size(), "load_dataset: bad row length");
+        std::vector<int> br(ds.n), orow(ds.n);
+        for (int q = 0; q < ds.n; ++q) {
+            br[q] = bs[q] - '0';
+            orow[q] = os[q] - '0';
+        }
+        ds.bases.push_back(br);
+        ds.outcomes.push_back(orow);
+    }
+    require(ds.size() == m, "load_dataset: row count mismatch");
+    ds.validate();
+    return ds;
+}
+
+// ------------------------------------------------------------------ noise (noise.cpp)
+double KrausChannel::completeness_defect() const {
+    if (operators.empty()) return 1.0;
+    const std::int64_t d = operators.front().rows();
+    ComplexMatrix acc = ComplexMatrix::Zero(d, d);
+    for (const auto& k : operators) acc = acc + k.adjoint() * k;
+    return (acc - ComplexMatrix::Identity(d, d)).cwiseAbs().maxCoeff();
+}
+
+void KrausChannel::validate() const {
+    require(!operators.empty(), "KrausChannel: no operators");
+    const std::int64_t d = (std::int64_t)1 << arity;
+    for (const auto& k : operators) require(k.rows() == d && k.cols() == d, "KrausChannel: wrong operator shape");
+    require(completeness_defect() <= 1e-10, "KrausChannel: completeness violated");
+}
+
+namespace {
+ComplexMatrix mat2(cplx a, cplx b, cplx c, cplx d) { return (ComplexMatrix(2, 2) << a, b, c, d).finished(); }
+ComplexMatrix kron(const ComplexMatrix& a, const ComplexMatrix& b) {
+    ComplexMatrix o(a.rows() * b.rows(), a.cols() * b.cols());
+    for (std::int64_t i = 0; i < a.rows(); ++i)
+        for (std::int64_t j = 0; j < a.cols(); ++j)
+            for (std::int64_t k = 0; k < b.rows(); ++k)
+                for (std::int64_t l = 0; l < b.cols(); ++l) o(i * b.rows() + k, j * b.cols() + l) = a(i, j) * b(k, l);
+    return o;
+}
+}  // namespace
+
+KrausChannel depolarizing_channel(double p, int k) {  // noise.cpp:27-60
+    require(p >= 0.0 && p <= 1.0, "depolarizing_channel: p out of range");
+    require(k >= 1 && k <= 3, "depolarizing_channel: arity out of range");
+    const cplx I(0.0, 1.0);
+    const ComplexMatrix paulis[4] = {ComplexMatrix::Identity(2, 2), mat2(0, 1, 1, 0), mat2(0, -I, I, 0), mat2(1, 0, 0, -1)};
+    KrausChannel ch;
+    ch.name = "depolarizing";
+    ch.arity = k;
+    int words = 1;
+    for (int i = 0; i < k; ++i) words *= 4;
+    const double pw = p / (words - 1);
+    for (int w = 0; w < words; ++w) {
+        const double weight = w == 0 ? 1.0 - p : pw;
+        if (weight == 0.0) continue;
+        ComplexMatrix op = ComplexMatrix::Identity(1, 1);
+        for (int site = 0, ww = w; site < k; ++site, ww /= 4) op = kron(paulis[ww % 4], op);
+        ch.operators.push_back(op * cplx(std::sqrt(weight)));
+    }
+    ch.validate();
+    return ch;
+}
+
+KrausChannel amplitude_damping_channel(double gamma) {  // noise.cpp:62-72
+    require(gamma >= 0.0 && gamma <= 1.0, "amplitude_damping_channel: gamma out of range");
+    KrausChannel ch{"amplitude_damping", 1, {mat2(1, 0, 0, std::sqrt(1.0 - gamma)), mat2(0, std::sqrt(gamma), 0, 0)}};
+    ch.validate();
+    return ch;
+}
+
+KrausChannel phase_damping_channel(double lambda) {  // noise.cpp:74-84
+    require(lambda >= 0.0 && lambda <= 1.0, "phase_damping_channel: lambda out of range");
+    KrausChannel ch{"phase_damping", 1, {mat2(1, 0, 0, std::sqrt(1.0 - lambda)), mat2(0, 0, 0, std::sqrt(lambda))}};
+    ch.validate();
+    return ch;
+}
+
+KrausChannel reset_channel(double p) {  // noise.cpp:86-97
+    require(p >= 0.0 && p <= 1.0, "reset_channel: p out of range");
+    const double sp = std::sqrt(p), sq = std::sqrt(1.0 - p);
+    KrausChannel ch{"reset", 1, {mat2(sq, 0, 0, sq), mat2(sp, 0, 0, 0), mat2(0, sp, 0, 0)}};
+    ch.validate();
+    return ch;
+}
+
+KrausChannel thermal_relaxation_channel(double gamma, double lambda) {  // noise.cpp:99-111
+    const KrausChannel ad = amplitude_damping_channel(gamma), pd = phase_damping_channel(lambda);
+    KrausChannel ch;
+    ch.name = "thermal_relaxation";
+    ch.arity = 1;
+    for (const auto& k2 : pd.operators)
+        for (const auto& k1 : ad.operators) ch.operators.push_back(k2 * k1);
+    ch.validate();
+    return ch;
+}
+
+void NoiseConf::attach(const std::string& gate, KrausChannel channel) {  // noise.cpp:113-131
+    channel.validate();
+    rules.push_back({gate, std::nullopt, nullptr, std::move(channel)});
+}
+
+void NoiseConf::attach_on_wires(const std::string& gate, std::vector<int> wires, KrausChannel channel) {
+    channel.validate();
+    require(channel.arity == (int)wires.size(), "NoiseConf: channel arity does not match wire tuple");
+    rules.push_back({gate, std::move(wires), nullptr, std::move(channel)});
+}
+
+void NoiseConf::attach_predicate(std::function<bool(const GateInstruction&)> pred, KrausChannel channel) {
+    channel.validate();
+    rules.push_back({"", std::nullopt, std::move(pred), std::move(channel)});
+}
+
+std::vector<const KrausChannel*> NoiseConf::match(const GateInstruction& instr) const {  // noise.cpp:133-145
+    std::vector<const KrausChannel*> out;
+    for (const auto& r : rules) {
+        if (!r.gate.empty() && r.gate != gate_name(instr.name)) continue;
+        if (r.wires && *r.wires != instr.wires) continue;
+        if (r.predicate && !r.predicate(instr)) continue;
+        if (r.channel.arity != (int)instr.wires.size()) continue;
+        out.push_back(&r.channel);
+    }
+    return out;
+}
+
+std::vector<Trajectory> mc_trajectories(const Circuit& c, const NoiseConf& conf, RngStream& rng, int count) {
+    require(c.d == 2, "mc_trajectory: qubits only");
+    require(count >= 0, "mc_trajectories: negative count");
+    Template t = circuit_template(c, nullptr);
+    std::vector<int> ptr{0}, ids, kptr{0};
+    std::vector<double> kraus;
+    std::vector<const KrausChannel*> chans;
+    for (const auto& instr : c.ops) {
+        for (const KrausChannel* ch : conf.match(instr)) {
+            auto it = std::find(chans.begin(), chans.end(), ch);
+            if (it == chans.end()) {
+                chans.push_back(ch);
+                for (const auto& k : ch->operators) push_matrix(kraus, k);
+                kptr.push_back((int)(kraus.size() / 32));
+                it = chans.end() - 1;
+            }
+            ids.push_back((int)(it - chans.begin()));
+        }
+        ptr.push_back((int)ids.size());
+    }
+    const int n_apps = (int)ids.size();
+    std::vector<double> u((size_t)count * n_apps);
+    for (auto& x : u) x = rng.uniform();  // the reference draws one uniform per application, in order
+    const size_t N = (size_t)1 << c.n;
+    std::vector<cplx> states((size_t)count * N);
+    std::vector<double> logp(count);
+    if (count > 0)
+        check(qf_noise_trajectories(ctx(), c.n, (int)t.ops.size(), t.ops.data(), t.mats.empty() ? nullptr : t.mats.data(),
+                                    (int)(t.mats.size() / 32), ptr.data(), ids.data(), kptr.data(),
+                                    kraus.empty() ? nullptr : kraus.data(),
+                                    t.init ? reinterpret_cast<const double*>(t.init->data()) : nullptr, count,
+                                    u.empty() ? nullptr : u.data(), (int)g_prec,
+                                    reinterpret_cast<double*>(states.data()), logp.data(), nullptr, nullptr));
+    std::vector<Trajectory> out(count);
+    for (int k = 0; k < count; ++k) {
+        out[k].state.n = c.n;
+        out[k].state.d = 2;
+        out[k].state.amps = ComplexVector::Zero((std::int64_t)N);
+        std::copy(states.begin() + (size_t)k * N, states.begin() + (size_t)(k + 1) * N, out[k].state.amps.data());
+        out[k].log_prob = logp[k];
+    }
+    return out;
+}
+
+Trajectory mc_trajectory(const Circuit& c, const NoiseConf& conf, RngStream& rng) {  // noise.cpp:162-197
+    return mc_trajectories(c, conf, rng, 1)[0];
 }
 
 // ------------------------------------------------------------------ variational

@@ -10,6 +10,8 @@
 
 #include "qforge/circuit.hpp"
 #include "qforge/lattice.hpp"
+#include "qforge/noise.hpp"
+#include "qforge/shadows.hpp"
 #include "qforge/variational.hpp"
 
 using namespace qforge;
@@ -73,6 +75,74 @@ int main() {
         CHECK(energy(t, theta, h) == energy(t, theta, h));
         const double e1 = energy(t, theta, h), e3 = energy(t, theta, pauli_sum_to_coo(h));  // operator formats
         CHECK(approx(e1, e3, 1e-12));
+    });
+    test_case("shadow snapshots", [] {  // test_shadows.cpp:101-145, 184-193
+        RngStream r1(1);
+        auto ds = shadow_snapshots(StateVector::zero_state(3), std::vector<std::vector<int>>(50, {3, 3, 3}), r1);
+        bool zeros = true;
+        for (const auto& row : ds.outcomes)
+            for (int b : row) zeros = zeros && b == 0;
+        CHECK(zeros);
+        Circuit plus(3);
+        plus.h(0).h(1).h(2);
+        RngStream r2(2);
+        ds = shadow_snapshots(run(plus), std::vector<std::vector<int>>(50, {1, 1, 1}), r2);
+        zeros = true;
+        for (const auto& row : ds.outcomes)
+            for (int b : row) zeros = zeros && b == 0;
+        CHECK(zeros);
+        RngStream r3(3);
+        ds = shadow_snapshots(StateVector::zero_state(1), std::vector<std::vector<int>>(10000, {1}), r3);
+        int ones = 0;
+        for (const auto& row : ds.outcomes) ones += row[0];
+        CHECK(std::abs(ones / 10000.0 - 0.5) < 3.0 * std::sqrt(0.25 / 10000.0));
+        Circuit c(4);
+        c.h(0).cx(0, 1).ry(2, 0.8).cx(2, 3);
+        RngStream brng(7), a(9), b(9);
+        auto bases = random_bases(64, 4, brng);
+        CHECK(shadow_snapshots(run(c), bases, a, 1).outcomes == shadow_snapshots(run(c), bases, b, 4).outcomes);
+        bool threw = false;
+        try {
+            RngStream r4(4);
+            shadow_snapshots(StateVector::zero_state(1), {{0}}, r4);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        Circuit bell(2);
+        bell.h(0).cx(0, 1);
+        RngStream r5(21);
+        auto bb = random_bases(10000, 2, r5);
+        auto bds = shadow_snapshots(run(bell), bb, r5);
+        CHECK(std::abs(estimate_pauli(bds, {1, 1}, 10) - 1.0) < 0.5);
+        save_dataset(bds, "/tmp/qf_dropin_shadows.csv");
+        auto back = load_dataset("/tmp/qf_dropin_shadows.csv");
+        CHECK(back.bases == bds.bases && back.outcomes == bds.outcomes);
+    });
+    test_case("noise trajectories", [] {  // test_noise.cpp:175-195
+        Circuit c(4);
+        for (int q = 0; q < 4; ++q) c.h(q).rx(q, 0.3 + q);
+        c.cx(0, 1).cx(1, 2).cx(2, 3);
+        RngStream rng(3);
+        Trajectory t = mc_trajectory(c, {}, rng);
+        CHECK((t.state.amps - run(c).amps).cwiseAbs().maxCoeff() < 1e-12);
+        CHECK(t.log_prob == 0.0);
+        NoiseConf conf;
+        conf.attach("x", amplitude_damping_channel(1.0));
+        Circuit one(1);
+        one.x(0);
+        RngStream r5(5);
+        for (const Trajectory& tr : mc_trajectories(one, conf, r5, 20)) {
+            CHECK(approx(std::abs(tr.state.amps[0]), 1.0, 1e-12));
+            CHECK(approx(tr.log_prob, 0.0, 1e-12));
+        }
+        CHECK(depolarizing_channel(0.05, 2).operators.size() == 16);
+        CHECK(thermal_relaxation_channel(0.1, 0.2).completeness_defect() < 1e-12);
+        NoiseConf wires;
+        wires.attach_on_wires("cx", {1, 2}, depolarizing_channel(0.1, 2));
+        int matched = 0;
+        for (const auto& op : c.ops) matched += (int)wires.match(op).size();
+        CHECK(matched == 1);
     });
     test_case("sparse operator", [] {  // pauli.cpp:89-153, sparse.cpp:44-51
         PauliSum h = tfim_chain(4, 0.7);
