@@ -113,8 +113,6 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const bool pipe = jit_pipe_mode();
     Out o;
     if (pipe) o.s += "// qf-option: pipelined\n";
-    if (const char* e = std::getenv("QF_JIT_SCALAR"))
-        if (e[0] == '1') o.s += "// qf-option: scalar-fp32\n";
     o.s += kPrelude;
     o.s += "\n";
     o("namespace qfb {");
@@ -1086,7 +1084,6 @@ bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
         std::ofstream(base + ".cu") << src;
     }
     std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DQF_JIT=1"};
-    if (src.find("// qf-option: scalar-fp32") != std::string::npos) opts.push_back("-DQF_JIT_SCALAR=1");
     nvrtcProgram prog = nullptr;
     if (g_nvrtc.create(&prog, src.c_str(), "qf_sweep.cu", 0, nullptr, nullptr) != 0) {
         err = "nvrtcCreateProgram failed";

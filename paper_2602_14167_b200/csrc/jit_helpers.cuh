@@ -32,12 +32,6 @@ template <typename V> __device__ __forceinline__ V mk_basis(bool one) {
 
 __device__ __forceinline__ float2 swp(float2 a) { return make_float2(a.y, a.x); }
 
-#ifdef QF_JIT_SCALAR  // A/B switch: scalar FP32 helpers
-__device__ __forceinline__ float2 __fmul2_rn(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
-__device__ __forceinline__ float2 __ffma2_rn(float2 a, float2 b, float2 c) {
-    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
-}
-#endif
 
 // a * d (complex)
 __device__ __forceinline__ float2 jcmul(float2 a, float2 d) {
