@@ -45,12 +45,16 @@ int set_err(int code, const std::string& msg) {
     return code;
 }
 
+static std::string launch_detail(const char* call) {
+    return std::strstr(call, "jit_launch") ? " [" + qfb::jit_last_launch_detail() + "]" : std::string();
+}
+
 #define QF_CUDA(call)                                                                     \
     do {                                                                                  \
         cudaError_t e_ = (call);                                                          \
         if (e_ != cudaSuccess)                                                            \
             return set_err(QF_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
-                                         " at " #call);                                   \
+                                         " at " #call + launch_detail(#call));            \
     } while (0)
 
 struct DevBuf {

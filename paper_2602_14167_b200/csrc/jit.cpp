@@ -1198,7 +1198,9 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
         const DevSweep& sw = jb.pass->sweeps[jb.si];
         jk.threads = 1 << (sw.k - sw.R);
         jk.smem = jit_smem_bytes(P, *jb.pass, jb.si, jb.bwd);
-        if (jk.smem > 48 * 1024) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, (const void*)kern);
+        if (jk.smem + fa.sharedSizeBytes > 48 * 1024) {  // static tables count against the 48 KB default
             e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
             if (e != cudaSuccess) {
                 st.error = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
@@ -1282,6 +1284,9 @@ int jit_launch_hpsi(const JitKernel& k, const HArgs& a, int tiles, int batch, vo
                                  (cudaStream_t)stream);
 }
 
+thread_local std::string g_launch_detail;
+const std::string& jit_last_launch_detail() { return g_launch_detail; }
+
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream) {
     SweepArgs aa = a;
     aa.batch = batch;
@@ -1292,6 +1297,17 @@ int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, voi
         grid = dim3((unsigned)std::min<long long>(items, (long long)k.ctas));
     }
     cudaError_t e = cudaLaunchKernel((const void*)k.kernel, grid, dim3(k.threads), args, k.smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) {  // keep the launch configuration next to the error for diagnosis
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, (const void*)k.kernel);
+        char buf[320];
+        snprintf(buf, sizeof buf,
+                 "sweep launch grid (%u, %u) x %d threads, dynamic smem %zu B; kernel: %d regs, static smem %zu B, "
+                 "local %zu B, max threads %d, max dynamic smem %d B",
+                 grid.x, grid.y, k.threads, k.smem, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes,
+                 fa.maxThreadsPerBlock, fa.maxDynamicSharedSizeBytes);
+        g_launch_detail = buf;
+    }
     return (int)e;
 }
 

@@ -50,6 +50,7 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st);
 
 // Launch one specialised sweep.
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream);
+const std::string& jit_last_launch_detail();  // configuration of the last failed jit_launch
 
 // Specialised H|psi> + energy kernel of one observable (qf_hpsi); at most
 // kJitHpsiMaxTerms terms (larger sums keep the AOT hpsi_kernel).

@@ -269,3 +269,25 @@ def test_pauli_sum_to_coo_matches_oracle(ctx):
         qf.pauli_sum_to_coo(qf.tfim_terms(qf.build_lattice("chain", [27], [False]), 1.0))
     empty = qf.PauliSum(3)
     assert qf.pauli_sum_to_coo(empty).nnz() == 0
+
+
+def test_randomized_stress_regressions(ctx):
+    """Cases found by tools/stress_parity.py: stress_case6 (c128 adjoint kernel whose
+    static tables pushed static + dynamic shared memory past the 48 KB default)
+    and stress_case138 (deep su4-rich circuit, the c64 worst case: float32
+    arithmetic itself, the generic kernels agree)."""
+    import os
+    here = os.path.join(os.path.dirname(__file__), "cases")
+    for name, prec, tol in [("stress_case6.npz", "c128", 1e-10), ("stress_case6.npz", "c64", 1e-5),
+                            ("stress_case138.npz", "c128", 1e-10), ("stress_case138.npz", "c64", 5e-5)]:
+        d = np.load(os.path.join(here, name), allow_pickle=True)
+        n, P = int(d["n"]), int(d["P"])
+        ops = [tuple(o) for o in d["ops"]]
+        mats = d["mats"] if d["mats"].size else None
+        h = po.Hamil(n, d["codes"], d["wr"] + 1j * d["wi"])
+        E_ref, G_ref = po.energy_grad_batch(po.Ansatz(n, ops, P, mats), d["th"], h, mode="adjoint")
+        obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
+        E, G = engine.energy_grad_batch(ctx, engine.Program(ctx, n, ops, P, prec, mats), obs, d["th"])
+        # absolute floor: these random Hamiltonians can vanish on the state (E, G ~ 1e-17)
+        scale = max(np.abs(E_ref).max(), np.abs(G_ref).max(), 1e-3 * np.abs(h.wr + 1j * h.wi).sum())
+        assert max(np.abs(E - E_ref).max(), np.abs(G - G_ref).max()) <= tol * scale, (name, prec)
