@@ -141,3 +141,36 @@ def test_adam_step_mirror():
     th = np.zeros(2)
     qf.adam_step(st, th, np.array([0.3, -7.0]), 0.05)
     assert th[0] == pytest.approx(-0.05, rel=1e-6) and th[1] == pytest.approx(0.05, rel=1e-6)
+
+
+def test_kraus_channels_and_noise_rules():
+    """noise.cpp:10-145 restated in qforge.py: completeness, operator counts and
+    shapes, arity / range validation, rule matching (gate name, wire tuple,
+    predicate, arity) in insertion order."""
+    from paper_2602_14167_b200 import qforge as qf
+    for ch, count in [(qf.depolarizing_channel(0.05, 1), 4), (qf.depolarizing_channel(0.05, 2), 16),
+                      (qf.depolarizing_channel(0.0, 1), 1), (qf.amplitude_damping_channel(0.3), 2),
+                      (qf.phase_damping_channel(0.4), 2), (qf.reset_channel(0.2), 3),
+                      (qf.thermal_relaxation_channel(0.1, 0.2), 4)]:
+        assert len(ch.operators) == count and ch.completeness_defect() < 1e-12
+        assert all(k.shape == (1 << ch.arity, 1 << ch.arity) for k in ch.operators)
+    # depolarizing: site 0 is the least significant Kronecker factor (noise.cpp:44-55)
+    X = np.array([[0, 1], [1, 0]])
+    d2 = qf.depolarizing_channel(0.3, 2).operators
+    assert np.allclose(d2[1], np.sqrt(0.3 / 15) * np.kron(np.eye(2), X))
+    for bad in (lambda: qf.depolarizing_channel(1.5), lambda: qf.depolarizing_channel(0.1, 4),
+                lambda: qf.amplitude_damping_channel(-0.1), lambda: qf.reset_channel(2.0)):
+        with pytest.raises(ValueError):
+            bad()
+    conf = qf.NoiseConf()
+    dep2 = qf.depolarizing_channel(0.05, 2)
+    conf.attach("cx", dep2)
+    conf.attach("", qf.amplitude_damping_channel(0.1))
+    conf.attach_on_wires("h", [1], qf.phase_damping_channel(0.2))
+    conf.attach_predicate(lambda op: op.wires == [0], qf.reset_channel(0.1))
+    with pytest.raises(ValueError, match="arity"):
+        conf.attach_on_wires("cx", [0], dep2)
+    c = qf.Circuit(3)
+    c.h(0).h(1).cx(0, 1)
+    names = [[ch.name for ch in conf.match(op)] for op in c.ops]
+    assert names == [["amplitude_damping", "reset"], ["amplitude_damping", "phase_damping"], ["depolarizing"]]

@@ -362,3 +362,26 @@ def test_oracle_coo_matches_dense():
         same = r[1:] == r[:-1]
         assert np.all(c[1:][same] > c[:-1][same])
         assert np.all(v != 0)
+
+
+def test_trajectory_restatements_properties():
+    """Oracle restatements of the trajectory callers (oracle/pyoracle.py): haar_su4
+    is unitary with det 1 (circuit.cpp:472-489); MIPT with p = 1 or depth 0 has
+    zero half-chain entropy, a Bell pair has one bit; shadows of |+++> in the X
+    basis are all zeros and Z-basis samples of |0..0> are all zeros
+    (test_shadows.cpp:101-118)."""
+    import numpy as np
+    for s in range(5):
+        u = po.haar_su4(po.Rng(s))
+        assert np.abs(u.conj().T @ u - np.eye(4)).max() < 1e-12
+        assert abs(np.linalg.det(u) - 1.0) < 1e-12
+    assert np.abs(po.mipt_haar(6, 4, 1.0, 3, 9)).max() < 1e-12
+    assert np.abs(po.mipt_haar(6, 0, 0.5, 2, 9)).max() < 1e-12
+    bell = np.zeros(4, complex)
+    bell[0] = bell[3] = np.sqrt(0.5)
+    assert abs(po.subsystem_entropy_half(bell, 2) - 1.0) < 1e-12
+    plus = np.full(8, np.sqrt(1 / 8), complex)
+    assert not po.shadow_snapshots(plus, 3, [[1, 1, 1]] * 10, np.linspace(0, 0.99, 10)).any()
+    zero = np.zeros(8, complex)
+    zero[0] = 1
+    assert not po.shadow_snapshots(zero, 3, [[3, 3, 3]] * 10, np.linspace(0, 0.99, 10)).any()
