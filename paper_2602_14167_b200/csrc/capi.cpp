@@ -144,11 +144,6 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.write_lam = grads ? 1 : 0;
     ha.use_imag = 0;
     ha.epart = (double*)ctx->epart.p;
-    if (prog->use_jit && od->hj_state == 0 && !(std::getenv("QF_JIT_HPSI") && std::getenv("QF_JIT_HPSI")[0] == '0')) {
-        std::string err;
-        od->hj_state = ((int)od->plan.terms.size() <= kJitHpsiMaxTerms && jit_build_hpsi(od->plan, prec, od->hj, err))
-                           ? 1 : -1;
-    }
     if (od->hj_state == 1)
         QF_CUDA((cudaError_t)jit_launch_hpsi(od->hj, ha, tiles_h, bc, s));
     else
@@ -216,6 +211,17 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         tock(6, 3);
     }
     return QF_OK;
+}
+
+// Resolve the observable's specialised H|psi> kernel (compiled at most once;
+// outside any stream capture).
+void ensure_hpsi_kernel(qf_program* prog, ObsDev* od, int prec) {
+    if (prog->use_jit && od->hj_state == 0 && !(std::getenv("QF_JIT_HPSI") && std::getenv("QF_JIT_HPSI")[0] == '0')) {
+        std::string err;
+        od->hj_state = ((int)od->plan.terms.size() <= kJitHpsiMaxTerms && jit_build_hpsi(od->plan, prec, od->hj, err))
+                           ? 1 : -1;
+    }
+    if (!prog->use_jit && od->hj_state == 0) od->hj_state = -1;
 }
 
 // Evaluate rows [0, batch) of device thetas into device outputs (chunked).
@@ -286,6 +292,45 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
             QF_CUDA(cudaMemcpyAsync(ctx->zero_init.p, one, 8, cudaMemcpyHostToDevice, ctx->stream));
         }
         QF_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    ensure_hpsi_kernel(prog, od, prec);
+    // Single-chunk evaluations (small states / batches are launch bound) run as a
+    // CUDA graph: captured on first use, replayed while everything it captured is
+    // unchanged (program and observable identity, plan buffers, work buffers,
+    // argument pointers, batch).
+    static const bool graphs_off = std::getenv("QF_GRAPHS") && std::getenv("QF_GRAPHS")[0] == '0';
+    if (bc >= batch && !ctx->timing && !graphs_off) {
+        const std::vector<const void*> key = {
+            (const void*)prog->uid, (const void*)obs->uid, od, od->groups.p, od->terms.p, (const void*)(intptr_t)od->hj_state,
+            od_im, (const void*)(intptr_t)batch, d_thetas, d_E, d_Eim, d_G, ctx->psi.p, ctx->lam.p, ctx->tap_part.p,
+            ctx->tapsum.p, ctx->epart.p, ctx->gmat.p, ctx->zero_init.p, prog->init.p};
+        if (ctx->graph_exec && key == ctx->graph_key) {
+            QF_CUDA(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+            ctx->launches += ctx->graph_launches;
+            return QF_OK;
+        }
+        if (key != ctx->graph_nocapture_key) {
+            const long long l0 = ctx->launches;
+            QF_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            rc = eval_chunk(ctx, prog, od, 0, batch, d_thetas, d_E, d_Eim, d_G, od_im);
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+            cudaGraphExec_t exec = nullptr;
+            if (!rc && ce == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+                cudaGraphDestroy(g);
+                if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+                ctx->graph_exec = exec;
+                ctx->graph_key = key;
+                ctx->graph_launches = ctx->launches - l0;
+                QF_CUDA(cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+                return QF_OK;
+            }
+            // not capturable here: run uncaptured (and do not retry this configuration)
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            ctx->launches = l0;
+            ctx->graph_nocapture_key = key;
+        }
     }
     for (long long b0 = 0; b0 < batch; b0 += bc) {
         const int c = (int)std::min<long long>(bc, batch - b0);
@@ -404,6 +449,7 @@ int qf_ctx_destroy(qf_ctx* c) {
         b->release();
     c->pin.release();
     for (auto& ev : c->ev_pool) cudaEventDestroy(ev);
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
     cudaStreamDestroy(c->stream);
     delete c;
     return QF_OK;
@@ -518,6 +564,8 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
             return set_err(QF_ERUNTIME, "JIT required but unavailable: " + why);
         }
     }
+    static std::atomic<uint64_t> next_prog_uid{1};
+    p->uid = next_prog_uid++;
     *out = p;
     return QF_OK;
 }

@@ -168,6 +168,7 @@ struct qf_program {
     bool use_jit = false;
     JitPass jf, jb;
     JitStats jst;
+    uint64_t uid = 0;  // identity for the context's graph cache
 };
 
 struct ObsDev {
@@ -214,6 +215,12 @@ struct qf_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<std::pair<size_t, int>> pending;  // (start event index, class); end = start + 1
+    // CUDA graph of the last single-chunk evaluation, replayed while nothing it
+    // captured (program, observable plan, buffers, batch) changes
+    std::vector<const void*> graph_key;
+    std::vector<const void*> graph_nocapture_key;  // configuration whose capture failed
+    cudaGraphExec_t graph_exec = nullptr;
+    long long graph_launches = 0;
 };
 
 namespace qfcapi {
