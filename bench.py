@@ -137,6 +137,21 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_compute(cfg_name, cls_name, batch):
+    """FP32-pipe view of the same committed capture (the sweeps are FMA-pipe bound,
+    not HBM bound), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            e = json.load(f).get(cfg_name, {}).get(cls_name)
+    except Exception:
+        return None
+    if not e or e.get("batch") != batch or "sm__pipe_fma_cycles_active_pct" not in e:
+        return None
+    return {"fma_pipe_active_pct": e["sm__pipe_fma_cycles_active_pct"], "issue_active_pct": e.get("smsp__issue_active_pct"),
+            "top_stall": e.get("top_stall"), "source": e.get("source")}
+
+
 def ncu_traffic(cfg_name, cls_name, batch):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel class,
     from the committed `ncu --set full` capture (profiles/ncu_traffic.json) of the
@@ -359,6 +374,7 @@ def main():
     per_launch = cls_bytes[dom] / max(1, cls_launches[dom])
     roofline = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(cfg_name, names[dom], B),
+                "compute": ncu_compute(cfg_name, names[dom], B),
                 "algorithmic_bytes_per_launch": per_launch,
                 "avg_launch_ms": cls_ms[dom] / max(1, cls_launches[dom]), "peak_source": peak_src,
                 "classes": {names[i]: {"ms": cls_ms[i], "launches": cls_launches[i], "bytes": cls_bytes[i],
