@@ -65,9 +65,13 @@ struct BitSrc {
 
 }  // namespace
 
-bool jit_pipe_mode() {
+// Persistent cp.async double-buffered variant: QF_JIT_PIPE=1 for every sweep,
+// QF_JIT_PIPE=light for sweeps of at most two phases (HBM-latency bound).
+bool jit_pipe_mode(const PassPlan& pass, int si) {
     const char* e = std::getenv("QF_JIT_PIPE");
-    return e && e[0] == '1';
+    if (!e) return false;
+    if (e[0] == '1') return true;
+    return std::strcmp(e, "light") == 0 && pass.sweeps[si].n_phases <= 2;
 }
 
 // Gradient taps are staged per thread in shared memory ([slots][T] reals) and
@@ -84,7 +88,7 @@ size_t jit_smem_bytes(const ProgramPlan& P, const PassPlan& pass, int si, bool b
     const int T = 1 << (sw.k - sw.R);
     const int nwarps = (T + 31) / 32;
     (void)nwarps;
-    size_t b = ((size_t)1 << sw.k) * vs * (bwd ? 2 : 1) * (jit_pipe_mode() ? 2 : 1);
+    size_t b = ((size_t)1 << sw.k) * vs * (bwd ? 2 : 1) * (jit_pipe_mode(pass, si) ? 2 : 1);
     b += (size_t)((sw.n_mat + 1) & ~1) * vs;
     b += (size_t)jit_tap_stage(P, pass, si, bwd) * T * (vs / 2);
     return b;
@@ -110,7 +114,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         const char* e = std::getenv("QF_JIT_FUSE");
         return !(e && e[0] == '0');
     }();
-    const bool pipe = jit_pipe_mode();
+    const bool pipe = jit_pipe_mode(pass, si);
     Out o;
     if (pipe) o.s += "// qf-option: pipelined\n";
     o.s += kPrelude;
@@ -1207,7 +1211,7 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
                 return false;
             }
         }
-        jk.pipe = jit_pipe_mode();
+        jk.pipe = jit_pipe_mode(*jb.pass, jb.si);
         if (jk.pipe) {
             int dev = 0, sms = 148, per = 1;
             cudaGetDevice(&dev);

@@ -23,7 +23,7 @@ struct JitKernel {
     int ctas = 0;            // resident CTAs (pipe mode grid)
 };
 
-bool jit_pipe_mode();
+bool jit_pipe_mode(const PassPlan& pass, int si);
 
 struct JitPass {
     std::vector<JitKernel> sweeps;
