@@ -140,6 +140,17 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        if self._nv is not None and not self.samples:  # regions shorter than one sampling period
+            try:
+                nv, hdl = self._nv
+                bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+                self.samples.append([str(nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)),
+                                     str(nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)), "",
+                                     *["Active" if r & b else "Not Active" for b in bits]])
+            except Exception:
+                pass
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
