@@ -7,6 +7,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2602_14167_b200 import engine  # noqa: E402
 
+mode = os.environ.get("C1_MODE", "plain")
+if mode != "plain":
+    import torch
+    if mode in ("cuda", "device"):
+        torch.zeros(1, device="cuda")
+    if mode == "device":
+        torch.cuda.set_device(0)
 cfg = bench.CONFIGS["C1"]
 ops, P = bench.hea_template(cfg["n"], cfg["layers"])
 h = bench.hamiltonian("C1", cfg)
@@ -23,7 +30,7 @@ for rep in range(3):
     dt = (time.perf_counter() - t0) / 200
     ctx.reset_stats()
     engine.energy_grad_batch(ctx, prog, obs, th)
-    print(f"QF_GRAPHS={os.environ.get('QF_GRAPHS', '1')} {dt*1e6:.1f} us/call  {cfg['batch']/dt:.0f} evals/s  "
+    print(f"mode={mode} QF_GRAPHS={os.environ.get('QF_GRAPHS', '1')} {dt*1e6:.1f} us/call  {cfg['batch']/dt:.0f} evals/s  "
           f"launches/call={ctx.stats()[0]}", flush=True)
 ctx.set_timing(True)
 ctx.reset_stats()
