@@ -356,13 +356,23 @@ def main():
                 engine.energy_grad_batch_device(ctx, prog, obs, th_d, E_d, G_d)
                 dist.all_reduce(out_d)
 
-    # ---- device-resident value ----
-    # pre-warm: >= PREWARM_S of untimed evaluation before the W warm-up steps, so
-    # small configurations (microsecond calls) run at ramped-up clocks
-    t_pre = time.perf_counter()
-    while time.perf_counter() - t_pre < PREWARM_S:
-        step_device()
+    def agreed_count(seconds, one_call):
+        """iterations covering `seconds`, identical on every rank (the calls run collectives)"""
+        t0 = time.perf_counter()
+        one_call()
         torch.cuda.synchronize(dev)
+        dt = max(time.perf_counter() - t0, 1e-6)
+        c = torch.tensor([min(100000, int(seconds / dt) + 1)], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        return int(c.item())
+
+    # ---- device-resident value ----
+    # pre-warm: ~PREWARM_S of untimed evaluation before the W warm-up steps, so
+    # small configurations (microsecond calls) run at ramped-up clocks
+    for _ in range(agreed_count(PREWARM_S, step_device)):
+        step_device()
+    torch.cuda.synchronize(dev)
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize(dev)
@@ -397,12 +407,11 @@ def main():
     # ---- end to end through the public host-buffer call ----
     E_h = np.empty(B)
     G_h = np.empty((B, P))
-    t_pre = time.perf_counter()
-    while True:  # >= 2 calls and >= PREWARM_S / 2 untimed (clock ramp, graph capture)
-        for _ in range(2):
-            engine.energy_grad_batch(ctx, prog, obs, thetas)
-        if time.perf_counter() - t_pre >= PREWARM_S / 2:
-            break
+    def e2e_call():
+        engine.energy_grad_batch(ctx, prog, obs, thetas)
+
+    for _ in range(max(2, agreed_count(PREWARM_S / 2, e2e_call))):  # clock ramp, graph capture
+        e2e_call()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
