@@ -144,6 +144,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.write_lam = grads ? 1 : 0;
     ha.use_imag = 0;
     ha.epart = (double*)ctx->epart.p;
+    ha.prefetch = od->plan.terms.size() <= 4 * std::max<size_t>(1, od->plan.groups.size()) ? 1 : 0;
     if (od->hj_state == 1)
         QF_CUDA((cudaError_t)jit_launch_hpsi(od->hj, ha, tiles_h, bc, s));
     else

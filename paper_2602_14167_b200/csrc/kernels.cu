@@ -33,8 +33,20 @@ __device__ __forceinline__ double2 hp_iaxpy(double k, double2 s, double2 acc) {
     return make_double2(fma(-k, s.y, acc.x), fma(k, s.x, acc.y));
 }
 
+// cp.async of one amplitude into shared memory (8 B c64 via L1, 16 B c128 via L2)
+__device__ __forceinline__ void hp_cp_async(float2* dst, const float2* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void hp_cp_async(double2* dst, const double2* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+
 // ---------------------------------------------------------------------------
-// lambda = H psi and E = Re<psi|lambda>, output-stationary per tile
+// lambda = H psi and E = Re<psi|lambda>, output-stationary per tile.  Partner
+// tiles (flip groups above the tile) are double-buffered: the next group's tile
+// streams in with cp.async while the current group's terms are applied.
 // ---------------------------------------------------------------------------
 template <typename RT, int NA>
 __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
@@ -44,8 +56,8 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
     const int tid = threadIdx.x;
     const uint32_t TS = 1u << a.kh;
     V* own = reinterpret_cast<V*>(smem_raw);
-    V* part = own + TS;
-    double* red = reinterpret_cast<double*>(part + TS);
+    V* const part = own + TS;  // partner buffer(s): part, and part + TS with a.prefetch
+    double* red = reinterpret_cast<double*>(own + (a.prefetch ? 3 : 2) * TS);
     const uint32_t tile = blockIdx.x;
     const int b = blockIdx.y;
     const size_t N = size_t(1) << a.n;
@@ -62,11 +74,33 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
         acc[i].x = acc[i].y = RT(0);
         dg[i] = RT(0);
     }
+    auto next_outer = [&](int from) {
+        while (from < a.n_groups && a.groups[from].f_out == 0) ++from;
+        return from;
+    };
+    auto prefetch = [&](int gi, V* buf) {
+        const V* pp = ps + (base ^ a.groups[gi].f_out);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) hp_cp_async(buf + tid + T * i, pp + tid + T * i);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int k = 0;  // outer groups seen
+    const int first = next_outer(0);
+    if (a.prefetch && first < a.n_groups) prefetch(first, part);
     __syncthreads();
     for (int gi = 0; gi < a.n_groups; ++gi) {
         const DevGroup g = a.groups[gi];
         const V* src = own;
-        if (g.f_out) {
+        if (g.f_out && a.prefetch) {
+            // this group's tile (buffer k & 1) has landed for every thread, and every
+            // thread is done with buffer (k + 1) & 1 (the previous outer group)
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            __syncthreads();
+            const int nn = next_outer(gi + 1);
+            if (nn < a.n_groups) prefetch(nn, part + TS * ((k + 1) & 1));
+            src = part + TS * (k & 1);
+            ++k;
+        } else if (g.f_out) {  // compute-heavy groups: plain staged load
             __syncthreads();
             const V* pp = ps + (base ^ g.f_out);
 #pragma unroll
@@ -232,7 +266,7 @@ cudaError_t launch_sweep(int prec, bool bwd, const SweepArgs& a, int batch, int 
 template <typename RT, int NA>
 static cudaError_t launch_hpsi_t(const HArgs& a, int batch, int T, cudaStream_t s) {
     const size_t vs = sizeof(RT) * 2;
-    const size_t smem = ((size_t)2 << a.kh) * vs + 8 * 8;
+    const size_t smem = ((size_t)(a.prefetch ? 3 : 2) << a.kh) * vs + 8 * 8;
     auto kern = hpsi_kernel<RT, NA>;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {

@@ -140,6 +140,7 @@ struct HArgs {
     int write_lam;
     int use_imag;
     double* epart;             // [B][tiles]
+    int prefetch;              // generic kernel: double-buffer partner tiles (few terms per group)
 };
 
 // Kernel arguments of one sweep launch (AOT interpreter and NVRTC kernels).
