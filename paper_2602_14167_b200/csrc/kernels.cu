@@ -33,6 +33,77 @@ __device__ __forceinline__ double2 hp_iaxpy(double k, double2 s, double2 acc) {
     return make_double2(fma(-k, s.y, acc.x), fma(k, s.x, acc.y));
 }
 
+// Walsh rows: bit i of c_hp_walsh[z] = parity(i & z), i, z < 16
+__constant__ uint16_t c_hp_walsh[16] = {0x0000, 0xaaaa, 0xcccc, 0x6666, 0xf0f0, 0x5a5a, 0x3c3c, 0x9696,
+                                        0xff00, 0x55aa, 0x33cc, 0x9966, 0x0ff0, 0xa55a, 0xc33c, 0x6996};
+
+// k with its sign flipped when bit i of M is set (sign-bit xor, no select)
+__device__ __forceinline__ float hp_sgn(float k, uint32_t M, int i) {
+    return __int_as_float(__float_as_int(k) ^ (int)((M << (31 - i)) & 0x80000000u));
+}
+__device__ __forceinline__ double hp_sgn(double k, uint32_t M, int i) {
+    return __hiloint2double(__double2hiint(k) ^ (int)((M << (31 - i)) & 0x80000000u), __double2loint(k));
+}
+
+// one off-diagonal term on the NA amplitudes of a thread: slot i reads the
+// partner thread's slot i ^ FH (compile-time offsets off sb)
+template <int NA, int TPB, int FH, bool IM, typename V, typename RT>
+__device__ __forceinline__ void hp_term(V (&acc)[NA], const V* sb, RT k, uint32_t M) {
+    constexpr int TT = NA > 1 ? TPB : 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        const V s = sb[TT * (i ^ FH)];
+        const RT ki = hp_sgn(k, M, i);
+        acc[i] = IM ? hp_iaxpy(ki, s, acc[i]) : hp_axpy(ki, s, acc[i]);
+    }
+}
+
+// the same with the slot permutation applied to the offsets (no dispatch)
+template <int NA, int TPB, bool IM, typename V, typename RT>
+__device__ __forceinline__ void hp_term_xor(int fh, V (&acc)[NA], const V* sb, RT k, uint32_t M) {
+    constexpr int TT = NA > 1 ? TPB : 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        const V s = sb[TT * (i ^ fh)];
+        const RT ki = hp_sgn(k, M, i);
+        acc[i] = IM ? hp_iaxpy(ki, s, acc[i]) : hp_axpy(ki, s, acc[i]);
+    }
+}
+
+#define QF_HP_CASE(c) \
+    case c:           \
+        if constexpr (c < NA) hp_term<NA, TPB, c, IM>(acc, sb, k, M); \
+        break;
+template <int NA, int TPB, bool IM, typename V, typename RT>
+__device__ __forceinline__ void hp_term_sw(int fh, V (&acc)[NA], const V* sb, RT k, uint32_t M) {
+    switch (fh) {
+        QF_HP_CASE(0) QF_HP_CASE(1) QF_HP_CASE(2) QF_HP_CASE(3) QF_HP_CASE(4) QF_HP_CASE(5)
+        QF_HP_CASE(6) QF_HP_CASE(7) QF_HP_CASE(8) QF_HP_CASE(9) QF_HP_CASE(10) QF_HP_CASE(11)
+        QF_HP_CASE(12) QF_HP_CASE(13) QF_HP_CASE(14) QF_HP_CASE(15)
+        default: break;
+    }
+}
+#undef QF_HP_CASE
+
+// the fields of one term the H|psi> loop needs (coefficients already picked by use_imag)
+struct HpTerm {
+    int32_t kind, yodd;
+    uint32_t f_in, z, fz_par;
+    double cr, ci;
+};
+__device__ __forceinline__ HpTerm hp_load_term(const HArgs& a, int t) {
+    const DevTerm& d = a.terms[t];
+    HpTerm h;
+    h.kind = d.kind;
+    h.yodd = d.yodd;
+    h.f_in = d.f_in;
+    h.z = d.z;
+    h.fz_par = d.fz_par;
+    h.cr = a.use_imag ? d.ci_re : d.c_re;
+    h.ci = a.use_imag ? d.ci_im : d.c_im;
+    return h;
+}
+
 // cp.async of one amplitude into shared memory (8 B c64 via L1, 16 B c128 via L2)
 __device__ __forceinline__ void hp_cp_async(float2* dst, const float2* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -48,9 +119,12 @@ __device__ __forceinline__ void hp_cp_async(double2* dst, const double2* src) {
 // tiles (flip groups above the tile) are double-buffered: the next group's tile
 // streams in with cp.async while the current group's terms are applied.
 // ---------------------------------------------------------------------------
-template <typename RT, int NA>
-__global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
+// TPB threads (compile-time, = blockDim.x when NA > 1) x NA amplitudes per tile
+template <typename RT, int NA, int TPB, bool SW>
+__global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
     using V = typename CxT<RT>::T;
+    constexpr int kLgT = TPB == 256 ? 8 : TPB == 128 ? 7 : 0;
+    static_assert(NA == 1 || kLgT > 0, "hpsi: TPB must be 128 or 256");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int T = blockDim.x;
     const int tid = threadIdx.x;
@@ -64,13 +138,12 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
     const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)b * N;
     const uint32_t base = tile << a.kh;
 
-    V po[NA], acc[NA];
+    V acc[NA];  // the own amplitudes stay in shared memory (registers go to occupancy)
     RT dg[NA];
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
         const uint32_t p = tid + (uint32_t)T * i;
-        po[i] = ps[base + p];
-        own[p] = po[i];
+        own[p] = ps[base + p];
         acc[i].x = acc[i].y = RT(0);
         dg[i] = RT(0);
     }
@@ -108,36 +181,38 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
             __syncthreads();
             src = part;
         }
+        // the next term's fields load while this term is applied
+        HpTerm nx;
+        if (g.term_begin < g.term_end) nx = hp_load_term(a, g.term_begin);
         for (int t = g.term_begin; t < g.term_end; ++t) {
-            const DevTerm d = a.terms[t];
-            const RT cr = (RT)(a.use_imag ? d.ci_re : d.c_re);
-            const RT ci = (RT)(a.use_imag ? d.ci_im : d.c_im);
+            const HpTerm d = nx;
+            if (t + 1 < g.term_end) nx = hp_load_term(a, t + 1);
+            const RT cr = (RT)d.cr;
+            const RT ci = (RT)d.ci;
             const uint32_t zlo = d.z & (TS - 1);
             const uint32_t cpar = (__popc(base & d.z) ^ d.fz_par) & 1;
+            // amplitude i of this thread is p = tid + TPB i, so parity(p & z) =
+            // parity(tid & z) ^ parity(i & z_hi): one Walsh row covers all NA signs
+            const uint32_t s0 = (__popc(tid & zlo) ^ cpar) & 1;
+            uint32_t M = (NA > 1 ? (uint32_t)c_hp_walsh[(zlo >> kLgT) & (NA - 1)] : 0u) ^ (0u - s0);
+            if (d.kind == TK_FLIP) M = 0;
             if (d.kind == TK_DIAG) {
 #pragma unroll
-                for (int i = 0; i < NA; ++i) {
-                    const uint32_t p = tid + (uint32_t)T * i;
-                    const uint32_t par = (__popc(p & zlo) ^ cpar) & 1;
-                    dg[i] += par ? -cr : cr;
-                }
-            } else if (!d.yodd) {
-                // real coefficient (Re(w) i^y with y even): acc += (+-cr) src
-#pragma unroll
-                for (int i = 0; i < NA; ++i) {
-                    const uint32_t p = tid + (uint32_t)T * i;
-                    RT k = cr;
-                    if (d.kind == TK_GEN && ((__popc(p & zlo) ^ cpar) & 1)) k = -k;
-                    acc[i] = hp_axpy(k, src[p ^ d.f_in], acc[i]);
-                }
+                for (int i = 0; i < NA; ++i) dg[i] += hp_sgn(cr, M, i);
             } else {
-                // imaginary coefficient (y odd): acc += (+-ci) i src
-#pragma unroll
-                for (int i = 0; i < NA; ++i) {
-                    const uint32_t p = tid + (uint32_t)T * i;
-                    RT k = ci;
-                    if ((__popc(p & zlo) ^ cpar) & 1) k = -k;
-                    acc[i] = hp_iaxpy(k, src[p ^ d.f_in], acc[i]);
+                // partner of amplitude i: thread tid ^ flo, register slot i ^ fh
+                const int fh = NA > 1 ? (int)(d.f_in >> kLgT) : 0;
+                const V* sb = src + (tid ^ (d.f_in & (uint32_t)(T - 1)));
+                if (SW) {
+                    if (!d.yodd)  // real coefficient (Re(w) i^y with y even): acc += (+-cr) src
+                        hp_term_sw<NA, TPB, false>(fh, acc, sb, cr, M);
+                    else  // imaginary coefficient (y odd): acc += (+-ci) i src
+                        hp_term_sw<NA, TPB, true>(fh, acc, sb, ci, M);
+                } else {
+                    if (!d.yodd)
+                        hp_term_xor<NA, TPB, false>(fh, acc, sb, cr, M);
+                    else
+                        hp_term_xor<NA, TPB, true>(fh, acc, sb, ci, M);
                 }
             }
         }
@@ -145,9 +220,10 @@ __global__ void __launch_bounds__(256) hpsi_kernel(const HArgs a) {
     double e = 0;
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
-        acc[i].x = fma(dg[i], po[i].x, acc[i].x);
-        acc[i].y = fma(dg[i], po[i].y, acc[i].y);
-        e += (double)po[i].x * (double)acc[i].x + (double)po[i].y * (double)acc[i].y;
+        const V po = own[tid + T * i];
+        acc[i].x = fma(dg[i], po.x, acc[i].x);
+        acc[i].y = fma(dg[i], po.y, acc[i].y);
+        e += (double)po.x * (double)acc[i].x + (double)po.y * (double)acc[i].y;
     }
     if (a.write_lam) {
         V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * N;
@@ -263,11 +339,11 @@ cudaError_t launch_sweep(int prec, bool bwd, const SweepArgs& a, int batch, int 
     return bwd ? launch_sweep_f32_bwd(a, batch, smem, s) : launch_sweep_f32_fwd(a, batch, smem, s);
 }
 
-template <typename RT, int NA>
+template <typename RT, int NA, int TPB, bool SW>
 static cudaError_t launch_hpsi_t(const HArgs& a, int batch, int T, cudaStream_t s) {
     const size_t vs = sizeof(RT) * 2;
     const size_t smem = ((size_t)(a.prefetch ? 3 : 2) << a.kh) * vs + 8 * 8;
-    auto kern = hpsi_kernel<RT, NA>;
+    auto kern = hpsi_kernel<RT, NA, TPB, SW>;
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -279,16 +355,23 @@ static cudaError_t launch_hpsi_t(const HArgs& a, int batch, int T, cudaStream_t 
     return cudaGetLastError();
 }
 
+// 16 amplitudes per thread from 2048-amplitude tiles up (the per-term setup is
+// amortised over NA amplitudes), 256 threads below
 template <typename RT>
 static cudaError_t dispatch_hpsi(const HArgs& a, int batch, cudaStream_t s) {
     const int TS = 1 << a.kh;
+    // complex128: runtime slot offsets (no per-term dispatch; branch resolution
+    // stalled the FP64 loop); complex64: the jump-table dispatch with immediate
+    // offsets wins (C5 193 vs 216 ms, C4 2.83 vs 3.19 s per launch, measured)
+    constexpr bool SW = sizeof(RT) == 4;
+    if (TS == 2048) return launch_hpsi_t<RT, 16, 128, SW>(a, batch, 128, s);
     const int T = TS < 256 ? TS : 256;
     switch (TS / T) {
-        case 1: return launch_hpsi_t<RT, 1>(a, batch, T, s);
-        case 2: return launch_hpsi_t<RT, 2>(a, batch, T, s);
-        case 4: return launch_hpsi_t<RT, 4>(a, batch, T, s);
-        case 8: return launch_hpsi_t<RT, 8>(a, batch, T, s);
-        case 16: return launch_hpsi_t<RT, 16>(a, batch, T, s);
+        case 1: return launch_hpsi_t<RT, 1, 256, SW>(a, batch, T, s);
+        case 2: return launch_hpsi_t<RT, 2, 256, SW>(a, batch, T, s);
+        case 4: return launch_hpsi_t<RT, 4, 256, SW>(a, batch, T, s);
+        case 8: return launch_hpsi_t<RT, 8, 256, SW>(a, batch, T, s);
+        case 16: return launch_hpsi_t<RT, 16, 256, SW>(a, batch, T, s);
         default: return cudaErrorInvalidValue;
     }
 }
