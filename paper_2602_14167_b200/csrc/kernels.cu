@@ -45,6 +45,13 @@ __device__ __forceinline__ double hp_sgn(double k, uint32_t M, int i) {
     return __hiloint2double(__double2hiint(k) ^ (int)((M << (31 - i)) & 0x80000000u), __double2loint(k));
 }
 
+// s with both parts negated when bit i of M is set
+__device__ __forceinline__ double2 hp_negv(double2 s, uint32_t M, int i) {
+    const int m = (int)((M << (31 - i)) & 0x80000000u);
+    return make_double2(__hiloint2double(__double2hiint(s.x) ^ m, __double2loint(s.x)),
+                        __hiloint2double(__double2hiint(s.y) ^ m, __double2loint(s.y)));
+}
+
 // one off-diagonal term on the NA amplitudes of a thread: slot i reads the
 // partner thread's slot i ^ FH (compile-time offsets off sb)
 template <int NA, int TPB, int FH, bool IM, typename V, typename RT>
@@ -53,18 +60,6 @@ __device__ __forceinline__ void hp_term(V (&acc)[NA], const V* sb, RT k, uint32_
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
         const V s = sb[TT * (i ^ FH)];
-        const RT ki = hp_sgn(k, M, i);
-        acc[i] = IM ? hp_iaxpy(ki, s, acc[i]) : hp_axpy(ki, s, acc[i]);
-    }
-}
-
-// the same with the slot permutation applied to the offsets (no dispatch)
-template <int NA, int TPB, bool IM, typename V, typename RT>
-__device__ __forceinline__ void hp_term_xor(int fh, V (&acc)[NA], const V* sb, RT k, uint32_t M) {
-    constexpr int TT = NA > 1 ? TPB : 0;
-#pragma unroll
-    for (int i = 0; i < NA; ++i) {
-        const V s = sb[TT * (i ^ fh)];
         const RT ki = hp_sgn(k, M, i);
         acc[i] = IM ? hp_iaxpy(ki, s, acc[i]) : hp_axpy(ki, s, acc[i]);
     }
@@ -181,7 +176,33 @@ __global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
             __syncthreads();
             src = part;
         }
-        // the next term's fields load while this term is applied
+        if constexpr (!SW) {
+            static_assert(sizeof(RT) == 8, "hpsi: the branch-free body is the complex128 one");
+            // complex128: one branch-free body for every term kind (diagonal terms
+            // are flip-0 terms, the coefficient is complex with one zero part), so
+            // consecutive terms interleave their shared-memory loads
+#pragma unroll 2
+            for (int t = g.term_begin; t < g.term_end; ++t) {
+                const HpTerm d = hp_load_term(a, t);
+                const uint32_t zlo = d.z & (TS - 1);
+                const uint32_t cpar = (__popc(base & d.z) ^ d.fz_par) & 1;
+                const uint32_t s0 = (__popc(tid & zlo) ^ cpar) & 1;
+                uint32_t M = (NA > 1 ? (uint32_t)c_hp_walsh[(zlo >> kLgT) & (NA - 1)] : 0u) ^ (0u - s0);
+                M = d.kind == TK_FLIP ? 0u : M;
+                const RT kr = d.yodd ? RT(0) : (RT)d.cr;
+                const RT ki = d.yodd ? (RT)d.ci : RT(0);
+                const int fh = NA > 1 ? (int)(d.f_in >> kLgT) : 0;
+                const V* sb = src + (tid ^ (d.f_in & (uint32_t)(T - 1)));
+                constexpr int TT = NA > 1 ? TPB : 0;
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const V sv = hp_negv(sb[TT * (i ^ fh)], M, i);
+                    acc[i].x = fma(kr, sv.x, fma(-ki, sv.y, acc[i].x));
+                    acc[i].y = fma(kr, sv.y, fma(ki, sv.x, acc[i].y));
+                }
+            }
+        } else {
+        // complex64: the next term's fields load while this term is applied
         HpTerm nx;
         if (g.term_begin < g.term_end) nx = hp_load_term(a, g.term_begin);
         for (int t = g.term_begin; t < g.term_end; ++t) {
@@ -203,18 +224,12 @@ __global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
                 // partner of amplitude i: thread tid ^ flo, register slot i ^ fh
                 const int fh = NA > 1 ? (int)(d.f_in >> kLgT) : 0;
                 const V* sb = src + (tid ^ (d.f_in & (uint32_t)(T - 1)));
-                if (SW) {
-                    if (!d.yodd)  // real coefficient (Re(w) i^y with y even): acc += (+-cr) src
-                        hp_term_sw<NA, TPB, false>(fh, acc, sb, cr, M);
-                    else  // imaginary coefficient (y odd): acc += (+-ci) i src
-                        hp_term_sw<NA, TPB, true>(fh, acc, sb, ci, M);
-                } else {
-                    if (!d.yodd)
-                        hp_term_xor<NA, TPB, false>(fh, acc, sb, cr, M);
-                    else
-                        hp_term_xor<NA, TPB, true>(fh, acc, sb, ci, M);
-                }
+                if (!d.yodd)  // real coefficient (Re(w) i^y with y even): acc += (+-cr) src
+                    hp_term_sw<NA, TPB, false>(fh, acc, sb, cr, M);
+                else  // imaginary coefficient (y odd): acc += (+-ci) i src
+                    hp_term_sw<NA, TPB, true>(fh, acc, sb, ci, M);
             }
+        }
         }
     }
     double e = 0;
@@ -360,9 +375,9 @@ static cudaError_t launch_hpsi_t(const HArgs& a, int batch, int T, cudaStream_t 
 template <typename RT>
 static cudaError_t dispatch_hpsi(const HArgs& a, int batch, cudaStream_t s) {
     const int TS = 1 << a.kh;
-    // complex128: runtime slot offsets (no per-term dispatch; branch resolution
-    // stalled the FP64 loop); complex64: the jump-table dispatch with immediate
-    // offsets wins (C5 193 vs 216 ms, C4 2.83 vs 3.19 s per launch, measured)
+    // complex128: the branch-free body with runtime slot offsets (C5: 171 ms per
+    // launch vs 216 with the dispatch); complex64: the jump-table dispatch with
+    // immediate offsets (C4: 2.82 s vs 2.93 branch-free, 3.19 runtime offsets)
     constexpr bool SW = sizeof(RT) == 4;
     if (TS == 2048) return launch_hpsi_t<RT, 16, 128, SW>(a, batch, 128, s);
     const int T = TS < 256 ? TS : 256;
