@@ -1,0 +1,5 @@
+set -x
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/v_smoke.log 2>&1; echo smoke=$? >> gpurun_out/v_smoke.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/v_pytest.log 2>&1; echo pytest=$? >> gpurun_out/v_pytest.log
+timeout 300 ./cpp/test_dropin > gpurun_out/v_dropin.log 2>&1; echo dropin=$? >> gpurun_out/v_dropin.log
+timeout 600 python bench.py > gpurun_out/v_bench.log 2>&1; echo bench=$? >> gpurun_out/v_bench.log
