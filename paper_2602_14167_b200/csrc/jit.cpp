@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -1149,27 +1150,53 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) jobs.push_back({&P, &P.bwd, (int)i, true, {}, {}, false});
     const std::string dir = cache_dir();
     mkdirs(dir);
+    // Several processes (one per GPU under torchrun) build the same program at
+    // once: each source is claimed across processes with an O_EXCL lock file
+    // next to its cache entry, so every kernel is compiled once per host and
+    // the other processes pick up the cubin.  Pass 1 compiles what this
+    // process claims and defers what another holds; pass 2 waits for those
+    // (bounded; a stale or abandoned claim is compiled here instead).
+    std::vector<std::string> srcs(jobs.size()), paths(jobs.size());
+    std::vector<size_t> deferred;
+    std::mutex def_mu;
+    auto publish = [&](size_t j) {
+        const std::string tmp = paths[j] + ".tmp" + std::to_string(getpid()) + "_" + std::to_string(j);
+        {
+            std::ofstream f(tmp, std::ios::binary);
+            f.write(jobs[j].cubin.data(), (std::streamsize)jobs[j].cubin.size());
+        }
+        rename(tmp.c_str(), paths[j].c_str());
+    };
     std::atomic<size_t> next{0};
     auto worker = [&] {
         for (;;) {
             size_t j = next.fetch_add(1);
             if (j >= jobs.size()) return;
             Job& jb = jobs[j];
-            const std::string src = jit_source(*jb.P, *jb.pass, jb.si, jb.bwd);
+            srcs[j] = jit_source(*jb.P, *jb.pass, jb.si, jb.bwd);
             char key[64];
-            snprintf(key, sizeof key, "%016llx_%d_%d", (unsigned long long)fnv1a(src), maj, min);
-            const std::string path = dir + "/" + key + ".cubin";
-            if (read_file(path, jb.cubin)) {
+            snprintf(key, sizeof key, "%016llx_%d_%d", (unsigned long long)fnv1a(srcs[j]), maj, min);
+            paths[j] = dir + "/" + key + ".cubin";
+            if (read_file(paths[j], jb.cubin)) {
                 jb.from_cache = true;
                 continue;
             }
-            if (!compile_one(src, jb.cubin, jb.err)) continue;
-            const std::string tmp = path + ".tmp" + std::to_string(getpid()) + "_" + std::to_string(j);
-            {
-                std::ofstream f(tmp, std::ios::binary);
-                f.write(jb.cubin.data(), (std::streamsize)jb.cubin.size());
+            const std::string lock = paths[j] + ".lock";
+            int fd = open(lock.c_str(), O_CREAT | O_EXCL | O_WRONLY, 0644);
+            if (fd < 0) {
+                struct stat stl;
+                const bool stale = stat(lock.c_str(), &stl) == 0 && time(nullptr) - stl.st_mtime > 300;
+                if (!stale) {
+                    std::lock_guard<std::mutex> lk(def_mu);
+                    deferred.push_back(j);
+                    continue;
+                }
             }
-            rename(tmp.c_str(), path.c_str());
+            if (compile_one(srcs[j], jb.cubin, jb.err)) publish(j);
+            if (fd >= 0) {
+                close(fd);
+                unlink(lock.c_str());
+            }
         }
     };
     unsigned nthr = std::thread::hardware_concurrency();
@@ -1177,6 +1204,36 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     nthr = std::max(1u, std::min<unsigned>(nthr, (unsigned)jobs.size()));
     std::vector<std::thread> pool;
     for (unsigned i = 0; i < nthr; ++i) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    pool.clear();
+    next = 0;
+    auto waiter = [&] {
+        for (;;) {
+            size_t d = next.fetch_add(1);
+            if (d >= deferred.size()) return;
+            const size_t j = deferred[d];
+            Job& jb = jobs[j];
+            const std::string lock = paths[j] + ".lock";
+            const auto t_wait = std::chrono::steady_clock::now();
+            for (;;) {
+                if (read_file(paths[j], jb.cubin)) {
+                    jb.from_cache = true;
+                    break;
+                }
+                struct stat stl;
+                const bool held = stat(lock.c_str(), &stl) == 0;
+                if (!held || std::chrono::steady_clock::now() - t_wait > std::chrono::seconds(600)) {
+                    // the holder finished without a cubin (compile error: reproduce it here) or is stuck
+                    if (read_file(paths[j], jb.cubin)) jb.from_cache = true;
+                    else if (compile_one(srcs[j], jb.cubin, jb.err)) publish(j);
+                    break;
+                }
+                std::this_thread::sleep_for(std::chrono::milliseconds(50));
+            }
+        }
+    };
+    nthr = std::max(1u, std::min<unsigned>(nthr, (unsigned)std::max<size_t>(1, deferred.size())));
+    for (unsigned i = 0; i < nthr && !deferred.empty(); ++i) pool.emplace_back(waiter);
     for (auto& t : pool) t.join();
     fwd.sweeps.assign(P.fwd.sweeps.size(), {});
     bwd.sweeps.assign(P.bwd.sweeps.size(), {});
