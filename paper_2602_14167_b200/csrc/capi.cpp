@@ -261,6 +261,16 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     const size_t per_entry = N * vs * (grads ? 2 : 1) + (grads ? (size_t)nt * tiles_b * 8 + (size_t)nt * 8 : 0) +
                              tiles_h * 8 + (size_t)(P.fwd.total_mat + P.bwd.total_mat) * vs;
     size_t budget = ctx->budget;
+    // The work buffers already hold the whole batch (a repeated call): one
+    // chunk, no device memory query (cudaMemGetInfo costs more than a small
+    // state's whole evaluation).
+    const size_t whole = (size_t)batch * N * vs;
+    const bool resident = !budget && batch <= 65535 && ctx->psi.cap >= whole &&
+                          (!grads || (ctx->lam.cap >= whole && ctx->tap_part.cap >= (size_t)batch * nt * tiles_b * 8 &&
+                                      ctx->tapsum.cap >= (size_t)batch * nt * 8)) &&
+                          ctx->epart.cap >= (size_t)batch * tiles_h * 8 &&
+                          ctx->gmat.cap >= (size_t)batch * (P.fwd.total_mat + P.bwd.total_mat) * vs;
+    if (resident) budget = per_entry * (size_t)batch;
     if (!budget) {
         size_t fr = 0, tot = 0;
         QF_CUDA(cudaMemGetInfo(&fr, &tot));
