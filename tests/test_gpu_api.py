@@ -328,3 +328,23 @@ def test_graph_replay_matches_uncaptured_path(ctx):
         ctx.set_timing(False)
     for (Eg, Gg), (Ep, Gp) in zip(graphed, plain + plain):
         assert np.array_equal(Eg, Ep) and np.array_equal(Gg, Gp)
+
+
+def test_batch_rows_independent_of_call_history(ctx):
+    """Repeated calls reuse the work buffers without re-querying device memory
+    when they already hold the batch; growing, shrinking and regrowing the batch
+    on one program must give every row bitwise the result of evaluating it alone."""
+    from paper_2602_14167_b200 import engine
+    from paper_2602_14167_b200.rng import RngStream
+    n = 9
+    _, ops, P = po.hea_template(n, 2)
+    h = po.tfim(n, 1.1)
+    prog = engine.Program(ctx, n, ops, P, "c64")
+    obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
+    rs = RngStream(4242)
+    th = np.array([[rs.normal() for _ in range(P)] for _ in range(12)])
+    alone = [engine.energy_grad_batch(ctx, prog, obs, th[i:i + 1]) for i in range(12)]
+    for B in (8, 3, 8, 12, 1, 12):
+        E, G = engine.energy_grad_batch(ctx, prog, obs, th[:B])
+        for i in range(B):
+            assert E[i] == alone[i][0][0] and np.array_equal(G[i], alone[i][1][0]), (B, i)
