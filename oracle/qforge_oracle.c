@@ -17,6 +17,38 @@
 
 static __thread char g_err[256];
 
+/* Intra-state threading for fixture generation at n = 26/30 (default 1 = the
+ * reference's single-threaded loops).  Only loops whose iterations write
+ * disjoint amplitudes with the reference's per-element arithmetic are split,
+ * and per-term expectation sums are still accumulated in term order, so the
+ * results are bit-identical to the sequential restatement. */
+static int g_inner = 1;
+void qo_set_inner_threads(int t) { g_inner = t < 1 ? 1 : t; }
+
+typedef void (*range_fn)(void* ctx, int64_t b, int64_t e);
+typedef struct { range_fn fn; void* ctx; int64_t b, e; } range_job;
+static void* range_worker(void* p) {
+    range_job* j = (range_job*)p;
+    j->fn(j->ctx, j->b, j->e);
+    return NULL;
+}
+/* fn over [0, n) in g_inner contiguous chunks (sequential below 2^16 items) */
+static void par_range(int64_t n, range_fn fn, void* ctx) {
+    int w = g_inner;
+    if (w <= 1 || n < ((int64_t)1 << 16)) {
+        fn(ctx, 0, n);
+        return;
+    }
+    pthread_t th[256];
+    range_job jobs[256];
+    if (w > 256) w = 256;
+    for (int i = 0; i < w; ++i) {
+        jobs[i] = (range_job){fn, ctx, n * i / w, n * (i + 1) / w};
+        pthread_create(&th[i], NULL, range_worker, &jobs[i]);
+    }
+    for (int i = 0; i < w; ++i) pthread_join(th[i], NULL);
+}
+
 static int fail(const char* msg) {
     snprintf(g_err, sizeof g_err, "%s", msg);
     return -1;
@@ -134,6 +166,56 @@ int qo_gate_matrix(const qo_op* op, const double complex* mats, const double* th
 /* ------------------------------------------------------------------------ */
 /* apply_local_unitary: src/circuit.cpp:78-176 (d == 2)                       */
 /* ------------------------------------------------------------------------ */
+typedef struct {
+    double complex* a;
+    const double complex* u;
+    int64_t dk, s0, s1;
+    int k;
+    int64_t ws[8];
+} alu_ctx;
+
+static void alu_diag(void* p, int64_t b, int64_t e) { /* :96-107 */
+    alu_ctx* c = (alu_ctx*)p;
+    for (int64_t idx = b; idx < e; ++idx) {
+        int64_t loc = 0;
+        for (int i = 0; i < c->k; ++i) loc = (loc << 1) | ((idx / c->ws[i]) & 1);
+        c->a[idx] *= c->u[loc * c->dk + loc];
+    }
+}
+
+/* pair index j -> lo = j with a zero inserted at stride s (the :112-121 loop nest, flattened) */
+static void alu_1q(void* p, int64_t b, int64_t e) {
+    alu_ctx* c = (alu_ctx*)p;
+    const int64_t s = c->s0;
+    const double complex u00 = c->u[0], u01 = c->u[1], u10 = c->u[2], u11 = c->u[3];
+    double complex* a = c->a;
+    for (int64_t j = b; j < e; ++j) {
+        const int64_t lo = ((j & ~(s - 1)) << 1) | (j & (s - 1));
+        double complex a0 = a[lo], a1 = a[lo + s];
+        a[lo] = u00 * a0 + u01 * a1;
+        a[lo + s] = u10 * a0 + u11 * a1;
+    }
+}
+
+static void alu_2q(void* p, int64_t b, int64_t e) { /* :128-144, flattened */
+    alu_ctx* c = (alu_ctx*)p;
+    const int64_t s0 = c->s0, s1 = c->s1;
+    const int64_t hibit = s0 > s1 ? s0 : s1, lobit = s0 < s1 ? s0 : s1;
+    double complex m[4][4];
+    for (int r = 0; r < 4; ++r)
+        for (int q = 0; q < 4; ++q) m[r][q] = c->u[r * 4 + q];
+    double complex* a = c->a;
+    for (int64_t j = b; j < e; ++j) {
+        int64_t x = ((j & ~(lobit - 1)) << 1) | (j & (lobit - 1));
+        const int64_t base = ((x & ~(hibit - 1)) << 1) | (x & (hibit - 1));
+        double complex v[4] = {a[base], a[base + s1], a[base + s0], a[base + s0 + s1]};
+        for (int r = 0; r < 4; ++r) {
+            a[base + (r >> 1) * s0 + (r & 1) * s1] =
+                m[r][0] * v[0] + m[r][1] * v[1] + m[r][2] * v[2] + m[r][3] * v[3];
+        }
+    }
+}
+
 int qo_apply_local_unitary(int n, double complex* a, const double complex* u, int k,
                            const int* wires) {
     const int64_t dk = (int64_t)1 << k;
@@ -142,56 +224,35 @@ int qo_apply_local_unitary(int n, double complex* a, const double complex* u, in
     int64_t stride[64];
     for (int i = 0; i < n; ++i) stride[i] = (int64_t)1 << (n - 1 - i); /* :86-87 */
     const int64_t dim = (int64_t)1 << n;
+    alu_ctx c;
+    c.a = a;
+    c.u = u;
+    c.dk = dk;
+    c.k = k;
 #define U(r, c) u[(r) * dk + (c)]
     if (k <= 8) { /* :90-108 diagonal fast path, exact-zero test */
         int diagonal = 1;
         for (int64_t r = 0; r < dk && diagonal; ++r)
-            for (int64_t c = 0; c < dk && diagonal; ++c)
-                if (r != c && U(r, c) != 0.0) diagonal = 0;
+            for (int64_t q = 0; q < dk && diagonal; ++q)
+                if (r != q && U(r, q) != 0.0) diagonal = 0;
         if (diagonal) {
-            int64_t ws[8];
-            for (int i = 0; i < k; ++i) ws[i] = stride[wires[i]];
-            for (int64_t idx = 0; idx < dim; ++idx) {
-                int64_t loc = 0;
-                for (int i = 0; i < k; ++i) loc = (loc << 1) | ((idx / ws[i]) & 1);
-                a[idx] *= U(loc, loc);
-            }
+            for (int i = 0; i < k; ++i) c.ws[i] = stride[wires[i]];
+            par_range(dim, alu_diag, &c);
             return 0;
         }
     }
+#undef U
     if (k == 1) { /* :109-122 */
-        const int64_t s = stride[wires[0]];
-        const double complex u00 = U(0, 0), u01 = U(0, 1), u10 = U(1, 0), u11 = U(1, 1);
-        for (int64_t hi = 0; hi < dim; hi += 2 * s) {
-            for (int64_t lo = hi; lo < hi + s; ++lo) {
-                double complex a0 = a[lo], a1 = a[lo + s];
-                a[lo] = u00 * a0 + u01 * a1;
-                a[lo + s] = u10 * a0 + u11 * a1;
-            }
-        }
+        c.s0 = stride[wires[0]];
+        par_range(dim / 2, alu_1q, &c);
         return 0;
     }
     if (k == 2) { /* :123-145 */
-        const int64_t s0 = stride[wires[0]], s1 = stride[wires[1]];
-        double complex m[4][4];
-        for (int r = 0; r < 4; ++r)
-            for (int c = 0; c < 4; ++c) m[r][c] = U(r, c);
-        const int64_t hibit = s0 > s1 ? s0 : s1, lobit = s0 < s1 ? s0 : s1;
-        for (int64_t b0 = 0; b0 < dim; b0 += 2 * hibit) {
-            for (int64_t b1 = b0; b1 < b0 + hibit; b1 += 2 * lobit) {
-                for (int64_t base = b1; base < b1 + lobit; ++base) {
-                    double complex v[4] = {a[base], a[base + s1], a[base + s0],
-                                           a[base + s0 + s1]};
-                    for (int r = 0; r < 4; ++r) {
-                        a[base + (r >> 1) * s0 + (r & 1) * s1] =
-                            m[r][0] * v[0] + m[r][1] * v[1] + m[r][2] * v[2] + m[r][3] * v[3];
-                    }
-                }
-            }
-        }
+        c.s0 = stride[wires[0]];
+        c.s1 = stride[wires[1]];
+        par_range(dim / 4, alu_2q, &c);
         return 0;
     }
-#undef U
     return fail("apply_local_unitary: only 1- and 2-qubit gates on the hot path");
 }
 
@@ -235,33 +296,70 @@ int qo_run(int n, int n_ops, const qo_op* ops, const double complex* mats,
     return 0;
 }
 
-/* expectation_pauli: src/circuit.cpp:319-347 */
+/* expectation_pauli: src/circuit.cpp:319-347.  Each term's sum runs over s in
+ * the reference order; with inner threads the terms are spread over threads and
+ * the per-term sums are still added to acc in term order (bit-identical). */
+typedef struct {
+    int n;
+    const double complex* psi;
+    const double* w_re;
+    const double* w_im;
+    const int8_t* codes;
+    double complex* sums;
+} ex_ctx;
+
+static double complex term_sum(int n, const double complex* psi, double wr, double wi,
+                               const int8_t* code) {
+    static const double complex ipowt[4] = {1.0, CMPLX(0, 1), -1.0, CMPLX(0, -1)};
+    const int64_t dim = (int64_t)1 << n;
+    uint64_t flip = 0, zmask = 0;
+    int ycount = 0;
+    for (int i = 0; i < n; ++i) {
+        uint64_t bit = 1ULL << (n - 1 - i);
+        switch (code[i]) {
+            case 1: flip |= bit; break;
+            case 2: flip |= bit; zmask |= bit; ++ycount; break;
+            case 3: zmask |= bit; break;
+            default: break;
+        }
+    }
+    double complex base = CMPLX(wr, wi) * ipowt[ycount & 3];
+    double complex sum = 0.0;
+    for (int64_t s = 0; s < dim; ++s) {
+        double complex v = base;
+        if (__builtin_parityll((uint64_t)s & zmask)) v = -v;
+        sum += conj(psi[s ^ (int64_t)flip]) * v * psi[s];
+    }
+    return sum;
+}
+
+static void ex_terms(void* p, int64_t b, int64_t e) {
+    ex_ctx* c = (ex_ctx*)p;
+    for (int64_t t = b; t < e; ++t)
+        c->sums[t] = term_sum(c->n, c->psi, c->w_re[t], c->w_im[t], c->codes + (size_t)t * c->n);
+}
+
 int qo_expectation_pauli(int n, const double complex* psi, int n_terms,
                          const double* w_re, const double* w_im, const int8_t* codes,
                          double complex* out) {
-    static const double complex ipowt[4] = {1.0, CMPLX(0, 1), -1.0, CMPLX(0, -1)};
-    const int64_t dim = (int64_t)1 << n;
     double complex acc = 0.0;
-    for (int t = 0; t < n_terms; ++t) {
-        uint64_t flip = 0, zmask = 0;
-        int ycount = 0;
-        for (int i = 0; i < n; ++i) {
-            uint64_t bit = 1ULL << (n - 1 - i);
-            switch (codes[(size_t)t * n + i]) {
-                case 1: flip |= bit; break;
-                case 2: flip |= bit; zmask |= bit; ++ycount; break;
-                case 3: zmask |= bit; break;
-                default: break;
-            }
+    if (g_inner > 1 && n >= 16 && n_terms > 1) {
+        double complex* sums = malloc((size_t)n_terms * sizeof(double complex));
+        ex_ctx c = {n, psi, w_re, w_im, codes, sums};
+        int w = g_inner < n_terms ? g_inner : n_terms;
+        pthread_t th[256];
+        range_job jobs[256];
+        if (w > 256) w = 256;
+        for (int i = 0; i < w; ++i) {
+            jobs[i] = (range_job){ex_terms, &c, (int64_t)n_terms * i / w, (int64_t)n_terms * (i + 1) / w};
+            pthread_create(&th[i], NULL, range_worker, &jobs[i]);
         }
-        double complex base = CMPLX(w_re[t], w_im[t]) * ipowt[ycount & 3];
-        double complex sum = 0.0;
-        for (int64_t s = 0; s < dim; ++s) {
-            double complex v = base;
-            if (__builtin_parityll((uint64_t)s & zmask)) v = -v;
-            sum += conj(psi[s ^ (int64_t)flip]) * v * psi[s];
-        }
-        acc += sum;
+        for (int i = 0; i < w; ++i) pthread_join(th[i], NULL);
+        for (int t = 0; t < n_terms; ++t) acc += sums[t];
+        free(sums);
+    } else {
+        for (int t = 0; t < n_terms; ++t)
+            acc += term_sum(n, psi, w_re[t], w_im[t], codes + (size_t)t * n);
     }
     *out = acc;
     return 0;
@@ -350,6 +448,27 @@ static int rotation_generator(int kind) {
  *   dE/dtheta_s = sum_{j: slot_j = s} coef_j * Im <lambda_j| G_j |psi_j>,
  * with psi_j the state after gate j and lambda_j = U_{j+1}^+ ... U_G^+ H psi.
  * H uses Re(w) only: Re<psi|H|psi> depends on the Hermitian part alone. */
+typedef struct {
+    const double complex* in;
+    double complex* out;
+    double complex base;
+    uint64_t flip, zmask;
+    int64_t b0, b1;
+    int gen;
+    const double complex* lam;
+    double* part;
+    int64_t chunk;
+} gen_ctx;
+
+static void ps_term(void* p, int64_t b, int64_t e) {
+    gen_ctx* c = (gen_ctx*)p;
+    for (int64_t s = b; s < e; ++s) {
+        double complex v = c->base;
+        if (__builtin_parityll((uint64_t)s & c->zmask)) v = -v;
+        c->out[s ^ (int64_t)c->flip] += v * c->in[s];
+    }
+}
+
 static void apply_pauli_sum(int n, const qo_hamil* h, const double complex* psi,
                             double complex* out) {
     const int64_t dim = (int64_t)1 << n;
@@ -365,12 +484,23 @@ static void apply_pauli_sum(int n, const qo_hamil* h, const double complex* psi,
             if (c == 2) { flip |= bit; zmask |= bit; ++y; }
             if (c == 3) zmask |= bit;
         }
-        double complex base = h->w_re[t] * ipowt[y & 3];
-        /* (P psi)[s ^ flip] = base * (-1)^{popc(s & z)} psi[s] */
-        for (int64_t s = 0; s < dim; ++s) {
-            double complex v = base;
-            if (__builtin_parityll((uint64_t)s & zmask)) v = -v;
-            out[s ^ (int64_t)flip] += v * psi[s];
+        /* (P psi)[s ^ flip] = base * (-1)^{popc(s & z)} psi[s]: s -> s ^ flip is a bijection */
+        gen_ctx c = {psi, out, h->w_re[t] * ipowt[y & 3], flip, zmask, 0, 0, 0, NULL, NULL, 0};
+        par_range(dim, ps_term, &c);
+    }
+}
+
+static void gen_apply(void* p, int64_t b, int64_t e) {
+    gen_ctx* c = (gen_ctx*)p;
+    const double complex* in = c->in;
+    double complex* out = c->out;
+    for (int64_t s = b; s < e; ++s) {
+        int bit0 = (s & c->b0) != 0;
+        switch (c->gen) {
+            case 1: out[s] = in[s ^ c->b0]; break;
+            case 2: out[s] = (bit0 ? CMPLX(0, 1) : CMPLX(0, -1)) * in[s ^ c->b0]; break;
+            case 3: out[s] = bit0 ? -in[s] : in[s]; break;
+            case 4: out[s] = (bit0 ^ ((s & c->b1) != 0)) ? -in[s] : in[s]; break;
         }
     }
 }
@@ -378,17 +508,42 @@ static void apply_pauli_sum(int n, const qo_hamil* h, const double complex* psi,
 static void apply_generator(int n, int gen, int q0, int q1, const double complex* in,
                             double complex* out) {
     const int64_t dim = (int64_t)1 << n;
-    const int64_t b0 = (int64_t)1 << (n - 1 - q0);
-    const int64_t b1 = q1 >= 0 ? (int64_t)1 << (n - 1 - q1) : 0;
-    for (int64_t s = 0; s < dim; ++s) {
-        int bit0 = (s & b0) != 0;
-        switch (gen) {
-            case 1: out[s] = in[s ^ b0]; break;
-            case 2: out[s] = (bit0 ? CMPLX(0, 1) : CMPLX(0, -1)) * in[s ^ b0]; break;
-            case 3: out[s] = bit0 ? -in[s] : in[s]; break;
-            case 4: out[s] = (bit0 ^ ((s & b1) != 0)) ? -in[s] : in[s]; break;
-        }
+    gen_ctx c = {in, out, 0, 0, 0, (int64_t)1 << (n - 1 - q0), q1 >= 0 ? (int64_t)1 << (n - 1 - q1) : 0,
+                 gen, NULL, NULL, 0};
+    par_range(dim, gen_apply, &c);
+}
+
+/* Im <lambda|tmp>, summed in fixed chunks of 2^16 (new math, order fixed for any thread count) */
+static void im_chunks(void* p, int64_t b, int64_t e) {
+    gen_ctx* c = (gen_ctx*)p;
+    for (int64_t k = b; k < e; ++k) {
+        double im = 0.0;
+        for (int64_t s = k * c->chunk; s < (k + 1) * c->chunk; ++s) im += cimag(conj(c->lam[s]) * c->in[s]);
+        c->part[k] = im;
     }
+}
+
+static double im_inner(int64_t N, const double complex* lam, const double complex* tmp) {
+    const int64_t chunk = N < ((int64_t)1 << 16) ? N : ((int64_t)1 << 16);
+    const int64_t nc = N / chunk;
+    double* part = malloc((size_t)nc * sizeof(double));
+    gen_ctx c = {tmp, NULL, 0, 0, 0, 0, 0, 0, lam, part, chunk};
+    if (g_inner > 1 && nc >= g_inner) {
+        pthread_t th[256];
+        range_job jobs[256];
+        int w = g_inner > 256 ? 256 : g_inner;
+        for (int i = 0; i < w; ++i) {
+            jobs[i] = (range_job){im_chunks, &c, nc * i / w, nc * (i + 1) / w};
+            pthread_create(&th[i], NULL, range_worker, &jobs[i]);
+        }
+        for (int i = 0; i < w; ++i) pthread_join(th[i], NULL);
+    } else {
+        im_chunks(&c, 0, nc);
+    }
+    double im = 0.0;
+    for (int64_t k = 0; k < nc; ++k) im += part[k];
+    free(part);
+    return im;
 }
 
 static int adjoint_gradient(const qo_ansatz* a, const double* theta, const qo_hamil* h,
@@ -408,8 +563,7 @@ static int adjoint_gradient(const qo_ansatz* a, const double* theta, const qo_ha
             if (op->slot >= 0) {
                 if (!gen) { rc = fail("adjoint: parameter feeds a non-rotation gate"); break; }
                 apply_generator(n, gen, op->q0, op->q1, psi, tmp);
-                double im = 0.0;
-                for (int64_t s = 0; s < N; ++s) im += cimag(conj(lam[s]) * tmp[s]);
+                const double im = im_inner(N, lam, tmp);
                 grad[op->slot] += op->coef * im;
             }
             double complex u[16], ud[16];

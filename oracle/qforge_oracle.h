@@ -120,6 +120,9 @@ long long qo_pauli_sum_to_coo(int n, int n_terms, const double* w_re, const doub
                               const int8_t* codes, long long* rows, long long* cols,
                               double complex* vals, long long capacity);
 
+/* fixture generation: split gate loops over t threads (bit-identical results) */
+void qo_set_inner_threads(int t);
+
 const char* qo_last_error(void);
 
 #ifdef __cplusplus
