@@ -171,6 +171,30 @@ def measured_hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_fp_peaks():
+    """FP32 / FP64 CUDA-core peaks measured on this pool's B200 (tools/micro/peaks.cu,
+    committed as profiles/r2_fp_peaks.json): (fp32 TFLOP/s, fp64 TFLOP/s, source)."""
+    p = os.path.join(ROOT, "profiles", "r2_fp_peaks.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["fp32_ffma_3reg_tflops"]), float(d["fp64_dfma_tflops"]), "measured (profiles/r2_fp_peaks.json)"
+    except Exception:
+        return 74.45, 37.2, "nominal (148 SMs x 128 FP32 lanes x 1965 MHz; FP64 half rate)"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def ncu_compute(cfg_name, cls_name, batch):
     """FP32-pipe view of the same committed capture (the sweeps are FMA-pipe bound,
     not HBM bound), or None."""
@@ -224,7 +248,9 @@ def cpu_sample(cfg_name, cfg, ops, P, h, thetas, seconds=12.0):
     dt = time.perf_counter() - t0
     energies_per_s = count / dt
     evals_per_s = energies_per_s / (1 + 2 * P)
-    return {"value": evals_per_s, "unit": UNIT, "cores": cores, "kind": "port",
+    return {"value": evals_per_s, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+            "compiler": "gcc -O2 (no -ffast-math / -march, like proj/src/CMakeLists.txt:8; oracle/Makefile)",
+            "precision": "c128 (the reference's complex<double>)",
             "sample": f"{count} energy() calls of {cfg_name} (n={cfg['n']}, P={P}) on {cores} threads in "
                       f"{dt:.1f} s; eval = 1 + 2P = {1 + 2 * P} energies (parameter shift, "
                       f"variational.cpp:54-81), extrapolated"}
@@ -334,27 +360,12 @@ def main():
     out_d = torch.zeros(B * (1 + P), dtype=torch.float64, device=dev)
     E_d = out_d[:B]
     G_d = out_d[B:].view(B, P)
-    if term_shard:
-        b0, b1 = 0, B
-    else:
-        b0, b1 = B * rank // world, B * (rank + 1) // world
-
+    # The engine shards itself (qf_energy_grad_batch_device with a communicator:
+    # the rank's batch rows or term block, one NCCL all-reduce on its stream):
+    # every rank passes the full batch and receives the full result.
     def step_device():
         with torch.cuda.stream(ext):
-            if world > 1:
-                out_d.zero_()
-            if b1 > b0:
-                engine.energy_grad_batch_device(ctx, prog, obs, th_d[b0:b1], E_d[b0:b1], G_d[b0:b1])
-            if world > 1 and not term_shard:
-                dist.all_reduce(out_d)
-
-    if term_shard:
-        # term sharding lives inside the C-ABI host call; the device-resident leg
-        # uses the same call with every rank evaluating the full batch on its terms
-        def step_device():  # noqa: F811
-            with torch.cuda.stream(ext):
-                engine.energy_grad_batch_device(ctx, prog, obs, th_d, E_d, G_d)
-                dist.all_reduce(out_d)
+            engine.energy_grad_batch_device(ctx, prog, obs, th_d, E_d, G_d)
 
     def agreed_count(seconds, one_call):
         """iterations covering `seconds`, identical on every rank (the calls run collectives)"""
@@ -400,11 +411,13 @@ def main():
     # instrumented pass: the same K steps with per-class CUDA events on the
     # engine stream (kernel launches counted, graphs off)
     ctx.reset_stats()
-    ctx.set_timing(True)
+    ctx.set_timing(2)  # per class and per launch
     for _ in range(args.steps):
         step_device()
     torch.cuda.synchronize(dev)
     launches, cls_launches, cls_ms, cls_bytes = ctx.stats()
+    cls_flops = ctx.flops()
+    per_launch = ctx.launch_times()
     ctx.set_timing(False)
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     if world > 1:
@@ -433,22 +446,37 @@ def main():
     # consistency of the two legs (same numbers through both APIs)
     torch.cuda.synchronize(dev)
     E_dev = E_d.cpu().numpy()
-    agree = float(np.abs(E_dev - E_h).max())
+    G_dev = G_d.cpu().numpy()
+    agree = float(max(np.abs(E_dev - E_h).max(), np.abs(G_dev - G_h).max()))
+    if agree != 0.0:  # both legs run the same kernels on the same inputs: bitwise equal
+        raise SystemExit(f"device-resident and end-to-end results differ: max |d| = {agree}")
 
     # ---- roofline of the dominant kernel class ----
     names = ["forward_sweep", "hpsi_energy", "adjoint_sweep", "reduction"]
     dom = max(range(3), key=lambda i: cls_ms[i])
     peak, peak_src = measured_hbm_peak()
+    fp32_peak, fp64_peak, fp_src = measured_fp_peaks()
+    fpeak = fp64_peak if cfg["prec"] == "c128" else fp32_peak
     achieved = (cls_bytes[dom] / 1e9) / (cls_ms[dom] / 1e3) if cls_ms[dom] > 0 else 0.0
-    per_launch = cls_bytes[dom] / max(1, cls_launches[dom])
-    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "GB/s",
+    bytes_per_launch = cls_bytes[dom] / max(1, cls_launches[dom])
+    ftf = (cls_flops[dom] / 1e12) / (cls_ms[dom] / 1e3) if cls_ms[dom] > 0 else 0.0
+    roofline = {"bound": "hbm" if achieved / peak >= ftf / fpeak else ("fp64" if cfg["prec"] == "c128" else "fp32"),
+                "kernel": names[dom], "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(cfg_name, names[dom], B),
                 "compute": ncu_compute(cfg_name, names[dom], B),
-                "algorithmic_bytes_per_launch": per_launch,
+                "flops": {"achieved": ftf, "peak": fpeak, "unit": "TFLOP/s", "frac": ftf / fpeak,
+                          "flops_per_launch": cls_flops[dom] / max(1, cls_launches[dom]), "peak_source": fp_src,
+                          "counting": "canonical algorithmic flops (SURVEY.md 8(d)): 14 per dense 1q gate and "
+                                      "amplitude, 6 per diagonal gate, 8 per tap / term inner product; adjoint "
+                                      "gates count twice (two states)"},
+                "algorithmic_bytes_per_launch": bytes_per_launch,
                 "avg_launch_ms": cls_ms[dom] / max(1, cls_launches[dom]), "peak_source": peak_src,
                 "classes": {names[i]: {"ms": cls_ms[i], "launches": cls_launches[i], "bytes": cls_bytes[i],
-                                       "GBps": (cls_bytes[i] / 1e9) / (cls_ms[i] / 1e3) if cls_ms[i] else None}
-                            for i in range(4)}}
+                                       "GBps": (cls_bytes[i] / 1e9) / (cls_ms[i] / 1e3) if cls_ms[i] else None,
+                                       "TFLOPs": (cls_flops[i] / 1e12) / (cls_ms[i] / 1e3) if cls_ms[i] else None}
+                            for i in range(4)},
+                "per_launch_ms": {("fwd%d" % k if k < 1000 else "hpsi" if k == 1000 else "bwd%d" % (k - 2000)):
+                                  round(v[0] / max(1, v[1]), 4) for k, v in sorted(per_launch.items())}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -467,7 +495,7 @@ def main():
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * P * 8,
                         "d2h_bytes_per_step": B * (1 + P) * 8},
                 "gpu_launches": launches, "clocks": clocks,
-                "program": dict(prog.info(), jit=prog.jit_status()), "e2e_vs_device_max_abs_dE": agree}
+                "program": dict(prog.info(), jit=prog.jit_status()), "e2e_vs_device_max_abs_diff": agree}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

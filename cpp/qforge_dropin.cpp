@@ -130,13 +130,41 @@ std::shared_ptr<ProgramHandle> make_program(const Template& t, int n_params) {
     return h;
 }
 
+// FNV-1a over raw bytes (device-cache keys: content, not identity or size)
+struct Fnv {
+    std::uint64_t h = 1469598103934665603ull;
+    void add(const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) {
+            h ^= b[i];
+            h *= 1099511628211ull;
+        }
+    }
+    template <class T> void add(const T& v) { add(&v, sizeof v); }
+};
+
+std::uint64_t pauli_sum_key(const PauliSum& h) {
+    Fnv f;
+    f.add(h.n);
+    f.add(h.terms.size());
+    for (const auto& t : h.terms) {
+        f.add(t.weight);
+        f.add(t.codes.size());
+        for (int c : t.codes) f.add(c);
+    }
+    return f.h;
+}
+
 qf_observable* observable(const PauliSum& h) {
+    // keyed on the sum's content: `terms` is public and may be edited in place,
+    // and a copied PauliSum shares the cache pointer until it diverges
     struct Cache {
         std::shared_ptr<ObservableHandle> obs;
-        size_t terms = 0;
+        std::uint64_t key = 0;
     };
+    const std::uint64_t key = pauli_sum_key(h);
     auto cache = std::static_pointer_cast<Cache>(h.device_cache);
-    if (!cache || cache->terms != h.terms.size()) {
+    if (!cache || cache->key != key) {
         cache = std::make_shared<Cache>();
         std::vector<int8_t> codes;
         std::vector<double> wr, wi;
@@ -148,7 +176,7 @@ qf_observable* observable(const PauliSum& h) {
         cache->obs = std::make_shared<ObservableHandle>();
         check(qf_observable_create(ctx(), h.n, (int)h.terms.size(), codes.data(), wr.data(), wi.data(),
                                    &cache->obs->o));
-        cache->terms = h.terms.size();
+        cache->key = key;
         h.device_cache = cache;
     }
     return cache->obs->o;
@@ -799,17 +827,40 @@ AnsatzSpec hea_ansatz(int n, int layers) {
 
 namespace {
 
-// Parameter-slot discovery: probe the opaque builder.
+bool same_matrix(const ComplexMatrix& x, const ComplexMatrix& y) {
+    if (x.rows() != y.rows() || x.cols() != y.cols()) return false;
+    for (std::int64_t i = 0; i < x.size(); ++i)
+        if (x.data()[i] != y.data()[i]) return false;
+    return true;
+}
+
+bool same_init(const std::optional<ComplexVector>& x, const std::optional<ComplexVector>& y) {
+    if (x.has_value() != y.has_value()) return false;
+    return !x || same_matrix(*x, *y);
+}
+
+std::uint64_t template_key(const Template& t, int n_params) {
+    Fnv f;
+    f.add(t.n);
+    f.add(n_params);
+    for (const qf_op& q : t.ops) {
+        f.add(q.kind); f.add(q.q0); f.add(q.q1); f.add(q.slot); f.add(q.coef); f.add(q.offset); f.add(q.mat);
+    }
+    f.add(t.mats.data(), t.mats.size() * sizeof(double));
+    f.add(t.init.has_value());
+    if (t.init) f.add(t.init->data(), (size_t)t.init->size() * sizeof(cplx));
+    return f.h;
+}
+
+// Parameter-slot discovery: probe the opaque builder.  The
+// builder is probed on every call and the compiled program is reused only
+// while the discovered template (ops, slots, matrices, initial state) and
+// n_params are unchanged: `builder` and `n_params` are public fields.
 std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
     struct Cache {
-        std::map<int, std::shared_ptr<ProgramHandle>> by_prec;
-        int n = 0;
+        std::map<std::pair<int, std::uint64_t>, std::shared_ptr<ProgramHandle>> progs;  // (precision, template key)
     };
     auto cache = std::static_pointer_cast<Cache>(a.device_cache);
-    if (cache) {
-        auto f = cache->by_prec.find((int)g_prec);
-        if (f != cache->by_prec.end()) return f->second;
-    }
     a.validate();
     const int P = a.n_params;
     RealVector t0 = RealVector::Zero(P), ta(P), tb(P), tc(P);
@@ -824,13 +875,15 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
         for (size_t i = 0; same && i < c0.ops.size(); ++i)
             same = c->ops[i].name == c0.ops[i].name && c->ops[i].wires == c0.ops[i].wires;
         require(same, "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)");
+        require(same_init(c->initial_state, c0.initial_state),
+                "AnsatzSpec: theta feeds the initial state (not supported on the device path)");
     }
     std::vector<SlotMap> slots(c0.ops.size());
     for (size_t i = 0; i < c0.ops.size(); ++i) {
         const GateInstruction& op = c0.ops[i];
         if (!is_rotation(op.name)) {
             for (const Circuit* c : {&ca, &cb, &cc})
-                require(c->ops[i].params == op.params,
+                require(c->ops[i].params == op.params && same_matrix(c->ops[i].matrix, op.matrix),
                         "AnsatzSpec: theta feeds a gate without a Pauli generator "
                         "(su4/unitary parameters are not supported on the device path)");
             continue;
@@ -857,13 +910,19 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
                 "AnsatzSpec: builder is not affine in a single theta slot");
         slots[i] = {s, coef, o};
     }
-    auto prog = make_program(circuit_template(c0, &slots), P);
+    const Template t = circuit_template(c0, &slots);
+    const auto key = std::make_pair((int)g_prec, template_key(t, P));
+    if (cache) {
+        auto f = cache->progs.find(key);
+        if (f != cache->progs.end()) return f->second;
+    }
+    auto prog = make_program(t, P);
     if (!cache) {
         cache = std::make_shared<Cache>();
         a.device_cache = cache;
     }
-    cache->n = c0.n;
-    cache->by_prec[(int)g_prec] = prog;
+    if (cache->progs.size() >= 8) cache->progs.clear();  // bound the programs kept per spec
+    cache->progs[key] = prog;
     return prog;
 }
 
@@ -966,41 +1025,34 @@ void adam_step(AdamState& state, RealVector& theta, const RealVector& grad, doub
 }
 
 VqeResult vqe_run(const AnsatzSpec& ansatz, const std::vector<RealVector>& theta0_batch, const PauliSum& h, int steps,
-                  double lr, GradMode grad_mode, int /*workers*/) {  // variational.cpp:103-143
+                  double lr, GradMode grad_mode, int /*workers: results never depend on it*/) {  // variational.cpp:103-143
     ansatz.validate();
     require(!theta0_batch.empty(), "vqe_run: empty batch");
     require(steps >= 1, "vqe_run: steps must be >= 1");
-    const int B = (int)theta0_batch.size();
-    VqeResult out;
-    out.traces.assign(B, {});
-    std::vector<RealVector> th = theta0_batch;
-    std::vector<AdamState> adam(B);
-    for (int s = 0; s < steps; ++s) {  // the whole batch advances together: one device call per step
-        std::vector<double> E;
-        std::vector<RealVector> G;
-        if (grad_mode == GradMode::adjoint) {
-            energy_gradient_batch(ansatz, th, h, E, &G);
-        } else {
-            energy_gradient_batch(ansatz, th, h, E, nullptr);
-            G.resize(B);
-            for (int b = 0; b < B; ++b) G[b] = gradient(ansatz, th[b], h, grad_mode, 1e-5, 1);
-        }
-        for (int b = 0; b < B; ++b) {
-            out.traces[b].push_back(E[b]);
-            adam_step(adam[b], th[b], G[b], lr);
-        }
-    }
-    std::vector<double> E;
-    energy_gradient_batch(ansatz, th, h, E, nullptr);
-    out.best_energy = INFINITY;
+    const int B = (int)theta0_batch.size(), P = ansatz.n_params;
+    if (grad_mode == GradMode::parameter_shift)
+        for (int j = 0; j < P; ++j)
+            require(ansatz.shift_eligible[j], "gradient: parameter not shift-eligible, use finite_diff");
+    std::vector<double> flat((size_t)B * P);
     for (int b = 0; b < B; ++b) {
-        out.traces[b].push_back(E[b]);
-        if (E[b] < out.best_energy) {
-            out.best_energy = E[b];
-            out.best_index = b;
-        }
+        require(theta0_batch[b].size() == P, "gradient: parameter count mismatch");
+        std::memcpy(flat.data() + (size_t)b * P, theta0_batch[b].data(), sizeof(double) * P);
     }
-    out.final_thetas = th;
+    auto prog = ansatz_program(ansatz);
+    // theta, the Adam moments and the traces stay on the device for all steps
+    // (one native call; the batch advances in lock step, one host copy at the end)
+    std::vector<double> tr((size_t)B * (steps + 1)), fin((size_t)B * P);
+    const int mode = grad_mode == GradMode::adjoint ? QF_GRAD_ADJOINT
+                     : grad_mode == GradMode::finite_diff ? QF_GRAD_FINITE_DIFF : QF_GRAD_PARAMETER_SHIFT;
+    VqeResult out;
+    check(qf_vqe_run(ctx(), prog->p, observable(h), B, flat.data(), steps, lr, mode, 1e-5, tr.data(), fin.data(),
+                     &out.best_energy, &out.best_index));
+    out.traces.assign(B, {});
+    out.final_thetas.assign(B, RealVector(P));
+    for (int b = 0; b < B; ++b) {
+        out.traces[b].assign(tr.begin() + (size_t)b * (steps + 1), tr.begin() + (size_t)(b + 1) * (steps + 1));
+        for (int j = 0; j < P; ++j) out.final_thetas[b][j] = fin[(size_t)b * P + j];
+    }
     return out;
 }
 

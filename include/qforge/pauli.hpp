@@ -25,9 +25,8 @@ struct PauliSum {
     void add(cplx weight, const std::vector<int>& codes);
     void add_word(cplx weight, const std::vector<std::pair<int, int>>& site_codes);
 
-    // device copy (qf_observable), rebuilt when the terms change
+    // device copy (qf_observable), rebuilt when the terms change (content-keyed)
     mutable std::shared_ptr<void> device_cache;
-    mutable std::size_t device_cache_terms = 0;
 };
 
 // canonical COO of the sum, built on the GPU (pauli.cpp:89-153); `workers` is

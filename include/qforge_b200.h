@@ -27,8 +27,11 @@
  *   - precondition failures return QF_EINVAL (the C++ shim maps it to
  *     std::invalid_argument, common.hpp:24-26); everything else is a runtime
  *     failure (std::runtime_error).  qf_last_error() has the message.
- *   - results never depend on the number of GPUs (parallel.hpp:9-10): every batch
- *     slot has exactly one owner and term chunks are fixed.
+ *   - batch-sharded results never depend on the number of GPUs (parallel.hpp:9-10):
+ *     every batch slot has exactly one owner and the all-reduce adds exact zeros.
+ *     Term-sharded results (one large state, QF_SHARD_TERMS) equal the 1-GPU
+ *     result up to floating-point summation order (each rank sums its own term
+ *     block; measured <= 1e-12 relative, tests/test_gpu_api.py virtual ranks).
  *
  * Calls are synchronous (they return after results are on the host) except the
  * *_device variants, which are stream-ordered on the context's stream.
@@ -168,6 +171,16 @@ int qf_expectation(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs
  * evaluates its share and every rank receives the full result. */
 int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs,
                          int batch, const double* thetas, double* energies, double* grads);
+/* The exact contribution rank `rank` of `world` makes to qf_energy_grad_batch
+ * before the all-reduce (zero rows outside its batch block, or its term block's
+ * partial sums), with no communicator: the multi-GPU split replayed on one GPU
+ * (summing the parts over ranks reproduces the collective's result). */
+/* The multi-GPU partition rule (batch rows or Hamiltonian terms): rank r of p
+ * owns [count r / p, count (r + 1) / p).  Host-only (no device needed). */
+int qf_shard_range(int64_t count, int rank, int world, int64_t* begin, int64_t* end);
+int qf_energy_grad_batch_partial(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs,
+                                 int batch, const double* thetas, int rank, int world,
+                                 double* energies, double* grads);
 
 /* pauli_sum_to_coo (reference src/pauli.cpp:89-153): the Pauli sum as a canonical
  * sparse matrix (row-major, ascending columns, duplicates summed per flip mask,
@@ -227,11 +240,25 @@ int qf_noise_trajectories(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops
 
 /* ---- evaluation on device-resident buffers (stream-ordered, no host sync) ----
  * d_thetas [batch][P], d_energies [batch], d_grads [batch][P] (may be NULL), all
- * float64 device pointers.  Single-GPU semantics (no collective). */
+ * float64 device pointers.  With a communicator attached every rank passes the
+ * full batch and receives the full result, as for qf_energy_grad_batch (the
+ * rank's share, one NCCL all-reduce on the context stream). */
 int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* prog,
                                 const qf_observable* obs, int batch,
                                 const double* d_thetas, double* d_energies,
                                 double* d_grads);
+/* vqe_run (reference src/variational.cpp:103-143) with theta, the Adam moments
+ * and the energy traces resident on the device: `steps` x (batched energy +
+ * gradient, Adam(beta1 0.9, beta2 0.999, eps 1e-8)), then the final energies.
+ * theta0 / final_thetas: [batch][P] host; traces: [batch][steps + 1] host
+ * (trace[s] = energy before update s, the last entry the final energy);
+ * best = first strict minimum of the final energies.  grad_mode: the reference's
+ * GradMode (parameter shift / finite differences as one batched evaluation of
+ * the 2P shifted sets per step) or the adjoint method. */
+enum qf_grad_mode { QF_GRAD_PARAMETER_SHIFT = 0, QF_GRAD_FINITE_DIFF = 1, QF_GRAD_ADJOINT = 2 };
+int qf_vqe_run(qf_ctx* ctx, const qf_program* prog, const qf_observable* obs, int batch,
+               const double* theta0, int steps, double lr, int grad_mode, double fd_step,
+               double* traces, double* final_thetas, double* best_energy, int* best_index);
 /* Adam (variational.cpp:83-101) over batch x P device arrays, t = step count after
  * this update (1-based). */
 int qf_adam_step_device(qf_ctx* ctx, int batch, int n_params, double* d_theta,
@@ -244,7 +271,15 @@ int qf_adam_step_device(qf_ctx* ctx, int batch, int n_params, double* d_theta,
  * device time per class from CUDA events recorded on the context stream
  * (resolved lazily, no syncs inside evaluation calls).  Classes: 0 = forward
  * sweeps, 1 = H|psi> / energy, 2 = adjoint sweeps, 3 = reductions. */
-int qf_ctx_set_timing(qf_ctx* ctx, int enabled);
+int qf_ctx_set_timing(qf_ctx* ctx, int enabled);  /* 0 off, 1 per class, 2 + per launch */
+/* Per-launch device times (timing level 2): launch id (forward sweep i, 1000 =
+ * H|psi>, 2000 + i = adjoint sweep i), accumulated ms and launch count; *n = the
+ * number of ids (entries beyond cap are counted but not written). */
+/* Canonical algorithmic flops per class since the last reset (SURVEY.md 8(d):
+ * 14 per dense one-qubit gate and amplitude, 6 per diagonal gate, 8 per tap
+ * inner product and per Hamiltonian term; adjoint gates count twice). */
+int qf_ctx_flops(qf_ctx* ctx, double* flops_by_class /* [4] */);
+int qf_ctx_launch_times(qf_ctx* ctx, int cap, int* ids, double* ms, long long* counts, int* n);
 int qf_ctx_reset_stats(qf_ctx* ctx);
 int qf_ctx_stats(qf_ctx* ctx, long long* launches, long long* launches_by_class /* [4] */,
                  double* ms_by_class /* [4] */, double* bytes_by_class /* [4] */);

@@ -54,6 +54,10 @@ SIGNATURES = {
     "qf_expectation": (_I, [_P, _P, _P, _D, _D]),
     "qf_energy_grad_batch": (_I, [_P, _P, _P, _I, _D, _D, _D]),
     "qf_energy_grad_batch_device": (_I, [_P, _P, _P, _I, _P, _P, _P]),
+    "qf_energy_grad_batch_partial": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _D]),
+    "qf_vqe_run": (_I, [_P, _P, _P, _I, _D, _I, ctypes.c_double, _I, ctypes.c_double, _D, _D, _D,
+                        ctypes.POINTER(_I)]),
+    "qf_shard_range": (_I, [ctypes.c_int64, _I, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "qf_adam_step_device": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, ctypes.c_double, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double]),
     "qf_plan_describe": (_I, [_I, _I, ctypes.POINTER(QfOp), _D, _I, _I, _I, ctypes.c_char_p, ctypes.c_size_t,
@@ -71,6 +75,8 @@ SIGNATURES = {
     "qf_pauli_sum_to_coo": (_I, [_P, _P, _I, _I, _P, _P, _P, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]),
     "qf_ctx_set_timing": (_I, [_P, _I]),
     "qf_ctx_reset_stats": (_I, [_P]),
+    "qf_ctx_flops": (_I, [_P, _D]),
+    "qf_ctx_launch_times": (_I, [_P, _I, ctypes.POINTER(_I), _D, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(_I)]),
     "qf_ctx_stats": (_I, [_P, ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong), _D, _D]),
 }
 

@@ -17,8 +17,24 @@ std::mutex g_nccl_mu;
 
 namespace qfcapi {
 
+// Drops the context's captured evaluation graph (it may reference kernels,
+// plans or buffers that are about to be released or rebuilt).
+void drop_graph(qf_ctx* ctx) {
+    if (ctx->graph_exec) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaGraphExecDestroy(ctx->graph_exec);
+        ctx->graph_exec = nullptr;
+    }
+    ctx->graph_key.clear();
+    ctx->graph_nocapture_key.clear();
+}
+
 int ensure_obs_dev(qf_observable* o, int prec, int kh, ObsDev& d, int t_begin, int t_end) {
     if (d.ready && d.plan.kh == kh) return QF_OK;
+    if (d.hj.kernel) {  // the previous plan's specialised kernel goes with it
+        drop_graph(o->ctx);
+        jit_release(d.hj);
+    }
     std::string e = build_observable_plan(o->n, t_end - t_begin, o->codes.data() + (size_t)t_begin * o->n,
                                           o->w_re.data() + t_begin, o->w_im.data() + t_begin, kh, d.plan);
     if (!e.empty()) return set_err(QF_EINVAL, e);
@@ -27,6 +43,8 @@ int ensure_obs_dev(qf_observable* o, int prec, int kh, ObsDev& d, int t_begin, i
     QF_CUDA(upload(d.terms, d.plan.terms, s));
     d.ready = true;
     d.hj_state = 0;  // plan (re)built: the specialised H|psi> kernel follows it
+    static std::atomic<uint64_t> next_gen{1};
+    d.gen = next_gen++;  // captured graphs of the previous plan (its kernel, groups, terms) are stale
     (void)prec;
     return QF_OK;
 }
@@ -42,7 +60,13 @@ void resolve_events(qf_ctx* ctx) {
     for (auto& pr : ctx->pending) {
         float ms = 0;
         cudaEventElapsedTime(&ms, ctx->ev_pool[pr.first], ctx->ev_pool[pr.first + 1]);
-        ctx->ms[pr.second] += ms;
+        if (pr.second < 4) {
+            ctx->ms[pr.second] += ms;
+        } else {  // per-launch timing (timing level 2): id = class - 100
+            auto& e = ctx->launch_ms[pr.second - 100];
+            e.first += ms;
+            e.second += 1;
+        }
     }
     ctx->pending.clear();
     ctx->ev_used = 0;
@@ -78,6 +102,18 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         if (ctx->timing) {
             record_event(ctx, s);
             ctx->pending.push_back({ev_start[i / 2], cls});
+        }
+    };
+    // timing level 2: every sweep / H|psi> launch bracketed by its own events
+    // (ids: forward sweep i, 1000 = H|psi>, 2000 + i = adjoint sweep i)
+    size_t l_ev = 0;
+    auto ltick = [&] {
+        if (ctx->timing >= 2) l_ev = record_event(ctx, s);
+    };
+    auto ltock = [&](int id) {
+        if (ctx->timing >= 2) {
+            record_event(ctx, s);
+            ctx->pending.push_back({l_ev, 100 + id});
         }
     };
 
@@ -118,13 +154,16 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     for (size_t i = 0; i < P.fwd.sweeps.size(); ++i) {
         sa.sw = P.fwd.sweeps[i];
         sa.from_zero = (i == 0 && first_from_zero) ? 1 : 0;
+        ltick();
         if (prog->use_jit)
             QF_CUDA((cudaError_t)jit_launch(prog->jf.sweeps[i], sa, 1 << (n - sa.sw.k), bc, s));
         else
             QF_CUDA(launch_sweep(prec, false, sa, bc, P.fwd.max_mat, 0, s));
+        ltock((int)i);
         ctx->launches++;
         ctx->class_launches[0]++;
         ctx->bytes[0] += (double)bc * N * vs * (sa.from_zero ? 1 : 2);
+        ctx->flops[0] += (double)bc * N * prog->fwd_fpa[i];
     }
     if (!prog->has_init && P.fwd.sweeps.empty()) ctx->bytes[0] += (double)bc * N * vs;
     tock(0, 0);
@@ -145,13 +184,18 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.use_imag = 0;
     ha.epart = (double*)ctx->epart.p;
     ha.prefetch = od->plan.terms.size() <= 4 * std::max<size_t>(1, od->plan.groups.size()) ? 1 : 0;
+    ltick();
     if (od->hj_state == 1)
         QF_CUDA((cudaError_t)jit_launch_hpsi(od->hj, ha, tiles_h, bc, s));
     else
         QF_CUDA(launch_hpsi(prec, ha, bc, s));
+    ltock(1000);
     ctx->launches++;
     ctx->class_launches[1]++;
-    ctx->bytes[1] += (double)bc * N * vs * (ha.n_groups + (grads ? 1 : 0));
+    // compulsory bytes: psi read once, lambda written once (partner tiles of
+    // flips above the tile are re-reads, served from L2 when the state fits)
+    ctx->bytes[1] += (double)bc * N * vs * (grads ? 2 : 1);
+    ctx->flops[1] += (double)bc * N * 8.0 * ((double)od->plan.terms.size() + 1.0);
     ReduceArgs ra{};
     ra.part = (const double*)ctx->epart.p;
     ra.count = 1;
@@ -186,13 +230,16 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         sa.gmat_pass_base = P.fwd.total_mat;
         for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) {
             sa.sw = P.bwd.sweeps[i];
+            ltick();
             if (prog->use_jit)
                 QF_CUDA((cudaError_t)jit_launch(prog->jb.sweeps[i], sa, 1 << (n - sa.sw.k), bc, s));
             else
                 QF_CUDA(launch_sweep(prec, true, sa, bc, P.bwd.max_mat, P.bwd.max_taps, s));
+            ltock(2000 + (int)i);
             ctx->launches++;
             ctx->class_launches[2]++;
             ctx->bytes[2] += (double)bc * N * vs * 4;
+            ctx->flops[2] += (double)bc * N * prog->bwd_fpa[i];
         }
         tock(4, 2);
         tick(6);
@@ -227,7 +274,7 @@ void ensure_hpsi_kernel(qf_program* prog, ObsDev* od, int prec) {
 
 // Evaluate rows [0, batch) of device thetas into device outputs (chunked).
 int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, const double* d_thetas,
-                double* d_E, double* d_Eim, double* d_G, bool term_shard) {
+                double* d_E, double* d_Eim, double* d_G, bool term_shard, int rank, int world) {
     const ProgramPlan& P = prog->plan;
     if (obs->n != P.n) return set_err(QF_EINVAL, "expectation_pauli: size mismatch");
     if (d_G && !P.adjoint_ok) return set_err(QF_EINVAL, P.adjoint_error);
@@ -235,16 +282,17 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     const Geometry geo = geometry(prec, n);
     ObsDev* od = &obs->dev[prec];
     int rc;
-    if (term_shard && ctx->comm) {
-        const int T = (int)obs->w_re.size();
-        const int t0 = (int)((long long)T * ctx->rank / ctx->world);
-        const int t1 = (int)((long long)T * (ctx->rank + 1) / ctx->world);
-        if (obs->shard_world != ctx->world) {
+    if (term_shard && world > 1) {
+        // rank r owns the contiguous term block [T r / p, T (r + 1) / p)
+        int64_t t0 = 0, t1 = 0;
+        qf_shard_range((int64_t)obs->w_re.size(), rank, world, &t0, &t1);
+        if (obs->shard_world != world || obs->shard_rank != rank) {
             obs->shard_dev[0].ready = obs->shard_dev[1].ready = false;
-            obs->shard_world = ctx->world;
+            obs->shard_world = world;
+            obs->shard_rank = rank;
         }
         od = &obs->shard_dev[prec];
-        rc = ensure_obs_dev(obs, prec, geo.kh, *od, t0, t1);
+        rc = ensure_obs_dev(obs, prec, geo.kh, *od, (int)t0, (int)t1);
     } else {
         rc = ensure_obs_dev(obs, prec, geo.kh, *od, 0, (int)obs->w_re.size());
     }
@@ -312,7 +360,8 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     static const bool graphs_off = std::getenv("QF_GRAPHS") && std::getenv("QF_GRAPHS")[0] == '0';
     if (bc >= batch && !ctx->timing && !graphs_off) {
         const std::vector<const void*> key = {
-            (const void*)prog->uid, (const void*)obs->uid, od, od->groups.p, od->terms.p, (const void*)(intptr_t)od->hj_state,
+            (const void*)prog->uid, (const void*)obs->uid, (const void*)od->gen, od, od->groups.p, od->terms.p,
+            (const void*)(intptr_t)od->hj_state, od->hj.kernel,
             od_im, (const void*)(intptr_t)batch, d_thetas, d_E, d_Eim, d_G, ctx->psi.p, ctx->lam.p, ctx->tap_part.p,
             ctx->tapsum.p, ctx->epart.p, ctx->gmat.p, ctx->zero_init.p, prog->init.p};
         if (ctx->graph_exec && key == ctx->graph_key) {
@@ -428,6 +477,14 @@ int forward_one(qf_ctx* ctx, qf_program* prog, const double* d_theta) {
 extern "C" {
 
 int qf_abi_version(void) { return QF_ABI_VERSION; }
+
+int qf_shard_range(int64_t count, int rank, int world, int64_t* begin, int64_t* end) {
+    if (!begin || !end || world < 1 || rank < 0 || rank >= world || count < 0)
+        return set_err(QF_EINVAL, "qf_shard_range: bad arguments");
+    *begin = count * rank / world;
+    *end = count * (rank + 1) / world;
+    return QF_OK;
+}
 const char* qf_last_error(void) { return g_err.c_str(); }
 
 int qf_ctx_create(int device, qf_ctx** out) {
@@ -566,6 +623,27 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
     if ((ce = upload(p->slot_taps, taps, s)) != cudaSuccess) return fail(ce);
     if ((ce = upload(p->slot_coef, coef, s)) != cudaSuccess) return fail(ce);
     if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return fail(ce);
+    // canonical algorithmic flops per amplitude of every sweep:
+    // 14 per dense one-qubit gate, 6 per diagonal gate, 30 per dense 4x4, 0 for
+    // permutations; the adjoint applies each gate to two states and adds 8 per
+    // gradient-tap inner product
+    for (int pi = 0; pi < 2; ++pi) {
+        const PassPlan& pp = pi ? p->plan.bwd : p->plan.fwd;
+        std::vector<double>& out = pi ? p->bwd_fpa : p->fwd_fpa;
+        for (const DevSweep& sw : pp.sweeps) {
+            double f = 0;
+            for (int o = sw.op_begin; o < sw.op_end; ++o) {
+                switch (pp.ops[o].kind) {
+                    case DK_G1: case DK_R1: case DK_RX: case DK_RS: f += 14.0 * (pi ? 2 : 1); break;
+                    case DK_D1: case DK_D2: f += 6.0 * (pi ? 2 : 1); break;
+                    case DK_G2: f += 30.0 * (pi ? 2 : 1); break;
+                    case DK_TX: case DK_TY: case DK_TZ: case DK_TZZ: f += 8.0; break;
+                    default: break;
+                }
+            }
+            out.push_back(f);
+        }
+    }
     const char* jit_env = std::getenv("QF_JIT");
     if (!(jit_env && jit_env[0] == '0') && !p->plan.gates.empty()) {
         p->use_jit = jit_build(p->plan, p->jf, p->jb, p->jst);
@@ -613,6 +691,9 @@ int qf_program_destroy(qf_program* p) {
     if (!p) return QF_OK;
     cudaSetDevice(p->ctx->device);
     cudaStreamSynchronize(p->ctx->stream);
+    if (!p->ctx->graph_key.empty() && p->ctx->graph_key[0] == (const void*)p->uid) drop_graph(p->ctx);
+    jit_release(p->jf.sweeps);  // unload its modules (shared ones stay loaded for their other users)
+    jit_release(p->jb.sweeps);
     for (DevBuf* b : {&p->gates, &p->cmats, &p->fwd.phases, &p->fwd.ops, &p->bwd.phases, &p->bwd.ops,
                       &p->slot_ptr, &p->slot_taps, &p->slot_coef, &p->goff_fwd, &p->goff_bwd, &p->init})
         b->release();
@@ -758,7 +839,9 @@ int qf_observable_destroy(qf_observable* o) {
     if (!o) return QF_OK;
     cudaSetDevice(o->ctx->device);
     cudaStreamSynchronize(o->ctx->stream);
+    if (o->ctx->graph_key.size() > 1 && o->ctx->graph_key[1] == (const void*)o->uid) drop_graph(o->ctx);
     for (auto* d : {&o->dev[0], &o->dev[1], &o->shard_dev[0], &o->shard_dev[1]}) {
+        jit_release(d->hj);
         d->groups.release();
         d->terms.release();
     }
@@ -770,10 +853,74 @@ static void reset_stats(qf_ctx* ctx) {
     resolve_events(ctx);
     ctx->launches = 0;
     for (int i = 0; i < 4; ++i) {
-        ctx->ms[i] = ctx->bytes[i] = 0;
+        ctx->ms[i] = ctx->bytes[i] = ctx->flops[i] = 0;
         ctx->class_launches[i] = 0;
     }
+    ctx->launch_ms.clear();
 }
+
+}  // extern "C"
+
+namespace qfcapi {
+
+// The contribution of `rank` of `world` to a batched evaluation, written into
+// the zero-padded [batch x (1 + P)] float64 device buffer d_out (energies, then
+// gradients): batch sharding evaluates rows [B r / p, B (r + 1) / p) and leaves
+// the other rows 0 (so the sum over ranks is exact: x + 0 = x); term sharding
+// evaluates every row on the rank's term block (energy and gradient are linear
+// in H).  The NCCL path all-reduces exactly this buffer.
+int eval_shard(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, const double* d_thetas, int rank,
+               int world, bool grads, double* d_out) {
+    const int P = prog->plan.n_params;
+    double* dE = d_out;
+    double* dG = grads ? d_out + batch : nullptr;
+    if (world > 1 && obs->term_shard)
+        return eval_device(ctx, prog, obs, batch, d_thetas, dE, nullptr, dG, true, rank, world);
+    int64_t b0 = 0, b1 = 0;
+    qf_shard_range(batch, rank, world, &b0, &b1);
+    if (world > 1)
+        QF_CUDA(cudaMemsetAsync(d_out, 0, (size_t)batch * (1 + (grads ? P : 0)) * 8, ctx->stream));
+    if (b1 <= b0) return QF_OK;
+    return eval_device(ctx, prog, obs, (int)(b1 - b0), d_thetas + (size_t)b0 * P, dE + b0, nullptr,
+                       dG ? dG + (size_t)b0 * P : nullptr, false, 0, 1);
+}
+
+int allreduce_out(qf_ctx* ctx, double* d_out, size_t count) {
+    const int r = g_nccl.allReduce(d_out, d_out, count, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream);
+    if (r) return set_err(QF_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(r));
+    return QF_OK;
+}
+
+// host-buffer evaluation of one (virtual) rank's share; collective when requested
+int eval_host(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, const double* thetas, int rank,
+              int world, bool collective, double* energies, double* grads) {
+    if (grads && !prog->plan.adjoint_ok) return set_err(QF_EINVAL, prog->plan.adjoint_error);
+    int rc = check_thetas(prog, batch, thetas);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    const int P = prog->plan.n_params;
+    rc = stage_thetas(ctx, prog, batch, thetas);
+    if (rc) return rc;
+    const size_t out_n = (size_t)batch * (1 + (grads ? P : 0));
+    QF_CUDA(ctx->out.reserve(out_n * 8));
+    double* d_out = (double*)ctx->out.p;
+    rc = eval_shard(ctx, prog, obs, batch, (const double*)ctx->thetas.p, rank, world, grads != nullptr, d_out);
+    if (rc) return rc;
+    if (collective) {
+        rc = allreduce_out(ctx, d_out, out_n);
+        if (rc) return rc;
+    }
+    QF_CUDA(ctx->pin.reserve(out_n * 8));
+    QF_CUDA(cudaMemcpyAsync(ctx->pin.p, d_out, out_n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    QF_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(energies, ctx->pin.p, (size_t)batch * 8);
+    if (grads) std::memcpy(grads, (double*)ctx->pin.p + batch, (size_t)batch * P * 8);
+    return QF_OK;
+}
+
+}  // namespace qfcapi
+
+extern "C" {
 
 int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
                          const double* thetas, double* energies, double* grads) {
@@ -782,46 +929,50 @@ int qf_energy_grad_batch(qf_ctx* ctx, const qf_program* cprog, const qf_observab
     if (!ctx || !prog || !obs || batch < 0 || (batch > 0 && (!energies || (!thetas && prog->plan.n_params))))
         return set_err(QF_EINVAL, "qf_energy_grad_batch: bad arguments");
     if (batch == 0) return QF_OK;
-    if (grads && !prog->plan.adjoint_ok) return set_err(QF_EINVAL, prog->plan.adjoint_error);
-    int rc = check_thetas(prog, batch, thetas);
-    if (rc) return rc;
-    cudaSetDevice(ctx->device);
-    const int P = prog->plan.n_params;
-    rc = stage_thetas(ctx, prog, batch, thetas);
-    if (rc) return rc;
-    // output: [E (batch)] [G (batch x P)]
-    const size_t out_n = (size_t)batch * (1 + (grads ? P : 0));
-    QF_CUDA(ctx->out.reserve(out_n * 8));
-    double* dE = (double*)ctx->out.p;
-    double* dG = grads ? dE + batch : nullptr;
     const bool sharded = ctx->comm != nullptr;
-    const bool term_shard = sharded && obs->term_shard;
-    if (sharded && !term_shard) {
-        // batch sharding: rank r owns rows [b0, b1); zero elsewhere; one all-reduce (exact: x + 0 = x)
-        const int b0 = (int)((long long)batch * ctx->rank / ctx->world);
-        const int b1 = (int)((long long)batch * (ctx->rank + 1) / ctx->world);
-        QF_CUDA(cudaMemsetAsync(ctx->out.p, 0, out_n * 8, ctx->stream));
-        if (b1 > b0) {
-            // evaluate rows b0..b1 into temp area then scatter: reuse thetas offset via pointer arithmetic
-            rc = eval_device(ctx, prog, obs, b1 - b0, (const double*)ctx->thetas.p + (size_t)b0 * P, dE + b0,
-                             nullptr, dG ? dG + (size_t)b0 * P : nullptr, false);
-            if (rc) return rc;
-        }
-    } else {
-        rc = eval_device(ctx, prog, obs, batch, (const double*)ctx->thetas.p, dE, nullptr, dG, term_shard);
-        if (rc) return rc;
-    }
-    if (sharded) {
-        int r = g_nccl.allReduce(ctx->out.p, ctx->out.p, out_n, kNcclFloat64, kNcclSum, ctx->comm, ctx->stream);
-        if (r) return set_err(QF_ENCCL, std::string("ncclAllReduce: ") + g_nccl.errStr(r));
-    }
-    QF_CUDA(ctx->pin.reserve(out_n * 8));
-    QF_CUDA(cudaMemcpyAsync(ctx->pin.p, ctx->out.p, out_n * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    QF_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(energies, ctx->pin.p, (size_t)batch * 8);
-    if (grads) std::memcpy(grads, (double*)ctx->pin.p + batch, (size_t)batch * P * 8);
+    return eval_host(ctx, prog, obs, batch, thetas, sharded ? ctx->rank : 0, sharded ? ctx->world : 1, sharded,
+                     energies, grads);
+}
+
+int qf_energy_grad_batch_partial(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
+                                 const double* thetas, int rank, int world, double* energies, double* grads) {
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    qf_observable* obs = const_cast<qf_observable*>(cobs);
+    if (!ctx || !prog || !obs || batch < 0 || world < 1 || rank < 0 || rank >= world ||
+        (batch > 0 && (!energies || (!thetas && prog->plan.n_params))))
+        return set_err(QF_EINVAL, "qf_energy_grad_batch_partial: bad arguments");
+    if (batch == 0) return QF_OK;
+    return eval_host(ctx, prog, obs, batch, thetas, rank, world, false, energies, grads);
+}
+
+}  // extern "C"
+
+namespace qfcapi {
+
+// device-buffer evaluation with the context's sharding (stream-ordered)
+int eval_entry_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, const double* d_thetas,
+                      double* d_energies, double* d_grads) {
+    if (!ctx->comm)
+        return eval_device(ctx, prog, obs, batch, d_thetas, d_energies, nullptr, d_grads, false, 0, 1);
+    // sharded: the rank's share into the zero-padded buffer, one all-reduce, then
+    // the caller's buffers (stream-ordered; no host sync)
+    const int P = prog->plan.n_params;
+    const size_t out_n = (size_t)batch * (1 + (d_grads ? P : 0));
+    QF_CUDA(ctx->out.reserve(out_n * 8));
+    double* d_out = (double*)ctx->out.p;
+    int rc = eval_shard(ctx, prog, obs, batch, d_thetas, ctx->rank, ctx->world, d_grads != nullptr, d_out);
+    if (rc) return rc;
+    rc = allreduce_out(ctx, d_out, out_n);
+    if (rc) return rc;
+    QF_CUDA(cudaMemcpyAsync(d_energies, d_out, (size_t)batch * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (d_grads)
+        QF_CUDA(cudaMemcpyAsync(d_grads, d_out + batch, (size_t)batch * P * 8, cudaMemcpyDeviceToDevice, ctx->stream));
     return QF_OK;
 }
+
+}  // namespace qfcapi
+
+extern "C" {
 
 int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch,
                                 const double* d_thetas, double* d_energies, double* d_grads) {
@@ -831,7 +982,89 @@ int qf_energy_grad_batch_device(qf_ctx* ctx, const qf_program* cprog, const qf_o
         return set_err(QF_EINVAL, "qf_energy_grad_batch_device: bad arguments");
     if (batch == 0) return QF_OK;
     cudaSetDevice(ctx->device);
-    return eval_device(ctx, prog, obs, batch, d_thetas, d_energies, nullptr, d_grads, false);
+    return eval_entry_device(ctx, prog, obs, batch, d_thetas, d_energies, d_grads);
+}
+
+int qf_vqe_run(qf_ctx* ctx, const qf_program* cprog, const qf_observable* cobs, int batch, const double* theta0,
+               int steps, double lr, int grad_mode, double fd_step, double* traces, double* final_thetas,
+               double* best_energy, int* best_index) {
+    // vqe_run (reference src/variational.cpp:103-143) with the whole batch resident:
+    // per step one batched energy (+ adjoint gradient, or one batched call over the
+    // 2P shifted parameter sets) and one Adam kernel; one host copy at the end.
+    qf_program* prog = const_cast<qf_program*>(cprog);
+    qf_observable* obs = const_cast<qf_observable*>(cobs);
+    if (!ctx || !prog || !obs || !theta0 || !traces || !final_thetas || !best_energy || !best_index)
+        return set_err(QF_EINVAL, "qf_vqe_run: null argument");
+    if (batch < 1) return set_err(QF_EINVAL, "vqe_run: empty batch");
+    if (steps < 1) return set_err(QF_EINVAL, "vqe_run: steps must be >= 1");
+    if (grad_mode < QF_GRAD_PARAMETER_SHIFT || grad_mode > QF_GRAD_ADJOINT)
+        return set_err(QF_EINVAL, "qf_vqe_run: bad gradient mode");
+    if (grad_mode == QF_GRAD_FINITE_DIFF && !(fd_step > 0.0))
+        return set_err(QF_EINVAL, "gradient: finite-diff step must be positive");
+    const int P = prog->plan.n_params;
+    if (grad_mode == QF_GRAD_ADJOINT && !prog->plan.adjoint_ok) return set_err(QF_EINVAL, prog->plan.adjoint_error);
+    if (grad_mode == QF_GRAD_PARAMETER_SHIFT)
+        for (const auto& gi : prog->plan.gates)
+            if (gi.g.slot >= 0 && !gi.gen)
+                return set_err(QF_EINVAL, "gradient: parameter not shift-eligible, use finite_diff");
+    int rc = check_thetas(prog, batch, theta0);
+    if (rc) return rc;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const size_t BP = (size_t)batch * P;
+    LocalBuf th, m, v, g, tr, sh, es;
+    QF_CUDA(th.reserve(std::max<size_t>(16, BP * 8)));
+    QF_CUDA(m.reserve(std::max<size_t>(16, BP * 8)));
+    QF_CUDA(v.reserve(std::max<size_t>(16, BP * 8)));
+    QF_CUDA(g.reserve(std::max<size_t>(16, BP * 8)));
+    QF_CUDA(tr.reserve((size_t)(steps + 1) * batch * 8));
+    QF_CUDA(cudaMemsetAsync(m.p, 0, std::max<size_t>(16, BP * 8), s));
+    QF_CUDA(cudaMemsetAsync(v.p, 0, std::max<size_t>(16, BP * 8), s));
+    QF_CUDA(cudaMemsetAsync(g.p, 0, std::max<size_t>(16, BP * 8), s));
+    if (BP) QF_CUDA(cudaMemcpyAsync(th.p, theta0, BP * 8, cudaMemcpyHostToDevice, s));
+    const bool shifted = grad_mode != QF_GRAD_ADJOINT && P > 0;
+    const double shift = grad_mode == QF_GRAD_PARAMETER_SHIFT ? M_PI / 2.0 : fd_step;
+    const double denom = grad_mode == QF_GRAD_PARAMETER_SHIFT ? 2.0 : 2.0 * fd_step;
+    if (shifted) {
+        QF_CUDA(sh.reserve(BP * 2 * P * 8));
+        QF_CUDA(es.reserve(BP * 2 * 8));
+    }
+    double* d_th = (double*)th.p;
+    double* d_tr = (double*)tr.p;
+    for (int st = 0; st < steps; ++st) {
+        double* d_e = d_tr + (size_t)st * batch;
+        if (grad_mode == QF_GRAD_ADJOINT) {
+            rc = eval_entry_device(ctx, prog, obs, batch, d_th, d_e, (double*)g.p);
+        } else {
+            rc = eval_entry_device(ctx, prog, obs, batch, d_th, d_e, nullptr);
+            if (!rc && shifted) {
+                QF_CUDA(launch_shift_thetas(batch, P, d_th, shift, (double*)sh.p, s));
+                rc = eval_entry_device(ctx, prog, obs, (int)(2 * BP), (const double*)sh.p, (double*)es.p, nullptr);
+                if (!rc) QF_CUDA(launch_shift_grad(batch, P, (const double*)es.p, denom, (double*)g.p, s));
+            }
+        }
+        if (rc) return rc;
+        const double c1 = 1.0 - std::pow(0.9, st + 1), c2 = 1.0 - std::pow(0.999, st + 1);
+        QF_CUDA(launch_adam((int)BP, d_th, (double*)m.p, (double*)v.p, (const double*)g.p, lr, 0.9, 0.999, 1e-8,
+                            c1, c2, s));
+        ctx->launches += 1 + (shifted ? 2 : 0);
+    }
+    rc = eval_entry_device(ctx, prog, obs, batch, d_th, d_tr + (size_t)steps * batch, nullptr);
+    if (rc) return rc;
+    std::vector<double> trh((size_t)(steps + 1) * batch);
+    QF_CUDA(cudaMemcpyAsync(trh.data(), d_tr, trh.size() * 8, cudaMemcpyDeviceToHost, s));
+    if (BP) QF_CUDA(cudaMemcpyAsync(final_thetas, d_th, BP * 8, cudaMemcpyDeviceToHost, s));
+    QF_CUDA(cudaStreamSynchronize(s));
+    *best_energy = INFINITY;
+    *best_index = -1;
+    for (int b = 0; b < batch; ++b) {
+        for (int st = 0; st <= steps; ++st) traces[(size_t)b * (steps + 1) + st] = trh[(size_t)st * batch + b];
+        if (trh[(size_t)steps * batch + b] < *best_energy) {  // strict <, first index wins (:133-141)
+            *best_energy = trh[(size_t)steps * batch + b];
+            *best_index = b;
+        }
+    }
+    return QF_OK;
 }
 
 int qf_run_state(qf_ctx* ctx, const qf_program* cprog, const double* theta, int guard_log2, double* amps_out) {
@@ -952,7 +1185,7 @@ int qf_expectation(qf_ctx* ctx, const qf_program* cprog, const qf_observable* co
     if (rc) return rc;
     QF_CUDA(ctx->out.reserve(32));
     double* dE = (double*)ctx->out.p;
-    rc = eval_device(ctx, prog, obs, 1, (const double*)ctx->thetas.p, dE, dE + 1, nullptr, false);
+    rc = eval_device(ctx, prog, obs, 1, (const double*)ctx->thetas.p, dE, dE + 1, nullptr, false, 0, 1);
     if (rc) return rc;
     QF_CUDA(cudaMemcpyAsync(out_re_im, dE, 16, cudaMemcpyDeviceToHost, ctx->stream));
     QF_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1093,7 +1326,29 @@ int qf_pauli_sum_to_coo(qf_ctx* ctx, const qf_observable* obs, int n_guard, int 
 
 int qf_ctx_set_timing(qf_ctx* ctx, int enabled) {
     if (!ctx) return set_err(QF_EINVAL, "null context");
-    ctx->timing = enabled != 0;
+    ctx->timing = enabled < 0 ? 0 : enabled;
+    return QF_OK;
+}
+
+int qf_ctx_flops(qf_ctx* ctx, double* flops_by_class) {
+    if (!ctx || !flops_by_class) return set_err(QF_EINVAL, "qf_ctx_flops: bad arguments");
+    for (int i = 0; i < 4; ++i) flops_by_class[i] = ctx->flops[i];
+    return QF_OK;
+}
+
+int qf_ctx_launch_times(qf_ctx* ctx, int cap, int* ids, double* ms, long long* counts, int* n) {
+    if (!ctx || !n || cap < 0) return set_err(QF_EINVAL, "qf_ctx_launch_times: bad arguments");
+    resolve_events(ctx);
+    int k = 0;
+    for (const auto& kv : ctx->launch_ms) {
+        if (k < cap) {
+            if (ids) ids[k] = kv.first;
+            if (ms) ms[k] = kv.second.first;
+            if (counts) counts[k] = kv.second.second;
+        }
+        ++k;
+    }
+    *n = k;
     return QF_OK;
 }
 

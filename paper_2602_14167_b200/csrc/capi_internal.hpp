@@ -169,6 +169,7 @@ struct qf_program {
     JitPass jf, jb;
     JitStats jst;
     uint64_t uid = 0;  // identity for the context's graph cache
+    std::vector<double> fwd_fpa, bwd_fpa;  // canonical flops per amplitude of each sweep
 };
 
 struct ObsDev {
@@ -177,6 +178,7 @@ struct ObsDev {
     bool ready = false;
     JitKernel hj;       // specialised H|psi> kernel (jit.hpp)
     int hj_state = 0;   // 0 not built, 1 ready, -1 unavailable (AOT hpsi_kernel)
+    uint64_t gen = 0;   // plan generation (process-unique; part of the graph-cache key)
 };
 
 struct qf_observable {
@@ -186,7 +188,7 @@ struct qf_observable {
     std::vector<double> w_re, w_im;
     ObsDev dev[2];         // per precision (tile bits differ)
     bool term_shard = false;
-    int shard_world = 0;   // term-sharded sub-plan cache key
+    int shard_world = 0, shard_rank = -1;  // term-sharded sub-plan cache key
     ObsDev shard_dev[2];
     uint64_t uid = 0;      // identity for the context's COO offset cache
 };
@@ -207,11 +209,13 @@ struct qf_ctx {
     int rank = 0, world = 1;
     // stats (accumulated until qf_ctx_reset_stats); timing uses event pairs
     // recorded on the context stream and resolved lazily (no mid-call syncs)
-    bool timing = false;
+    int timing = 0;  // 1: per kernel class, 2: + per launch (launch_ms)
+    std::map<int, std::pair<double, long long>> launch_ms;  // launch id -> (ms, count)
     long long launches = 0;
     long long class_launches[4] = {0, 0, 0, 0};
     double ms[4] = {0, 0, 0, 0};
     double bytes[4] = {0, 0, 0, 0};
+    double flops[4] = {0, 0, 0, 0};  // canonical algorithmic flops per class
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<std::pair<size_t, int>> pending;  // (start event index, class); end = start + 1

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <fcntl.h>
+#include <sys/file.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -64,6 +65,42 @@ struct BitSrc {
     std::string expr;   // runtime expression (0/1), when rb < 0
 };
 
+// A per-thread condition: parity(tid & tm) ^ parity(tile_base & bm).  Used for
+// deferred conditional relabelings: a cx whose control is a thread or tile bit
+// (constant over the thread's registers) is not applied with selects per
+// amplitude pair; the thread instead records "register label l holds amplitude
+// l ^ (cond << t)" and conjugates the later gates on that bit by X (a few
+// selects per gate), folding the relabeling into its store addresses.
+struct Cond {
+    uint32_t tm = 0, bm = 0;
+    bool any() const { return tm || bm; }
+    Cond& operator^=(const Cond& o) {
+        tm ^= o.tm;
+        bm ^= o.bm;
+        return *this;
+    }
+};
+
+std::string cond_expr(const Cond& c) {
+    auto one = [](const char* v, uint32_t m) {
+        if ((m & (m - 1)) == 0) {
+            int j = __builtin_ctz(m);
+            return std::string("((") + v + " >> " + std::to_string(j) + ") & 1u)";
+        }
+        return std::string("__popc(") + v + " & " + std::to_string(m) + "u)";
+    };
+    std::string e;
+    if (c.tm) e = one("tid", c.tm);
+    if (c.bm) e = e.empty() ? one("tile_base", c.bm) : "(" + e + " ^ " + one("tile_base", c.bm) + ")";
+    if (e.empty()) return "0u";
+    return "(" + e + " & 1u)";
+}
+
+bool env_flag(const char* name) {
+    const char* e = std::getenv(name);
+    return e && e[0] == '1';
+}
+
 }  // namespace
 
 // Persistent cp.async double-buffered variant: QF_JIT_PIPE=1 for every sweep,
@@ -118,12 +155,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const bool pipe = jit_pipe_mode(pass, si);
     Out o;
     if (pipe) o.s += "// qf-option: pipelined\n";
+    if (env_flag("QF_JIT_NOPACK")) o.s += "#define QF_NOPACK 1\n";
     o.s += kPrelude;
     o.s += "\n";
     o("namespace qfb {");
     const size_t decl_pos = o.s.size();  // namespace-scope tables are inserted here
     o("extern \"C\" __global__ void __launch_bounds__(%d, %d) qf_sweep(const SweepArgs a) {", T, minb);
     o("  typedef %s V; typedef %s RT;", Vt, RTt);
+    const size_t sdecl_pos = o.s.size();  // function-scope static tables (diagonal-run products)
     o("  extern __shared__ __align__(16) unsigned char smem_raw[];");
     const unsigned TSZ = (1u << k) * (bwd ? 2u : 1u);  // one tile buffer (psi [+ lambda])
     const int S = jit_tap_stage(P, pass, si, bwd);
@@ -260,8 +299,13 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         o("    const V* gm = reinterpret_cast<const V*>(a.gmat) + (size_t)b * a.gmat_stride + a.gmat_pass_base + %d;",
           sw.mbase);
         o("    for (int i = (int)tid; i < %d; i += %d) smat[i] = gm[i];", sw.n_mat, T);
-        o("  }");
     }
+    // Uniform (per-state) products of a diagonal run's register-bit factors are
+    // built once per CTA into shared memory, straight from the global matrix
+    // table (the prologue is inserted here once every run is known; each entry
+    // lists its factor indices), behind the same barrier as the matrices.
+    const size_t stab_pos = o.s.size();
+    if (!pipe) o("  }");
     if (!direct_first && !pipe) {
         for (int j = 0; j < NR; ++j) {
             if (bwd)
@@ -272,10 +316,6 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
     }
     if (!pipe) o("  __syncthreads();");
-    // Uniform (per-state) products of a diagonal run's register-bit factors are
-    // built once per CTA into shared memory (the prologue is inserted here once
-    // every run is known); each entry lists its factor indices into smat.
-    const size_t stab_pos = o.s.size();
     auto env_off = [](const char* name) {
         const char* e = std::getenv(name);
         return e && e[0] == '1';
@@ -284,16 +324,17 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const bool use_ratio = bwd && !env_off("QF_JIT_NORATIO");
     const bool use_hoist = !env_off("QF_JIT_NOHOIST");
     const bool use_lazy = !env_off("QF_JIT_NOLAZY");
+    const bool use_defer = !env_off("QF_JIT_NODEFER");
     std::vector<std::vector<int>> stab_entries;
 
     std::vector<const char*> arrs = {"x"};
     if (bwd) arrs.push_back("y");
     int uid = 0;  // unique names inside fused blocks
-    auto emit_flush = [&](int first, int cnt) {
+    auto emit_flush = [&](int first, int cnt, bool last = false) {
         o("    __syncthreads();");
         o("    tap_flush<RT>(stg, %d, %d, a.tap_part + ((size_t)b * a.n_taps_total + %d) * ntiles + tile_id, ntiles);",
           cnt, T, sw.tap_begin + first);
-        o("    __syncthreads();");
+        if (!last) o("    __syncthreads();");  // the staging slots are reused
     };
     auto emit_flush_if_full = [&](int tap) {
         if (tap % S == S - 1) emit_flush(tap - (S - 1), S);
@@ -356,6 +397,23 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 if (!((l >> tbit) & 1) && (cbit < 0 || ((l >> cbit) & 1))) std::swap(phys[l], phys[l | (1 << tbit)]);
         };
         auto is_diagish = [&](uint8_t kd) { return kd == DK_D1 || kd == DK_D2 || kd == DK_TZ || kd == DK_TZZ; };
+        // deferred conditional relabelings of the register bits (see Cond)
+        std::vector<Cond> cond(R);
+        auto ext_cond = [&](int pos) {  // condition "memory bit pos is 1" for a non-register bit
+            Cond c;
+            const int tl = pos < 64 ? tl_of_pos[pos] : -1;
+            if (tl >= 0) c.tm = 1u << thr_of_tl[tl];
+            else c.bm = 1u << pos;
+            return c;
+        };
+        auto materialize = [&](int r) {  // apply a pending relabeling with selects
+            if (r < 0 || !cond[r].any()) return;
+            o("    { const bool c = %s != 0u;", cond_expr(cond[r]).c_str());
+            for (const char* A : arrs)
+                for (auto pr : pairs(r)) o("      jcswap(%s%d, %s%d, c);", A, pr.first, A, pr.second);
+            o("    }");
+            cond[r] = Cond{};
+        };
 
         // ---- fused run of diagonal gates and Z-type taps (they all commute) ----
         auto flush_diag_run = [&](const std::vector<int>& run) {
@@ -444,10 +502,15 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     if (s0.rb >= 0) m ^= 1 << s0.rb;
                     if (op.kind == DK_TZZ && s1.rb >= 0) m ^= 1 << s1.rb;
                     o("      { RT s = %s;", wsum.at(m).c_str());
-                    std::string rt;
-                    if (s0.rb < 0) rt = s0.expr;
-                    if (op.kind == DK_TZZ && s1.rb < 0) rt = rt.empty() ? s1.expr : "(" + rt + " ^ " + s1.expr + ")";
-                    if (!rt.empty()) o("        if (%s) s = -s;", rt.c_str());
+                    // sign: bits outside the registers, and relabeled register bits
+                    Cond sc;
+                    if (s0.rb < 0) sc ^= ext_cond(op.pos0);
+                    else sc ^= cond[s0.rb];
+                    if (op.kind == DK_TZZ) {
+                        if (s1.rb < 0) sc ^= ext_cond(op.pos1);
+                        else sc ^= cond[s1.rb];
+                    }
+                    if (sc.any()) o("        if (%s) s = -s;", cond_expr(sc).c_str());
                     o("        stg[%d * %d + tid] = s; }", op.tap % S, T);
                     emit_flush_if_full(op.tap);
                     continue;
@@ -498,6 +561,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     if (used) ubits.push_back(r);
                     for (auto& pi : perbit_idx[r]) uniform &= pi.first >= 0;
                 }
+                uint32_t cbits = 0;  // ubits (by index) carrying a pending relabeling
+                for (size_t bi = 0; bi < ubits.size(); ++bi)
+                    if (cond[ubits[bi]].any()) cbits |= 1u << bi;
+                if (!uniform || ubits.empty())
+                    for (int r : ubits) materialize(r);  // per-thread tables index by label
                 if (uniform && !ubits.empty()) {
                     // Adjoint pass: only conj(lambda) psi products are ever used, so each
                     // single-qubit diagonal may carry its own global phase: diag(d0, d1)
@@ -506,6 +574,20 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     const int kRatio = 0x8000;
                     const int ne = 1 << ubits.size();
                     std::vector<int> slot(ne, -1);
+                    if (cbits) {
+                        // A relabeled bit either indexes the table at run time (dense: the
+                        // identity entries are no longer skipped) or is materialised with
+                        // selects first; pick the cheaper (FMA-pipe work weighs double).
+                        int empties = 0;
+                        if (use_ratio && !have_c && d2s.empty()) empties = 1;  // e = 0 only
+                        const int extra = empties * (NR / ne) * (int)arrs.size();      // jcmul = 2 FMA-pipe instrs
+                        const int fsel = __builtin_popcount(cbits) * 2 * NR * (int)arrs.size();
+                        if (extra * 4 >= fsel) {
+                            for (size_t bi = 0; bi < ubits.size(); ++bi)
+                                if ((cbits >> bi) & 1u) materialize(ubits[bi]);
+                            cbits = 0;
+                        }
+                    }
                     for (int e = 0; e < ne; ++e) {
                         std::vector<int> f;
                         for (size_t bi = 0; bi < ubits.size(); ++bi)
@@ -523,9 +605,38 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                             const int i1 = (int)(std::find(ubits.begin(), ubits.end(), d.r1) - ubits.begin());
                             f.push_back(d.moff + (((e >> i0) & 1) << 1 | ((e >> i1) & 1)));
                         }
-                        if (f.empty()) continue;  // identity
+                        if (f.empty() && !cbits) continue;  // identity (dense table when indexed at run time)
                         slot[e] = (int)stab_entries.size();
                         stab_entries.push_back(f);
+                    }
+                    if (cbits) {
+                        std::string em;
+                        for (size_t bi = 0; bi < ubits.size(); ++bi)
+                            if ((cbits >> bi) & 1u)
+                                em += (em.empty() ? "" : " | ") + std::string("(") + cond_expr(cond[ubits[bi]]) + " << " +
+                                      std::to_string(bi) + ")";
+                        o("      const uint32_t em%d = %s;", id, em.c_str());
+                        for (int e = 0; e < ne; ++e) {
+                            if (have_c) {
+                                if (e == 0) {
+                                    o("      V c%d = %s;", id, rt_factors[0].c_str());
+                                    for (size_t q = 1; q < rt_factors.size(); ++q)
+                                        o("      c%d = cmul(c%d, %s);", id, id, rt_factors[q].c_str());
+                                }
+                                o("      const V u%d_%d = jcmul(stab[%d + (%du ^ em%d)], c%d);", id, e, slot[0], e, id, id);
+                            } else {
+                                o("      const V u%d_%d = stab[%d + (%du ^ em%d)];", id, e, slot[0], e, id);
+                            }
+                        }
+                        for (const char* A : arrs)
+                            for (int l = 0; l < NR; ++l) {
+                                int e = 0;
+                                for (size_t bi = 0; bi < ubits.size(); ++bi)
+                                    if ((l >> ubits[bi]) & 1) e |= 1 << bi;
+                                o("      %s%d = jcmul(%s%d, u%d_%d);", A, phys[l], A, phys[l], id, e);
+                            }
+                        o("    }");
+                        return;
                     }
                     if (have_c) {
                         o("      V c%d = %s;", id, rt_factors[0].c_str());
@@ -700,6 +811,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             }
             switch (op.kind) {
                 case DK_G1: case DK_R1: case DK_RX: {
+                    if (op.kind != DK_RX && cond[op.rb0].any()) {  // X G X = [[m3, m2], [m1, m0]]
+                        o("    { const V a0 = smat[%d], a1 = smat[%d], a2 = smat[%d], a3 = smat[%d]; const bool cc = %s != 0u;",
+                          op.moff, op.moff + 1, op.moff + 2, op.moff + 3, cond_expr(cond[op.rb0]).c_str());
+                        o("      const V m0 = cc ? a3 : a0, m1 = cc ? a2 : a1, m2 = cc ? a1 : a2, m3 = cc ? a0 : a3;");
+                    } else  // rx commutes with X
                     o("    { const V m0 = smat[%d], m1 = smat[%d], m2 = smat[%d], m3 = smat[%d]; (void)m1; (void)m2; (void)m3;",
                       op.moff, op.moff + 1, op.moff + 2, op.moff + 3);
                     for (const char* A : arrs)
@@ -714,6 +830,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     break;
                 }
                 case DK_RS: {
+                    if (cond[op.rb0].any())  // X R(theta) X = R(-theta): negate the shear parameters
+                        o("    { V m0 = smat[%d]; if (%s) { m0.x = -m0.x; m0.y = -m0.y; }", op.moff,
+                          cond_expr(cond[op.rb0]).c_str());
+                    else
                     o("    { const V m0 = smat[%d];", op.moff);
                     for (const char* A : arrs)
                         for (auto pr : pairs(op.rb0)) o("      jrs(%s%d, %s%d, m0);", A, pr.first, A, pr.second);
@@ -725,7 +845,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     break;
                 case DK_CX:
                     if (op.rb1 >= 0) {
+                        // X_c CX X_c = X_t CX: a relabeled control passes its condition to the target
+                        cond[op.rb0] ^= cond[op.rb1];
                         rename(op.rb0, op.rb1);
+                    } else if (use_defer) {
+                        cond[op.rb0] ^= ext_cond(op.pos0);
                     } else {
                         BitSrc c = src(op.pos0);
                         o("    { const bool c = %s != 0u;", c.expr.c_str());
@@ -738,6 +862,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                     flush_diag_run(std::vector<int>{oi});
                     break;
                 case DK_G2: {
+                    materialize(op.rb0);
+                    materialize(op.rb1);
                     o("    { const V* m = smat + %d;", op.moff);
                     const int e0 = 1 << op.rb0, e1 = 1 << op.rb1;
                     for (const char* A : arrs)
@@ -765,6 +891,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         }
                         if (op.kind == DK_TX)
                             o("      stg[%d * %d + tid] = (P.x - P.y) + (M.x - M.y); }", op.tap % S, T);
+                        else if (cond[op.rb0].any())  // X Y X = -Y
+                            o("      const RT t_ = (P.x + P.y) - (M.x + M.y); stg[%d * %d + tid] = %s ? -t_ : t_; }", op.tap % S,
+                              T, cond_expr(cond[op.rb0]).c_str());
                         else
                             o("      stg[%d * %d + tid] = (P.x + P.y) - (M.x + M.y); }", op.tap % S, T);
                         emit_flush_if_full(op.tap);
@@ -778,6 +907,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                         for (auto pr : pairs(op.rb0))
                             o("      s += recv(y%d, x%d) - recv(y%d, x%d);", pr.second, pr.first, pr.first, pr.second);
                     }
+                    if (op.kind == DK_TY && cond[op.rb0].any()) o("      if (%s) s = -s;", cond_expr(cond[op.rb0]).c_str());
                     o("      stg[%d * %d + tid] = s; }", op.tap % S, T);
                     emit_flush_if_full(op.tap);
                     break;
@@ -788,22 +918,35 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             ++oi;
         }
         flush_pending();
+        // pending relabelings become store-address XORs (register label l holds l ^ cond)
+        std::string gx, sx;
+        for (int r = 0; r < R; ++r) {
+            if (!cond[r].any()) continue;
+            const std::string c = cond_expr(cond[r]);
+            gx += " ^ ((0u - " + c + ") & " + std::to_string(1u << sw.tb[(int)ph.reg_tl[r]]) + "u)";
+            sx += " ^ ((0u - " + c + ") & " + std::to_string(swz_host(1u << ph.reg_tl[r], W)) + "u)";
+        }
         if (dlast) {
             emit_gbase(ph, "g_pl");
+            if (!gx.empty()) o("    const uint32_t g_x = 0u%s;", gx.c_str());
             for (int l = 0; l < NR; ++l) {
                 const uint32_t off = reg_goff(ph, l);
+                const std::string a = gx.empty() ? "g_pl | " + std::to_string(off) + "u"
+                                                 : "(g_pl | " + std::to_string(off) + "u) ^ g_x";
                 if (bwd)
-                    o("    st[g_pl | %uu] = x%d; lm[g_pl | %uu] = y%d;", off, phys[l], off, phys[l]);
+                    o("    st[%s] = x%d; lm[%s] = y%d;", a.c_str(), phys[l], a.c_str(), phys[l]);
                 else
-                    o("    st[g_pl | %uu] = x%d;", off, phys[l]);
+                    o("    st[%s] = x%d;", a.c_str(), phys[l]);
             }
             o("  }");
         } else {
+            if (!sx.empty()) o("    const uint32_t s_w = s_t%s;", sx.c_str());
+            const char* sb = sx.empty() ? "s_t" : "s_w";
             for (int l = 0; l < NR; ++l) {
                 if (bwd)
-                    o("    tile[s_t ^ %uu] = x%d; tile2[s_t ^ %uu] = y%d;", offs[l], phys[l], offs[l], phys[l]);
+                    o("    tile[%s ^ %uu] = x%d; tile2[%s ^ %uu] = y%d;", sb, offs[l], phys[l], sb, offs[l], phys[l]);
                 else
-                    o("    tile[s_t ^ %uu] = x%d;", offs[l], phys[l]);
+                    o("    tile[%s ^ %uu] = x%d;", sb, offs[l], phys[l]);
             }
             o("    __syncthreads();");
             o("  }");
@@ -826,7 +969,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     }
     if (bwd && sw.n_taps % std::max(S, 1) != 0) {
         const int rem = sw.n_taps % S;
-        emit_flush(sw.n_taps - rem, rem);
+        emit_flush(sw.n_taps - rem, rem, !pipe);
     }
     if (pipe) {
         o("  __syncthreads();");
@@ -852,21 +995,19 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         decl += "};\n";
         char buf[1024];
         snprintf(buf, sizeof buf,
-                 "  __shared__ __align__(16) V stab[%zu];\n"
-                 "  for (int e = (int)tid; e < %zu; e += %d) {  // diagonal-run tables (uniform per state)\n"
-                 "    V acc; acc.x = 1; acc.y = 0;\n"
-                 "    for (int q = 0; q < %zu; ++q) {\n"
-                 "      const unsigned i = qf_stab_f[e][q];\n"
-                 "      if (i == 0xffffu) break;\n"
-
-                 "      if (i & 0x8000u) { V d0 = smat[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(smat[(i & 0x7fffu) + 1], d0)); }\n"
-                 "      else acc = cmul(acc, smat[i]);\n"
-                 "    }\n"
-                 "    stab[e] = acc;\n"
-                 "  }\n"
-                 "  __syncthreads();\n",
-                 ne, ne, T, nf);
-        o.s.insert(stab_pos, buf);
+                 "    for (int e = (int)tid; e < %zu; e += %d) {  // diagonal-run tables (uniform per state)\n"
+                 "      V acc; acc.x = 1; acc.y = 0;\n"
+                 "      for (int q = 0; q < %zu; ++q) {\n"
+                 "        const unsigned i = qf_stab_f[e][q];\n"
+                 "        if (i == 0xffffu) break;\n"
+                 "        if (i & 0x8000u) { V d0 = gm[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(gm[(i & 0x7fffu) + 1], d0)); }\n"
+                 "        else acc = cmul(acc, gm[i]);\n"
+                 "      }\n"
+                 "      stab[e] = acc;\n"
+                 "    }\n",
+                 ne, T, nf);
+        o.s.insert(stab_pos, buf);  // (stab_pos > sdecl_pos > decl_pos: insert back to front)
+        o.s.insert(sdecl_pos, "  __shared__ __align__(16) V stab[" + std::to_string(ne) + "];\n");
         o.s.insert(decl_pos, decl);
     }
     return o.s;
@@ -898,6 +1039,7 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
     while ((1 << LT) < T) ++LT;
     const size_t N = (size_t)1 << O.n;
     Out o;
+    if (env_flag("QF_JIT_NOPACK")) o.s += "#define QF_NOPACK 1\n";
     o.s += kPrelude;
     o.s += "\n";
     o("namespace qfb {");
@@ -1083,6 +1225,20 @@ bool read_file(const std::string& p, std::string& out) {
     return !out.empty();
 }
 
+// Writes a cache entry atomically; a failed or short write is discarded.
+void publish_cubin(const std::string& path, const std::string& cubin, const std::string& tag) {
+    const std::string tmp = path + ".tmp" + std::to_string(getpid()) + tag;
+    bool ok;
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        f.write(cubin.data(), (std::streamsize)cubin.size());
+        f.flush();
+        ok = f.good();
+    }
+    if (ok) ok = rename(tmp.c_str(), path.c_str()) == 0;
+    if (!ok) unlink(tmp.c_str());
+}
+
 bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
     if (const char* d = std::getenv("QF_JIT_DUMP")) {  // debugging: keep the generated source and cubin
         const std::string base = std::string(d) + "/qf_" + std::to_string(fnv1a(src));
@@ -1112,6 +1268,46 @@ bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
     return true;
 }
 
+// ---- process-wide module table (see jit.hpp) ----
+struct Module {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    int refs = 0;
+};
+std::map<std::string, Module> g_modules;
+std::mutex g_modules_mu;
+
+// Loads (or shares) the module of `key`; false + err on failure (the caller
+// treats a cached cubin that fails to load as corrupt).
+bool module_acquire(const std::string& key, const std::string& cubin, const char* name, cudaKernel_t& kern,
+                    std::string& err) {
+    std::lock_guard<std::mutex> lk(g_modules_mu);
+    auto it = g_modules.find(key);
+    if (it != g_modules.end()) {
+        it->second.refs++;
+        kern = it->second.kern;
+        return true;
+    }
+    Module m;
+    cudaError_t e = cudaLibraryLoadData(&m.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        return false;
+    }
+    e = cudaLibraryGetKernel(&m.kern, m.lib, name);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaLibraryUnload(m.lib);
+        err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+        return false;
+    }
+    m.refs = 1;
+    kern = m.kern;
+    g_modules[key] = m;
+    return true;
+}
+
 struct Job {
     const ProgramPlan* P;
     const PassPlan* pass;
@@ -1122,6 +1318,22 @@ struct Job {
 };
 
 }  // namespace
+
+void jit_release(JitKernel& k) {
+    if (k.module.empty()) return;
+    std::lock_guard<std::mutex> lk(g_modules_mu);
+    auto it = g_modules.find(k.module);
+    if (it != g_modules.end() && --it->second.refs == 0) {
+        cudaLibraryUnload(it->second.lib);
+        g_modules.erase(it);
+    }
+    k.module.clear();
+    k.kernel = nullptr;
+}
+
+void jit_release(std::vector<JitKernel>& ks) {
+    for (auto& k : ks) jit_release(k);
+}
 
 bool jit_compile_source(const std::string& src, std::string& cubin, std::string& err) {
     {
@@ -1159,14 +1371,7 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     std::vector<std::string> srcs(jobs.size()), paths(jobs.size());
     std::vector<size_t> deferred;
     std::mutex def_mu;
-    auto publish = [&](size_t j) {
-        const std::string tmp = paths[j] + ".tmp" + std::to_string(getpid()) + "_" + std::to_string(j);
-        {
-            std::ofstream f(tmp, std::ios::binary);
-            f.write(jobs[j].cubin.data(), (std::streamsize)jobs[j].cubin.size());
-        }
-        rename(tmp.c_str(), paths[j].c_str());
-    };
+    auto publish = [&](size_t j) { publish_cubin(paths[j], jobs[j].cubin, "_" + std::to_string(j)); };
     std::atomic<size_t> next{0};
     auto worker = [&] {
         for (;;) {
@@ -1181,21 +1386,24 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
                 jb.from_cache = true;
                 continue;
             }
+            // claim: an advisory flock on the lock file (released by the kernel if
+            // the holder dies, so an abandoned claim never stalls later builds)
             const std::string lock = paths[j] + ".lock";
-            int fd = open(lock.c_str(), O_CREAT | O_EXCL | O_WRONLY, 0644);
-            if (fd < 0) {
-                struct stat stl;
-                const bool stale = stat(lock.c_str(), &stl) == 0 && time(nullptr) - stl.st_mtime > 300;
-                if (!stale) {
-                    std::lock_guard<std::mutex> lk(def_mu);
-                    deferred.push_back(j);
-                    continue;
-                }
-            }
-            if (compile_one(srcs[j], jb.cubin, jb.err)) publish(j);
-            if (fd >= 0) {
+            const int fd = open(lock.c_str(), O_CREAT | O_RDWR, 0644);
+            if (fd >= 0 && flock(fd, LOCK_EX | LOCK_NB) != 0) {
                 close(fd);
-                unlink(lock.c_str());
+                std::lock_guard<std::mutex> lk(def_mu);
+                deferred.push_back(j);
+                continue;
+            }
+            if (!read_file(paths[j], jb.cubin)) {  // re-check under the claim
+                if (compile_one(srcs[j], jb.cubin, jb.err)) publish(j);
+            } else {
+                jb.from_cache = true;
+            }
+            if (fd >= 0) {
+                flock(fd, LOCK_UN);
+                close(fd);
             }
         }
     };
@@ -1213,22 +1421,18 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
             if (d >= deferred.size()) return;
             const size_t j = deferred[d];
             Job& jb = jobs[j];
+            // wait for the holder's claim (blocking flock: returns when it finishes or dies)
             const std::string lock = paths[j] + ".lock";
-            const auto t_wait = std::chrono::steady_clock::now();
-            for (;;) {
-                if (read_file(paths[j], jb.cubin)) {
-                    jb.from_cache = true;
-                    break;
-                }
-                struct stat stl;
-                const bool held = stat(lock.c_str(), &stl) == 0;
-                if (!held || std::chrono::steady_clock::now() - t_wait > std::chrono::seconds(600)) {
-                    // the holder finished without a cubin (compile error: reproduce it here) or is stuck
-                    if (read_file(paths[j], jb.cubin)) jb.from_cache = true;
-                    else if (compile_one(srcs[j], jb.cubin, jb.err)) publish(j);
-                    break;
-                }
-                std::this_thread::sleep_for(std::chrono::milliseconds(50));
+            const int fd = open(lock.c_str(), O_CREAT | O_RDWR, 0644);
+            if (fd >= 0) flock(fd, LOCK_EX);
+            if (read_file(paths[j], jb.cubin)) {
+                jb.from_cache = true;
+            } else if (compile_one(srcs[j], jb.cubin, jb.err)) {  // holder failed: reproduce the error here
+                publish(j);
+            }
+            if (fd >= 0) {
+                flock(fd, LOCK_UN);
+                close(fd);
             }
         }
     };
@@ -1237,36 +1441,37 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     for (auto& t : pool) t.join();
     fwd.sweeps.assign(P.fwd.sweeps.size(), {});
     bwd.sweeps.assign(P.bwd.sweeps.size(), {});
+    auto fail = [&](const std::string& e) {  // releases every module acquired so far
+        st.error = e;
+        jit_release(fwd.sweeps);
+        jit_release(bwd.sweeps);
+        return false;
+    };
     for (auto& jb : jobs) {
-        if (!jb.err.empty()) {
-            st.error = jb.err;
-            return false;
-        }
-        cudaLibrary_t lib;
-        cudaError_t e = cudaLibraryLoadData(&lib, jb.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-        if (e != cudaSuccess) {
-            st.error = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
-            return false;
-        }
+        if (!jb.err.empty()) return fail(jb.err);
         cudaKernel_t kern;
-        e = cudaLibraryGetKernel(&kern, lib, "qf_sweep");
-        if (e != cudaSuccess) {
-            st.error = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
-            return false;
+        std::string lerr;
+        const size_t jidx = (size_t)(&jb - jobs.data());
+        if (!module_acquire(paths[jidx], jb.cubin, "qf_sweep", kern, lerr)) {
+            // a truncated / corrupt cache entry: drop it and compile afresh
+            unlink(paths[jidx].c_str());
+            if (!jb.from_cache || !compile_one(srcs[jidx], jb.cubin, jb.err)) return fail(jb.err.empty() ? lerr : jb.err);
+            publish(jidx);
+            jb.from_cache = false;
+            if (!module_acquire(paths[jidx], jb.cubin, "qf_sweep", kern, lerr)) return fail(lerr);
         }
-        JitKernel jk;
+        JitKernel& jk = (jb.bwd ? bwd : fwd).sweeps[jb.si];
         jk.kernel = (void*)kern;
+        jk.module = paths[jidx];
         const DevSweep& sw = jb.pass->sweeps[jb.si];
         jk.threads = 1 << (sw.k - sw.R);
         jk.smem = jit_smem_bytes(P, *jb.pass, jb.si, jb.bwd);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, (const void*)kern);
         if (jk.smem + fa.sharedSizeBytes > 48 * 1024) {  // static tables count against the 48 KB default
-            e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
-            if (e != cudaSuccess) {
-                st.error = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-                return false;
-            }
+            const cudaError_t e =
+                cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jk.smem);
+            if (e != cudaSuccess) return fail(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
         }
         jk.pipe = jit_pipe_mode(*jb.pass, jb.si);
         if (jk.pipe) {
@@ -1278,7 +1483,6 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
                 per = 1;
             jk.ctas = sms * per;
         }
-        (jb.bwd ? bwd : fwd).sweeps[jb.si] = jk;
         if (jb.from_cache) st.cached++;
         else st.compiled++;
     }
@@ -1304,28 +1508,22 @@ bool jit_build_hpsi(const ObservablePlan& O, int prec, JitKernel& out, std::stri
     snprintf(key, sizeof key, "%016llx_%d_%d", (unsigned long long)fnv1a(src), maj, min);
     const std::string path = dir + "/" + key + ".cubin";
     std::string cubin;
-    if (!read_file(path, cubin)) {
+    bool cached = read_file(path, cubin);
+    if (!cached) {
         if (!compile_one(src, cubin, err)) return false;
-        const std::string tmp = path + ".tmp" + std::to_string(getpid());
-        {
-            std::ofstream f(tmp, std::ios::binary);
-            f.write(cubin.data(), (std::streamsize)cubin.size());
-        }
-        rename(tmp.c_str(), path.c_str());
-    }
-    cudaLibrary_t lib;
-    cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-    if (e != cudaSuccess) {
-        err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
-        return false;
+        publish_cubin(path, cubin, "");
     }
     cudaKernel_t kern;
-    e = cudaLibraryGetKernel(&kern, lib, "qf_hpsi");
-    if (e != cudaSuccess) {
-        err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
-        return false;
+    if (!module_acquire(path, cubin, "qf_hpsi", kern, err)) {
+        unlink(path.c_str());  // corrupt cache entry: recompile once
+        if (!cached || !compile_one(src, cubin, err)) return false;
+        publish_cubin(path, cubin, "");
+        if (!module_acquire(path, cubin, "qf_hpsi", kern, err)) return false;
     }
+    cudaError_t e;
+    jit_release(out);
     out.kernel = (void*)kern;
+    out.module = path;
     out.threads = jit_hpsi_threads(O);
     out.smem = jit_hpsi_smem(O, prec);
     if (out.smem > 48 * 1024) {

@@ -21,7 +21,15 @@ struct JitKernel {
     size_t smem = 0;
     bool pipe = false;       // persistent, cp.async double-buffered variant
     int ctas = 0;            // resident CTAs (pipe mode grid)
+    std::string module;      // key of the loaded module in the process-wide table ("" = none)
 };
+
+// Loaded modules are shared process-wide by source hash (identical kernels of
+// different programs load once) and reference-counted: every JitKernel that
+// holds one is released exactly once (program / observable destruction, plan
+// rebuild), and the module is unloaded with its last user.
+void jit_release(JitKernel& k);
+void jit_release(std::vector<JitKernel>& ks);
 
 bool jit_pipe_mode(const PassPlan& pass, int si);
 

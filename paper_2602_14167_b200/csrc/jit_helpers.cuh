@@ -32,23 +32,37 @@ template <typename V> __device__ __forceinline__ V mk_basis(bool one) {
 
 __device__ __forceinline__ float2 swp(float2 a) { return make_float2(a.y, a.x); }
 
+// QF_NOPACK: the same arithmetic with scalar FP32 instructions (3-register FFMA)
+// instead of the packed FFMA2/FMUL2 forms (A/B of the two FP32 issue paths).
+#ifdef QF_NOPACK
+__device__ __forceinline__ float2 qf_ffma2(float2 a, float2 b, float2 c) {
+    return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+__device__ __forceinline__ float2 qf_fmul2(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 qf_fadd2(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+#else
+__device__ __forceinline__ float2 qf_ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 qf_fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 qf_fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+#endif
+
 
 // a * d (complex)
 __device__ __forceinline__ float2 jcmul(float2 a, float2 d) {
-    return __ffma2_rn(swp(a), make_float2(-d.y, d.y), __fmul2_rn(a, make_float2(d.x, d.x)));
+    return qf_ffma2(swp(a), make_float2(-d.y, d.y), qf_fmul2(a, make_float2(d.x, d.x)));
 }
 __device__ __forceinline__ double2 jcmul(double2 a, double2 d) { return cmul(a, d); }
 // acc + a * d (complex)
 __device__ __forceinline__ float2 jcfma(float2 a, float2 d, float2 acc) {
-    return __ffma2_rn(swp(a), make_float2(-d.y, d.y), __ffma2_rn(a, make_float2(d.x, d.x), acc));
+    return qf_ffma2(swp(a), make_float2(-d.y, d.y), qf_ffma2(a, make_float2(d.x, d.x), acc));
 }
 __device__ __forceinline__ double2 jcfma(double2 a, double2 d, double2 acc) { return cfma(d, a, acc); }
 
 // real 2x2 [[m0, m1], [m2, m3]] (real parts) on (a0, a1)
 __device__ __forceinline__ void jr1(float2& a0, float2& a1, float2 m0, float2 m1, float2 m2, float2 m3) {
     const float2 t0 = a0, t1 = a1;
-    a0 = __ffma2_rn(t1, make_float2(m1.x, m1.x), __fmul2_rn(t0, make_float2(m0.x, m0.x)));
-    a1 = __ffma2_rn(t1, make_float2(m3.x, m3.x), __fmul2_rn(t0, make_float2(m2.x, m2.x)));
+    a0 = qf_ffma2(t1, make_float2(m1.x, m1.x), qf_fmul2(t0, make_float2(m0.x, m0.x)));
+    a1 = qf_ffma2(t1, make_float2(m3.x, m3.x), qf_fmul2(t0, make_float2(m2.x, m2.x)));
 }
 __device__ __forceinline__ void jr1(double2& a0, double2& a1, double2 m0, double2 m1, double2 m2, double2 m3) {
     const double2 t0 = a0, t1 = a1;
@@ -67,8 +81,8 @@ template <typename V> __device__ __forceinline__ void jg1(V& a0, V& a1, V m0, V 
 __device__ __forceinline__ void jrx(float2& a0, float2& a1, float2 m0) {
     const float2 t0 = a0, t1 = a1;
     const float2 cc = make_float2(m0.x, m0.x), ss = make_float2(m0.y, -m0.y);
-    a0 = __ffma2_rn(swp(t1), ss, __fmul2_rn(t0, cc));
-    a1 = __ffma2_rn(swp(t0), ss, __fmul2_rn(t1, cc));
+    a0 = qf_ffma2(swp(t1), ss, qf_fmul2(t0, cc));
+    a1 = qf_ffma2(swp(t0), ss, qf_fmul2(t1, cc));
 }
 __device__ __forceinline__ void jrx(double2& a0, double2& a1, double2 m0) {
     const double2 t0 = a0, t1 = a1;
@@ -80,9 +94,9 @@ __device__ __forceinline__ void jrx(double2& a0, double2& a1, double2 m0) {
 // rotation [[c, -s], [s, c]] (up to a global sign) as three shears, m0 = (t, s)
 __device__ __forceinline__ void jrs(float2& a0, float2& a1, float2 m0) {
     const float2 mt = make_float2(-m0.x, -m0.x), ms = make_float2(m0.y, m0.y);
-    a0 = __ffma2_rn(a1, mt, a0);
-    a1 = __ffma2_rn(a0, ms, a1);
-    a0 = __ffma2_rn(a1, mt, a0);
+    a0 = qf_ffma2(a1, mt, a0);
+    a1 = qf_ffma2(a0, ms, a1);
+    a0 = qf_ffma2(a1, mt, a0);
 }
 __device__ __forceinline__ void jrs(double2& a0, double2& a1, double2 m0) {
     a0.x = fma(-m0.x, a1.x, a0.x);
@@ -94,19 +108,19 @@ __device__ __forceinline__ void jrs(double2& a0, double2& a1, double2 m0) {
 }
 // packed tap products (c64): lanes (u.x v.x, u.y v.y) sum to Re(conj(u) v);
 // lanes (u.x v.y, u.y v.x) differ to Im(conj(u) v)
-__device__ __forceinline__ float2 jre2(float2 u, float2 v) { return __fmul2_rn(u, v); }
-__device__ __forceinline__ float2 jre2a(float2 u, float2 v, float2 acc) { return __ffma2_rn(u, v, acc); }
-__device__ __forceinline__ float2 jim2(float2 u, float2 v) { return __fmul2_rn(u, swp(v)); }
-__device__ __forceinline__ float2 jim2a(float2 u, float2 v, float2 acc) { return __ffma2_rn(u, swp(v), acc); }
-__device__ __forceinline__ float2 jadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 jsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 jre2(float2 u, float2 v) { return qf_fmul2(u, v); }
+__device__ __forceinline__ float2 jre2a(float2 u, float2 v, float2 acc) { return qf_ffma2(u, v, acc); }
+__device__ __forceinline__ float2 jim2(float2 u, float2 v) { return qf_fmul2(u, swp(v)); }
+__device__ __forceinline__ float2 jim2a(float2 u, float2 v, float2 acc) { return qf_ffma2(u, swp(v), acc); }
+__device__ __forceinline__ float2 jadd2(float2 a, float2 b) { return qf_fadd2(a, b); }
+__device__ __forceinline__ float2 jsub2(float2 a, float2 b) { return qf_fadd2(a, make_float2(-b.x, -b.y)); }
 // acc + k v and acc + i k v (k real) for the specialised H|psi> kernels
-__device__ __forceinline__ float2 jaxpy(float k, float2 v, float2 acc) { return __ffma2_rn(make_float2(k, k), v, acc); }
+__device__ __forceinline__ float2 jaxpy(float k, float2 v, float2 acc) { return qf_ffma2(make_float2(k, k), v, acc); }
 __device__ __forceinline__ double2 jaxpy(double k, double2 v, double2 acc) {
     return make_double2(fma(k, v.x, acc.x), fma(k, v.y, acc.y));
 }
 __device__ __forceinline__ float2 jiaxpy(float k, float2 v, float2 acc) {
-    return __ffma2_rn(make_float2(-k, k), swp(v), acc);
+    return qf_ffma2(make_float2(-k, k), swp(v), acc);
 }
 __device__ __forceinline__ double2 jiaxpy(double k, double2 v, double2 acc) {
     return make_double2(fma(-k, v.y, acc.x), fma(k, v.x, acc.y));

@@ -319,6 +319,29 @@ __global__ void adam_kernel(int count, double* theta, double* m, double* v, cons
     theta[i] -= lr * mhat / (sqrt(vhat) + eps);
 }
 
+// parameter-shift / finite-difference batch (variational.cpp:72-79): row
+// (b, j, sgn) = theta_b with theta_b[j] += (sgn ? -shift : +shift)
+__global__ void shift_thetas_kernel(int B, int P, const double* theta, double shift, double* out) {
+    const int64_t total = (int64_t)B * 2 * P * P;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % P);
+        const int64_t row = i / P;  // = (b * P + j) * 2 + sgn
+        const int sgn = (int)(row & 1);
+        const int j = (int)((row >> 1) % P);
+        const int64_t b = (row >> 1) / P;
+        double t = theta[b * P + k];
+        if (k == j) t = sgn ? theta[b * P + k] - shift : theta[b * P + k] + shift;
+        out[i] = t;
+    }
+}
+
+// g[b][j] = (E(b, j, +) - E(b, j, -)) / denom
+__global__ void shift_grad_kernel(int B, int P, const double* E, double denom, double* g) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * P) return;
+    g[i] = (E[2 * (int64_t)i] - E[2 * (int64_t)i + 1]) / denom;
+}
+
 __global__ void convert_kernel(const float2* src, double2* dst, int64_t count) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -440,6 +463,18 @@ cudaError_t launch_adam(int count, double* theta, double* m, double* v, const do
                         double b1, double b2, double eps, double c1, double c2, cudaStream_t s) {
     if (count == 0) return cudaSuccess;
     adam_kernel<<<(count + 255) / 256, 256, 0, s>>>(count, theta, m, v, g, lr, b1, b2, eps, c1, c2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift_thetas(int B, int P, const double* theta, double shift, double* out, cudaStream_t s) {
+    if (B == 0 || P == 0) return cudaSuccess;
+    shift_thetas_kernel<<<1184, 256, 0, s>>>(B, P, theta, shift, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift_grad(int B, int P, const double* E, double denom, double* g, cudaStream_t s) {
+    if (B == 0 || P == 0) return cudaSuccess;
+    shift_grad_kernel<<<(B * P + 255) / 256, 256, 0, s>>>(B, P, E, denom, g);
     return cudaGetLastError();
 }
 

@@ -30,6 +30,8 @@ cudaError_t launch_reduce(const ReduceArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_gather_grads(const double* tapsum, int n_taps, const int* slot_ptr,
                                 const int* slot_taps, const double* slot_coef, int P,
                                 int batch, double* grads /* [B][P] */, cudaStream_t s);
+cudaError_t launch_shift_thetas(int B, int P, const double* theta, double shift, double* out, cudaStream_t s);
+cudaError_t launch_shift_grad(int B, int P, const double* E, double denom, double* g, cudaStream_t s);
 cudaError_t launch_adam(int count, double* theta, double* m, double* v, const double* g,
                         double lr, double b1, double b2, double eps, double c1, double c2,
                         cudaStream_t s);

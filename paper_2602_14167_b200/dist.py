@@ -1,5 +1,6 @@
-"""Multi-GPU partitioning (one process per GPU), mirroring the C-ABI's sharded
-qf_energy_grad_batch (csrc/capi.cpp) so host code and tests share one rule.
+"""Multi-GPU partitioning (one process per GPU).  The partition rule is the
+C-ABI's own (qf_shard_range, the function csrc/capi.cpp's sharded
+qf_energy_grad_batch uses), so host code and tests share one implementation.
 
 Batch sharding: rank r owns parameter-set rows [B r / p, B (r+1) / p); every
 other row of the [B x (1+P)] result buffer stays zero, so one all-reduce(sum)
@@ -13,7 +14,14 @@ from __future__ import annotations
 
 
 def shard_range(count: int, rank: int, world: int) -> tuple[int, int]:
-    return count * rank // world, count * (rank + 1) // world
+    """[begin, end) owned by `rank` of `world` (qf_shard_range; host-only call)."""
+    import ctypes
+
+    from . import _lib
+
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load().qf_shard_range(int(count), int(rank), int(world), ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
 
 
 def init_engine_comm(ctx, group=None) -> None:

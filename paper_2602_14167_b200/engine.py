@@ -35,8 +35,26 @@ class Context:
     def set_memory_budget(self, nbytes: int) -> None:
         check(self.lib.qf_ctx_set_memory_budget(self.handle, int(nbytes)))
 
-    def set_timing(self, on: bool) -> None:
-        check(self.lib.qf_ctx_set_timing(self.handle, 1 if on else 0))
+    def set_timing(self, on) -> None:
+        """False/0 off, True/1 per kernel class, 2 also per launch (launch_times)."""
+        check(self.lib.qf_ctx_set_timing(self.handle, int(on)))
+
+    def flops(self):
+        """Canonical algorithmic flops per kernel class since reset_stats."""
+        f = np.zeros(4)
+        check(self.lib.qf_ctx_flops(self.handle, dptr(f)))
+        return f.tolist()
+
+    def launch_times(self) -> dict:
+        """{launch id: (ms, count)} since reset_stats (timing level 2): forward sweep i,
+        1000 = H|psi>, 2000 + i = adjoint sweep i."""
+        n = ctypes.c_int()
+        check(self.lib.qf_ctx_launch_times(self.handle, 0, None, None, None, ctypes.byref(n)))
+        ids = (ctypes.c_int * max(1, n.value))()
+        ms = np.zeros(max(1, n.value))
+        cnt = (ctypes.c_longlong * max(1, n.value))()
+        check(self.lib.qf_ctx_launch_times(self.handle, n.value, ids, dptr(ms), cnt, ctypes.byref(n)))
+        return {int(ids[i]): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
 
     def reset_stats(self) -> None:
         check(self.lib.qf_ctx_reset_stats(self.handle))
@@ -241,6 +259,19 @@ def energy_grad_batch(ctx: Context, prog: Program, obs: Observable, thetas: np.n
     G = np.empty((B, prog.n_params), dtype=np.float64) if grads else None
     check(ctx.lib.qf_energy_grad_batch(ctx.handle, prog.handle, obs.handle, B, dptr(th), dptr(E),
                                        dptr(G) if grads else None))
+    return E, G
+
+
+def energy_grad_batch_partial(ctx: Context, prog: Program, obs: Observable, thetas: np.ndarray, rank: int,
+                              world: int, grads: bool = True):
+    """The contribution rank `rank` of `world` makes before the all-reduce
+    (qf_energy_grad_batch_partial): the multi-GPU split replayed on one GPU."""
+    th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64).reshape(-1, prog.n_params))
+    B = th.shape[0]
+    E = np.empty(B, dtype=np.float64)
+    G = np.empty((B, prog.n_params), dtype=np.float64) if grads else None
+    check(ctx.lib.qf_energy_grad_batch_partial(ctx.handle, prog.handle, obs.handle, B, dptr(th), int(rank),
+                                               int(world), dptr(E), dptr(G) if grads else None))
     return E, G
 
 

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import enum
 import json
+import weakref
 import math
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -309,7 +310,7 @@ class PauliSum:  # pauli.hpp:21-30
     def __init__(self, n: int = 0):
         self.n = n
         self.terms: list[PauliTerm] = []
-        self._obs = {}
+        self._obs = weakref.WeakKeyDictionary()
 
     def add(self, weight, codes) -> None:  # pauli.cpp:12-18
         codes = [int(c) for c in codes]
@@ -319,7 +320,6 @@ class PauliSum:  # pauli.hpp:21-30
         w = complex(weight)
         _require(math.isfinite(w.real) and math.isfinite(w.imag), "PauliSum::add: non-finite weight")
         self.terms.append(PauliTerm(w, codes))
-        self._obs = {}
 
     def add_word(self, weight, site_codes) -> None:  # pauli.cpp:20-27
         codes = [0] * self.n
@@ -345,13 +345,22 @@ class PauliSum:  # pauli.hpp:21-30
         w = np.array([t.weight for t in self.terms], dtype=np.complex128)
         return codes, w
 
+    def _content_key(self):
+        return (self.n, tuple((complex(t.weight), tuple(int(c) for c in t.codes)) for t in self.terms))
+
     def observable(self, ctx=None) -> _eng.Observable:
+        """Device copy for `ctx`, keyed on the context object (weakly) and on the
+        sum's content: `terms` is public and may be edited in place."""
         ctx = ctx or _eng.default_context()
-        key = id(ctx)
-        if key not in self._obs:
+        if not isinstance(self._obs, weakref.WeakKeyDictionary):
+            self._obs = weakref.WeakKeyDictionary()
+        key = self._content_key()
+        hit = self._obs.get(ctx)
+        if hit is None or hit[0] != key:
             codes, w = self.arrays()
-            self._obs[key] = _eng.Observable(ctx, self.n, codes, w)
-        return self._obs[key]
+            hit = (key, _eng.Observable(ctx, self.n, codes, w))
+            self._obs[ctx] = hit
+        return hit[1]
 
 
 class Lattice:
@@ -482,7 +491,7 @@ class AnsatzSpec:  # variational.hpp:14-21
         self.n_params = n_params
         self.builder = builder
         self.shift_eligible = list(shift_eligible) if shift_eligible is not None else []
-        self._programs = {}
+        self._programs = weakref.WeakKeyDictionary()  # ctx -> {(precision, n_params, builder): Program}
 
     def validate(self) -> None:  # variational.cpp:11-16
         _require(self.n_params >= 0, "AnsatzSpec: negative parameter count")
@@ -494,10 +503,13 @@ class AnsatzSpec:  # variational.hpp:14-21
     def program(self, precision: Optional[str] = None, ctx=None) -> _eng.Program:
         precision = precision or _precision
         ctx = ctx or _eng.default_context()
-        key = (precision, id(ctx))
-        if key not in self._programs:
-            self._programs[key] = _compile_ansatz(self, precision, ctx)
-        return self._programs[key]
+        if not isinstance(self._programs, weakref.WeakKeyDictionary):
+            self._programs = weakref.WeakKeyDictionary()
+        per_ctx = self._programs.setdefault(ctx, {})
+        key = (precision, self.n_params, id(self.builder), self.builder)  # builder/n_params are public fields
+        if key not in per_ctx:
+            per_ctx[key] = _compile_ansatz(self, precision, ctx)
+        return per_ctx[key]
 
 
 def _probe(builder, P: int, values: np.ndarray) -> Circuit:

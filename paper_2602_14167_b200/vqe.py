@@ -2,17 +2,17 @@
 
 The reference loops per batch entry on CPU threads: energy -> gradient (2P
 energies) -> adam_step, `steps` times, then a final energy and best-of-batch.
-Here the whole batch advances in lock step on the GPU: theta and the Adam
-moments stay resident in HBM, each step is one batched energy + gradient call
-(adjoint: one forward + one adjoint pass; parameter_shift / finite_diff: one
-batched call over the 2P shifted parameter sets, same rule as the reference)
-followed by one Adam kernel.  Trace semantics are the reference's: trace[s] is
-the energy before update s, the final energy is appended, best is the first
-strict minimum.
+Here the whole batch advances in lock step inside one native call (qf_vqe_run,
+csrc/capi.cpp): theta, the Adam moments and the energy traces stay resident in
+HBM, each step is one batched energy + gradient evaluation (adjoint: one forward
++ one adjoint pass; parameter_shift / finite_diff: one batched call over the 2P
+shifted parameter sets, same rule as the reference) followed by one Adam kernel.
+Trace semantics are the reference's: trace[s] is the energy before update s, the
+final energy is appended, best is the first strict minimum.
 """
 from __future__ import annotations
 
-import math
+import ctypes
 
 import numpy as np
 
@@ -20,8 +20,6 @@ from . import engine as _eng
 
 
 def vqe_run_device(ansatz, theta0_batch, h, steps: int, lr: float, grad_mode, precision=None):
-    import torch
-
     from .qforge import GradMode, VqeResult, _require
 
     ansatz.validate()
@@ -40,38 +38,13 @@ def vqe_run_device(ansatz, theta0_batch, h, steps: int, lr: float, grad_mode, pr
     obs = h.observable(ctx)
     _require(h.n == prog.n, "expectation_pauli: size mismatch")
     B = len(theta0)
-    dev = torch.device("cuda", ctx.device)
-    ext = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    with torch.cuda.stream(ext):
-        theta = torch.tensor(np.stack(theta0), dtype=torch.float64, device=dev).contiguous()
-        m = torch.zeros_like(theta)
-        v = torch.zeros_like(theta)
-        g = torch.zeros_like(theta)
-        trace = torch.zeros((steps + 1, B), dtype=torch.float64, device=dev)
-        if mode != GradMode.adjoint:
-            shift = math.pi / 2.0 if mode == GradMode.parameter_shift else 1e-5
-            denom = 2.0 if mode == GradMode.parameter_shift else 2.0e-5
-            eye = torch.eye(P, dtype=torch.float64, device=dev) * shift
-            Es = torch.zeros(B * 2 * P, dtype=torch.float64, device=dev)
-        for s in range(steps):
-            if mode == GradMode.adjoint:
-                _eng.energy_grad_batch_device(ctx, prog, obs, theta, trace[s], g)
-            else:
-                _eng.energy_grad_batch_device(ctx, prog, obs, theta, trace[s], None)
-                if P:
-                    T = torch.stack([theta[:, None, :] + eye[None], theta[:, None, :] - eye[None]], dim=2)
-                    T = T.reshape(B * 2 * P, P).contiguous()
-                    _eng.energy_grad_batch_device(ctx, prog, obs, T, Es, None)
-                    E2 = Es.view(B, P, 2)
-                    g.copy_((E2[:, :, 0] - E2[:, :, 1]) / denom)
-            _eng.adam_step_device(ctx, theta, m, v, g, s + 1, lr)
-        _eng.energy_grad_batch_device(ctx, prog, obs, theta, trace[steps], None)
-        tr = trace.t().contiguous().cpu().numpy()
-        fin = theta.cpu().numpy()
-    torch.cuda.synchronize(dev)
-    best_e, best_i = math.inf, -1
-    for b in range(B):  # strict <, first index wins (variational.cpp:133-141)
-        if tr[b, steps] < best_e:
-            best_e, best_i = float(tr[b, steps]), b
-    return VqeResult([list(map(float, tr[b])) for b in range(B)], [fin[b].copy() for b in range(B)],
-                     best_e, best_i)
+    th = np.ascontiguousarray(np.stack(theta0)) if P else np.zeros((B, 0))
+    traces = np.empty((B, steps + 1), dtype=np.float64)
+    fin = np.empty((B, P), dtype=np.float64)
+    best_e = ctypes.c_double()
+    best_i = ctypes.c_int()
+    _eng.check(ctx.lib.qf_vqe_run(ctx.handle, prog.handle, obs.handle, B, _eng.dptr(th), int(steps), float(lr),
+                                  int(mode), 1e-5, _eng.dptr(traces), _eng.dptr(fin), ctypes.byref(best_e),
+                                  ctypes.byref(best_i)))
+    return VqeResult([list(map(float, traces[b])) for b in range(B)], [fin[b].copy() for b in range(B)],
+                     float(best_e.value), int(best_i.value))

@@ -1,8 +1,11 @@
 """N > 1 host logic on CPU (world size 2, gloo): batch sharding with a zero-padded
 all-reduce reproduces the single-process result bitwise; term sharding sums to the
 full-Hamiltonian result.  The per-rank compute here is the CPU oracle standing in
-for the GPU kernels; the partition rule is the product's (paper_2602_14167_b200.dist,
-identical to csrc/capi.cpp)."""
+for the GPU kernels (no device in this container); the partition rule is the
+engine's own: paper_2602_14167_b200.dist.shard_range calls the C-ABI's
+qf_shard_range, the function csrc/capi.cpp's sharded evaluation uses.  The same
+split through the CUDA engine is replayed on one GPU by
+tests/test_gpu_api.py::test_virtual_ranks_batch_and_term_sharding."""
 import os
 import socket
 

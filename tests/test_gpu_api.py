@@ -10,6 +10,7 @@ import pytest
 from oracle import pyoracle as po
 from paper_2602_14167_b200 import qforge as qf
 from paper_2602_14167_b200 import engine
+from paper_2602_14167_b200.rng import RngStream
 
 pytestmark = pytest.mark.gpu
 
@@ -348,3 +349,70 @@ def test_batch_rows_independent_of_call_history(ctx):
         E, G = engine.energy_grad_batch(ctx, prog, obs, th[:B])
         for i in range(B):
             assert E[i] == alone[i][0][0] and np.array_equal(G[i], alone[i][1][0]), (B, i)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_virtual_ranks_batch_and_term_sharding(ctx, prec):
+    """the multi-GPU split replayed on one GPU.  For world = 2/4/8
+    each rank's contribution (qf_energy_grad_batch_partial: the exact buffer the
+    NCCL path all-reduces) is computed and summed in rank order.  Batch sharding
+    must reproduce the 1-GPU result bitwise (zero-padded rows); term sharding
+    (C4's mode: every rank the whole batch on its term block) must agree to
+    1e-12 (c128) / 1e-6 (c64) relative: only the summation order differs."""
+    from paper_2602_14167_b200 import _lib
+    from paper_2602_14167_b200.dist import shard_range
+    n, ops, P = po.hea_template(12, 2)
+    h = po.random_sum(12, 200, po.Rng(2004), True)
+    th = np.array([[s.normal() for _ in range(P)] for s in RngStream(77).split(11)])
+    prog = engine.Program(ctx, n, ops, P, prec)
+    obs = engine.Observable(ctx, n, h.codes, h.wr + 0j)
+    E1, G1 = engine.energy_grad_batch(ctx, prog, obs, th)
+    for world in (2, 4, 8):
+        E = np.zeros_like(E1)
+        G = np.zeros_like(G1)
+        for r in range(world):
+            Er, Gr = engine.energy_grad_batch_partial(ctx, prog, obs, th, r, world)
+            b0, b1 = shard_range(len(th), r, world)
+            assert not Er[:b0].any() and not Er[b1:].any()  # exact zeros outside the rank's rows
+            E += Er
+            G += Gr
+        assert np.array_equal(E, E1) and np.array_equal(G, G1), world
+    obs.set_sharding(_lib.QF_SHARD_TERMS)
+    tol = 1e-12 if prec == "c128" else 1e-6
+    for world in (2, 4, 8):
+        E = np.zeros_like(E1)
+        G = np.zeros_like(G1)
+        for r in range(world):
+            Er, Gr = engine.energy_grad_batch_partial(ctx, prog, obs, th, r, world)
+            E += Er
+            G += Gr
+        scale = max(np.abs(E1).max(), np.abs(G1).max())
+        assert np.abs(E - E1).max() <= tol * scale, (world, np.abs(E - E1).max() / scale)
+        assert np.abs(G - G1).max() <= tol * np.abs(G1).max(), (world, np.abs(G - G1).max() / np.abs(G1).max())
+    obs.set_sharding(_lib.QF_SHARD_BATCH)
+
+
+def test_device_entry_shards_with_communicator(ctx):
+    """qf_energy_grad_batch_device honours the communicator (rank share + one
+    all-reduce on the context stream), for batch and term sharding: equal to the
+    host-buffer call with the same communicator."""
+    import torch
+    from paper_2602_14167_b200 import _lib
+    n, ops, P = po.hea_template(10, 2)
+    h = po.random_sum(10, 40, po.Rng(9), True)
+    th = np.array([[s.normal() for _ in range(P)] for s in RngStream(5).split(6)])
+    c2 = engine.Context(0)
+    prog = engine.Program(c2, n, ops, P, "c128")
+    obs = engine.Observable(c2, n, h.codes, h.wr + 0j)
+    c2.set_comm(0, 1, engine.Context.nccl_unique_id())
+    dev = torch.device("cuda", 0)
+    for mode in (_lib.QF_SHARD_BATCH, _lib.QF_SHARD_TERMS):
+        obs.set_sharding(mode)
+        Eh, Gh = engine.energy_grad_batch(c2, prog, obs, th)
+        th_d = torch.tensor(th, device=dev)
+        E_d = torch.zeros(len(th), dtype=torch.float64, device=dev)
+        G_d = torch.zeros((len(th), P), dtype=torch.float64, device=dev)
+        engine.energy_grad_batch_device(c2, prog, obs, th_d, E_d, G_d)
+        torch.cuda.synchronize()
+        assert np.array_equal(E_d.cpu().numpy(), Eh) and np.array_equal(G_d.cpu().numpy(), Gh)
+    c2.set_comm(0, 1, None)

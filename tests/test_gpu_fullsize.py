@@ -71,8 +71,9 @@ def _run(case, prec, grads):
     h = _hamiltonian(case)
     th = _thetas(case)
     E, G = qf.energy_gradient_batch(ansatz, th, h, grads=grads, precision=prec)
-    for p in list(ansatz._programs.values()):
-        p.close()
+    for per_ctx in list(ansatz._programs.values()):
+        for p in per_ctx.values():
+            p.close()
     return E, G
 
 
