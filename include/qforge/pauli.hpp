@@ -6,6 +6,8 @@
 #include <utility>
 #include <vector>
 
+#include <string>
+
 #include "qforge/common.hpp"
 #include "qforge/lattice.hpp"
 #include "qforge/sparse.hpp"
@@ -24,6 +26,10 @@ struct PauliSum {
 
     void add(cplx weight, const std::vector<int>& codes);
     void add_word(cplx weight, const std::vector<std::pair<int, int>>& site_codes);
+
+    // wire format {"n","terms":[{"codes","w_im","w_re"}]} (pauli.cpp:29-50)
+    std::string to_json() const;
+    static PauliSum from_json(const std::string& text);
 
     // device copy (qf_observable), rebuilt when the terms change (content-keyed)
     mutable std::shared_ptr<void> device_cache;

@@ -8,6 +8,8 @@
 // (src/variational.cpp:54-81); this evaluates one forward and one adjoint pass.
 #include "capi_internal.hpp"
 
+#include <unistd.h>
+
 namespace qfcapi {
 
 NcclApi g_nccl;
@@ -59,11 +61,11 @@ void resolve_events(qf_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& pr : ctx->pending) {
         float ms = 0;
-        cudaEventElapsedTime(&ms, ctx->ev_pool[pr.first], ctx->ev_pool[pr.first + 1]);
-        if (pr.second < 4) {
-            ctx->ms[pr.second] += ms;
+        cudaEventElapsedTime(&ms, ctx->ev_pool[pr.start], ctx->ev_pool[pr.end]);
+        if (pr.cls < 4) {
+            ctx->ms[pr.cls] += ms;
         } else {  // per-launch timing (timing level 2): id = class - 100
-            auto& e = ctx->launch_ms[pr.second - 100];
+            auto& e = ctx->launch_ms[pr.cls - 100];
             e.first += ms;
             e.second += 1;
         }
@@ -72,9 +74,9 @@ void resolve_events(qf_ctx* ctx) {
     ctx->ev_used = 0;
 }
 
-// records an event on s; start/end pairs are consecutive in the pool
+// records an event on s (the pool is recycled only between evaluations, when
+// every pending pair is complete: see resolve_events calls)
 size_t record_event(qf_ctx* ctx, cudaStream_t s) {
-    if (ctx->ev_used >= 4096 && ctx->ev_used % 2 == 0) resolve_events(ctx);
     if (ctx->ev_used == ctx->ev_pool.size()) {
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -100,8 +102,8 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     };
     auto tock = [&](int i, int cls) {
         if (ctx->timing) {
-            record_event(ctx, s);
-            ctx->pending.push_back({ev_start[i / 2], cls});
+            const size_t end = record_event(ctx, s);
+            ctx->pending.push_back({ev_start[i / 2], end, cls});
         }
     };
     // timing level 2: every sweep / H|psi> launch bracketed by its own events
@@ -112,8 +114,8 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     };
     auto ltock = [&](int id) {
         if (ctx->timing >= 2) {
-            record_event(ctx, s);
-            ctx->pending.push_back({l_ev, 100 + id});
+            const size_t end = record_event(ctx, s);
+            ctx->pending.push_back({l_ev, end, 100 + id});
         }
     };
 
@@ -219,6 +221,10 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
 
     // --- adjoint ---
     if (grads) {
+        if (const char* e = std::getenv("QF_DEV_BWD_PAUSE_US")) {  // development: idle GPU before the adjoint
+            cudaStreamSynchronize(s);
+            usleep((useconds_t)std::atol(e));
+        }
         tick(4);
         const int nt = P.bwd.n_taps;
         const int tiles_b = 1 << (n - P.bwd.k);
@@ -281,6 +287,7 @@ int eval_device(qf_ctx* ctx, qf_program* prog, qf_observable* obs, int batch, co
     const int prec = P.prec, n = P.n;
     const Geometry geo = geometry(prec, n);
     ObsDev* od = &obs->dev[prec];
+    if (ctx->timing && ctx->ev_used > 4096) resolve_events(ctx);  // recycle the event pool between calls
     int rc;
     if (term_shard && world > 1) {
         // rank r owns the contiguous term block [T r / p, T (r + 1) / p)

@@ -218,7 +218,11 @@ struct qf_ctx {
     double flops[4] = {0, 0, 0, 0};  // canonical algorithmic flops per class
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
-    std::vector<std::pair<size_t, int>> pending;  // (start event index, class); end = start + 1
+    struct PendingTime {
+        size_t start, end;  // event pool indices
+        int cls;            // class (< 4) or 100 + launch id
+    };
+    std::vector<PendingTime> pending;
     // CUDA graph of the last single-chunk evaluation, replayed while nothing it
     // captured (program, observable plan, buffers, batch) changes
     std::vector<const void*> graph_key;

@@ -209,27 +209,38 @@ class Circuit:  # circuit.hpp:51-83
         self.ops[-1].matrix = u
         return self
 
-    def to_json(self) -> str:  # circuit.cpp:524-547 wire format {n,d,ops:[{name,wires,params}]}
+    def to_json(self) -> str:  # circuit.cpp:524-547: {"d","n","ops":[{"name","params","wires"[,"im","re","rows"]}]}
         ops = []
         for op in self.ops:
-            o = {"name": gate_name(op.name), "wires": op.wires, "params": op.params}
+            o = {"name": gate_name(op.name), "wires": [int(w) for w in op.wires],
+                 "params": [float(p) for p in op.params]}
             if op.name == Gate.unitary:
-                o["matrix_re"] = np.real(op.matrix).tolist()
-                o["matrix_im"] = np.imag(op.matrix).tolist()
+                m = np.asarray(op.matrix, dtype=np.complex128)
+                o["rows"] = int(m.shape[0])
+                o["re"] = [float(v) for v in m.real.reshape(-1)]
+                o["im"] = [float(v) for v in m.imag.reshape(-1)]
             ops.append(o)
-        return json.dumps({"n": self.n, "d": self.d, "ops": ops})
+        return _dump({"n": int(self.n), "d": int(self.d), "ops": ops})
 
     @staticmethod
-    def from_json(text: str) -> "Circuit":
+    def from_json(text: str) -> "Circuit":  # circuit.cpp:549-571
         j = json.loads(text)
         c = Circuit(j["n"], j.get("d", 2))
         for o in j["ops"]:
-            g = Gate[o["name"]]
+            g = Gate[o["name"]] if o["name"] in Gate.__members__ else None
+            _require(g is not None, "unknown gate name: " + str(o["name"]))
             if g == Gate.unitary:
-                c.unitary(o["wires"], np.array(o["matrix_re"]) + 1j * np.array(o["matrix_im"]))
+                rows = int(o["rows"])
+                m = (np.array(o["re"], dtype=float) + 1j * np.array(o["im"], dtype=float))[: rows * rows]
+                c.unitary(o["wires"], m.reshape(rows, rows))
             else:
-                c.gate(g, o["wires"], o.get("params", []))
+                c.gate(g, o["wires"], o["params"])
         return c
+
+
+def _dump(obj) -> str:
+    """nlohmann::json::dump() layout: compact separators, keys sorted."""
+    return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
 
 def _isfinite(p) -> bool:
@@ -328,9 +339,9 @@ class PauliSum:  # pauli.hpp:21-30
             codes[site] = code
         self.add(weight, codes)
 
-    def to_json(self) -> str:  # pauli.cpp:29-39
-        return json.dumps({"n": self.n, "terms": [{"w_re": t.weight.real, "w_im": t.weight.imag,
-                                                    "codes": t.codes} for t in self.terms]})
+    def to_json(self) -> str:  # pauli.cpp:29-39: {"n","terms":[{"codes","w_im","w_re"}]}
+        return _dump({"n": int(self.n), "terms": [{"w_re": float(t.weight.real), "w_im": float(t.weight.imag),
+                                                    "codes": [int(c) for c in t.codes]} for t in self.terms]})
 
     @staticmethod
     def from_json(text: str) -> "PauliSum":  # pauli.cpp:41-50
