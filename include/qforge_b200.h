@@ -120,6 +120,9 @@ int qf_program_set_initial_state(qf_program* prog, const double* amps);
 int qf_program_destroy(qf_program* prog);
 /* Schedule introspection: number of fused tile sweeps of the forward and
  * adjoint passes, and tile bits used. */
+/* Development: copies the context's psi (which = 0) or lambda (1) work buffer
+ * (state-major [B_chunk][2^n]) into `dst` (device or host memory). */
+int qf_debug_copy_state(qf_ctx* ctx, int which, void* dst, size_t bytes);
 int qf_program_info(const qf_program* prog, int* fwd_sweeps, int* bwd_sweeps,
                     int* fwd_tile_bits, int* bwd_tile_bits);
 

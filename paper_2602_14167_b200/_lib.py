@@ -45,6 +45,7 @@ SIGNATURES = {
     "qf_program_set_initial_state": (_I, [_P, _D]),
     "qf_program_destroy": (_I, [_P]),
     "qf_program_info": (_I, [_P] + [ctypes.POINTER(_I)] * 4),
+    "qf_debug_copy_state": (_I, [_P, _I, _P, ctypes.c_size_t]),
     "qf_program_jit_status": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I), _D,
                                    ctypes.POINTER(ctypes.c_char_p)]),
     "qf_observable_create": (_I, [_P, _I, _I, ctypes.POINTER(ctypes.c_int8), _D, _D, ctypes.POINTER(_P)]),

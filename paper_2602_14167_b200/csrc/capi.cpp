@@ -234,7 +234,10 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
         sa.tap_part = (double*)ctx->tap_part.p;
         sa.n_taps_total = nt;
         sa.gmat_pass_base = P.fwd.total_mat;
-        for (size_t i = 0; i < P.bwd.sweeps.size(); ++i) {
+        // development: QF_DEBUG_BWD_STOP=i leaves psi/lambda as the first i adjoint sweeps left them
+        size_t bwd_stop = P.bwd.sweeps.size();
+        if (const char* e = std::getenv("QF_DEBUG_BWD_STOP")) bwd_stop = std::min(bwd_stop, (size_t)std::atol(e));
+        for (size_t i = 0; i < bwd_stop; ++i) {
             sa.sw = P.bwd.sweeps[i];
             ltick();
             if (prog->use_jit)
@@ -797,6 +800,16 @@ int qf_jit_hpsi_check(int n, int n_terms, const int8_t* codes, const double* w_r
     std::string cubin, err;
     if (!jit_compile_source(jit_hpsi_source(plan, precision), cubin, err)) return set_err(QF_ERUNTIME, err);
     if (compiled) *compiled = 1;
+    return QF_OK;
+}
+
+int qf_debug_copy_state(qf_ctx* ctx, int which, void* dst, size_t bytes) {
+    if (!ctx || !dst) return set_err(QF_EINVAL, "qf_debug_copy_state: bad arguments");
+    const DevBuf& b = which ? ctx->lam : ctx->psi;
+    if (bytes > b.cap) return set_err(QF_EINVAL, "qf_debug_copy_state: more bytes than the buffer holds");
+    QF_CUDA(cudaSetDevice(ctx->device));
+    QF_CUDA(cudaStreamSynchronize((cudaStream_t)ctx->stream));
+    QF_CUDA(cudaMemcpy(dst, b.p, bytes, cudaMemcpyDefault));
     return QF_OK;
 }
 

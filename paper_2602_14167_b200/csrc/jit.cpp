@@ -223,8 +223,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             o("    }");
         }
         for (int j = 0; j < NR; ++j) {
-            o("    cp_async_v(buf + swz<%d>(tid + %uu), ps + (gb | %uu));", W, (unsigned)(T * j), joff[j]);
-            if (bwd) o("    cp_async_v(buf + %u + swz<%d>(tid + %uu), pl + (gb | %uu));", 1u << k, W, (unsigned)(T * j), joff[j]);
+            o("    cp_async_v(buf + swz<%d>(tid + %uu), ps + ((size_t)gb + %uull));", W, (unsigned)(T * j), joff[j]);
+            if (bwd) o("    cp_async_v(buf + %u + swz<%d>(tid + %uu), pl + ((size_t)gb + %uull));", 1u << k, W, (unsigned)(T * j), joff[j]);
         }
         o("  };");
         o("  V* cur = bufA; V* nxt = bufB;");
@@ -290,16 +290,16 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         for (int l = 0; l < NR; ++l) {
             const uint32_t off = reg_goff(phase(0), l);
             if (!bwd)
-                o("  V x%d = a.from_zero ? mk_basis<V>((g_p0 | %uu) == 0u) : st[g_p0 | %uu];", l, off, off);
+                o("  V x%d = a.from_zero ? mk_basis<V>((g_p0 | %uu) == 0u) : st[(size_t)g_p0 + %uull];", l, off, off);
             else
-                o("  V x%d = st[g_p0 | %uu]; V y%d = lm[g_p0 | %uu];", l, off, l, off);
+                o("  V x%d = st[(size_t)g_p0 + %uull]; V y%d = lm[(size_t)g_p0 + %uull];", l, off, l, off);
         }
     } else {
         for (int j = 0; j < NR; ++j) {
             if (!bwd)
-                o("  V v%d = a.from_zero ? mk_basis<V>((g_ld | %uu) == 0u) : st[g_ld | %uu];", j, joff[j], joff[j]);
+                o("  V v%d = a.from_zero ? mk_basis<V>((g_ld | %uu) == 0u) : st[(size_t)g_ld + %uull];", j, joff[j], joff[j]);
             else
-                o("  V v%d = st[g_ld | %uu]; V w%d = lm[g_ld | %uu];", j, joff[j], j, joff[j]);
+                o("  V v%d = st[(size_t)g_ld + %uull]; V w%d = lm[(size_t)g_ld + %uull];", j, joff[j], j, joff[j]);
         }
     }
     if (!pipe) {
@@ -939,8 +939,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if (!gx.empty()) o("    const uint32_t g_x = 0u%s;", gx.c_str());
             for (int l = 0; l < NR; ++l) {
                 const uint32_t off = reg_goff(ph, l);
-                const std::string a = gx.empty() ? "g_pl | " + std::to_string(off) + "u"
-                                                 : "(g_pl | " + std::to_string(off) + "u) ^ g_x";
+                // 64-bit index arithmetic: a 32-bit `g | C` index with C * sizeof(V) >= 2^31
+                // is miscompiled (the constant is split out of the address and wraps),
+                // which corrupted n >= 29 states (tools/micro/sweep_harness.cu)
+                const std::string a = gx.empty() ? "(size_t)g_pl + " + std::to_string(off) + "ull"
+                                                 : "((size_t)g_pl + " + std::to_string(off) + "ull) ^ (size_t)g_x";
                 if (bwd)
                     o("    st[%s] = x%d; lm[%s] = y%d;", a.c_str(), phys[l], a.c_str(), phys[l]);
                 else
@@ -970,9 +973,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
         for (int j = 0; j < NR; ++j) {
             if (bwd)
-                o("  st[g_ld | %uu] = v%d_o; lm[g_ld | %uu] = w%d_o;", joff[j], j, joff[j], j);
+                o("  st[(size_t)g_ld + %uull] = v%d_o; lm[(size_t)g_ld + %uull] = w%d_o;", joff[j], j, joff[j], j);
             else
-                o("  st[g_ld | %uu] = v%d_o;", joff[j], j);
+                o("  st[(size_t)g_ld + %uull] = v%d_o;", joff[j], j);
         }
     }
     if (bwd && sw.n_taps % std::max(S, 1) != 0) {
@@ -1059,7 +1062,7 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
     o("  const uint32_t tid = threadIdx.x, tile = blockIdx.x; const int b = blockIdx.y;");
     o("  const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)b * %zuull;", N);
     o("  const uint32_t base = tile << %d; (void)base;", kh);
-    for (int i = 0; i < NA; ++i) o("  const V po%d = ps[base + tid + %uu];", i, (unsigned)(T * i));
+    for (int i = 0; i < NA; ++i) o("  const V po%d = ps[(size_t)base + (tid + %uu)];", i, (unsigned)(T * i));
     bool own_smem = false;
     std::set<uint32_t> dmasks;
     for (const DevGroup& g : O.groups)
@@ -1082,7 +1085,7 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
         o("  {  // flip group 0x%x", g.f_out);
         if (outer) {
             for (int i = 0; i < NA; ++i)
-                o("    const V q%d = ps[(base ^ %uu) + tid + %uu];", i, g.f_out, (unsigned)(T * i));
+                o("    const V q%d = ps[(size_t)(base ^ %uu) + (tid + %uu)];", i, g.f_out, (unsigned)(T * i));
             if (need_smem) {
                 if (part_live) o("    __syncthreads();");
                 for (int i = 0; i < NA; ++i) o("    part[tid + %uu] = q%d;", (unsigned)(T * i), i);
@@ -1140,7 +1143,7 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
         o("  e += (double)po%d.x * (double)acc%d.x + (double)po%d.y * (double)acc%d.y;", i, i, i, i);
     o("  if (a.write_lam) {");
     o("    V* lm = reinterpret_cast<V*>(a.lam) + (size_t)b * %zuull;", N);
-    for (int i = 0; i < NA; ++i) o("    lm[base + tid + %uu] = acc%d;", (unsigned)(T * i), i);
+    for (int i = 0; i < NA; ++i) o("    lm[(size_t)base + (tid + %uu)] = acc%d;", (unsigned)(T * i), i);
     o("  }");
     o("  const unsigned m = lane_mask(%d);", T);
     o("  for (int off = %d; off > 0; off >>= 1) e += __shfl_xor_sync(m, e, off);", T >= 32 ? 16 : T / 2);

@@ -130,3 +130,34 @@ def test_c4_full_config(prec):
         grads = case["adjoint_grads"] is not None
         E, G = _run(case, prec, grads)
         _check(case, prec, E, G)
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+def test_n30_adjoint_matches_parameter_shift_of_engine_energies(prec):
+    """Regression (round 2): at n >= 29 the generated sweeps indexed HBM as
+    `st[g | C]` (32-bit) with C * sizeof(amplitude) >= 2^31; the compiler split
+    the constant out of the address and wrapped it, corrupting the last adjoint
+    sweep (tools/micro/sweep_harness.cu).  TFIM chain, HEA depth 1, n = 30: the
+    adjoint gradient against the parameter-shift rule (variational.cpp:72-79) on
+    the engine's own energies, on the components whose taps sit in the sweeps
+    that touch the top memory bits (qubits 0-2 ry / rz) and a few others."""
+    n = 30
+    a = qf.hea_ansatz(n, 1)
+    h = qf.tfim_terms(qf.build_lattice("chain", [n], [False]), 1.0)
+    P = a.n_params
+    s = RngStream(1004).split(1)[0]
+    th = np.array([[s.normal() for _ in range(P)]])
+    E, G = qf.energy_gradient_batch(a, th, h, grads=True, precision=prec)
+    comps = [0, 1, 2, 12, 29, 30, 31, 32, 45, 59]
+    rows = np.repeat(th, 2 * len(comps), axis=0)
+    for i, j in enumerate(comps):
+        rows[2 * i, j] += np.pi / 2
+        rows[2 * i + 1, j] -= np.pi / 2
+    Es, _ = qf.energy_gradient_batch(a, rows, h, grads=False, precision=prec)
+    S = (Es[0::2] - Es[1::2]) / 2
+    scale = np.abs(G[0]).max()
+    d = np.abs(G[0, comps] - S).max() / scale
+    assert d <= TOL[prec], (prec, d)
+    for per_ctx in list(a._programs.values()):
+        for p in per_ctx.values():
+            p.close()
