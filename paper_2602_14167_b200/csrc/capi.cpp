@@ -197,7 +197,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     // compulsory bytes: psi read once, lambda written once (partner tiles of
     // flips above the tile are re-reads, served from L2 when the state fits)
     ctx->bytes[1] += (double)bc * N * vs * (grads ? 2 : 1);
-    ctx->flops[1] += (double)bc * N * 8.0 * ((double)od->plan.terms.size() + 1.0);
+    ctx->flops[1] += (double)bc * N * 4.0 * ((double)od->plan.terms.size() + 1.0);  // one real-weighted complex FMA per term
     ReduceArgs ra{};
     ra.part = (const double*)ctx->epart.p;
     ra.count = 1;
@@ -633,10 +633,12 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
     if ((ce = upload(p->slot_taps, taps, s)) != cudaSuccess) return fail(ce);
     if ((ce = upload(p->slot_coef, coef, s)) != cudaSuccess) return fail(ce);
     if ((ce = cudaStreamSynchronize(s)) != cudaSuccess) return fail(ce);
-    // canonical algorithmic flops per amplitude of every sweep:
-    // 14 per dense one-qubit gate, 6 per diagonal gate, 30 per dense 4x4, 0 for
-    // permutations; the adjoint applies each gate to two states and adds 8 per
-    // gradient-tap inner product
+    // minimal algorithmic flops per amplitude of every sweep, FMA
+    // = 2: 6 per real rotation (ry, rx, h: two real products and a sum per
+    // component), 14 per dense complex one-qubit gate, 6 per diagonal phase (one
+    // complex product), 30 per dense 4x4 (per amplitude share), 0 for
+    // permutations (x, cx); the adjoint applies each gate to two states and adds
+    // 4 per gradient-tap product (one component of conj(lambda) G psi + the sum)
     for (int pi = 0; pi < 2; ++pi) {
         const PassPlan& pp = pi ? p->plan.bwd : p->plan.fwd;
         std::vector<double>& out = pi ? p->bwd_fpa : p->fwd_fpa;
@@ -644,10 +646,11 @@ int qf_program_create(qf_ctx* ctx, int n_qubits, int n_ops, const qf_op* ops, co
             double f = 0;
             for (int o = sw.op_begin; o < sw.op_end; ++o) {
                 switch (pp.ops[o].kind) {
-                    case DK_G1: case DK_R1: case DK_RX: case DK_RS: f += 14.0 * (pi ? 2 : 1); break;
+                    case DK_G1: f += 14.0 * (pi ? 2 : 1); break;
+                    case DK_R1: case DK_RX: case DK_RS: f += 6.0 * (pi ? 2 : 1); break;
                     case DK_D1: case DK_D2: f += 6.0 * (pi ? 2 : 1); break;
                     case DK_G2: f += 30.0 * (pi ? 2 : 1); break;
-                    case DK_TX: case DK_TY: case DK_TZ: case DK_TZZ: f += 8.0; break;
+                    case DK_TX: case DK_TY: case DK_TZ: case DK_TZZ: f += 4.0; break;
                     default: break;
                 }
             }

@@ -120,11 +120,18 @@ bool jit_pipe_mode(const PassPlan& pass, int si) {
     return std::strcmp(e, "light") == 0 && pass.sweeps[si].n_phases <= 2;
 }
 
+// complex64 adjoint sweeps exchange psi and lambda as interleaved float4 pairs
+// (QF_JIT_NOILV=1: two separate float2 tiles, the A/B baseline)
+bool jit_interleaved(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
+    return bwd && P.prec == QF_C64 && !jit_pipe_mode(pass, si) && !env_flag("QF_JIT_NOILV");
+}
+
 // Gradient taps are staged per thread in shared memory ([slots][T] reals) and
 // reduced in batches at fixed points (no per-tap shuffle chains).
 int jit_tap_stage(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
     if (!bwd) return 0;
-    const int cap = P.prec == QF_C128 ? 16 : 32;
+    int cap = P.prec == QF_C128 ? 16 : 32;
+    if (const char* e = std::getenv("QF_JIT_TAPSTAGE")) cap = std::max(1, atoi(e));  // development (occupancy A/B)
     return std::min(pass.sweeps[si].n_taps, cap);
 }
 
@@ -144,7 +151,11 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     const DevSweep& sw = pass.sweeps[si];
     const int k = sw.k, R = sw.R, NR = 1 << R, T = 1 << (k - R);
     const bool dbl = P.prec == QF_C128;
-    const int W = dbl ? 3 : 4;
+    // complex64 adjoint sweeps keep psi_p and lambda_p side by side in shared
+    // memory (one 16-byte float4 per amplitude): every phase exchange is one
+    // 128-bit STS + one 128-bit LDS per amplitude instead of two 64-bit each
+    const bool ilv = jit_interleaved(P, pass, si, bwd);
+    const int W = (dbl || ilv) ? 3 : 4;
     const char* Vt = dbl ? "double2" : "float2";
     const char* RTt = dbl ? "double" : "float";
     const int minb = [bwd] {
@@ -186,6 +197,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         o("  V* tile = reinterpret_cast<V*>(smem_raw);");
         o("  V* tile2 = tile + %u;", bwd ? (1u << k) : 0u);
         o("  V* smat = tile2 + %u;", 1u << k);
+        if (ilv) o("  float4* tq = reinterpret_cast<float4*>(smem_raw); (void)tq;");
         o("  RT* stg = reinterpret_cast<RT*>(smat + %d);", (sw.n_mat + 1) & ~1);
         o("  (void)tile; (void)tile2; (void)stg;");
         o("  const uint32_t tid = threadIdx.x, tile_id = blockIdx.x; const int b = blockIdx.y;");
@@ -316,7 +328,9 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     if (!pipe) o("  }");
     if (!direct_first && !pipe) {
         for (int j = 0; j < NR; ++j) {
-            if (bwd)
+            if (ilv)
+                o("  tq[swz<%d>(tid + %uu)] = make_float4(v%d.x, v%d.y, w%d.x, w%d.y);", W, (unsigned)(T * j), j, j, j, j);
+            else if (bwd)
                 o("  tile[swz<%d>(tid + %uu)] = v%d; tile2[swz<%d>(tid + %uu)] = w%d;", W, (unsigned)(T * j), j, W,
                   (unsigned)(T * j), j);
             else
@@ -386,7 +400,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
         if (!dfirst) {
             for (int l = 0; l < NR; ++l) {
-                if (bwd)
+                if (ilv)
+                    o("    V x%d, y%d; { const float4 q_ = tq[s_t ^ %uu]; x%d = make_float2(q_.x, q_.y); "
+                      "y%d = make_float2(q_.z, q_.w); }", l, l, offs[l], l, l);
+                else if (bwd)
                     o("    V x%d = tile[s_t ^ %uu]; V y%d = tile2[s_t ^ %uu];", l, offs[l], l, offs[l]);
                 else
                     o("    V x%d = tile[s_t ^ %uu];", l, offs[l]);
@@ -885,25 +902,34 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 }
                 case DK_TX: case DK_TY: {
                     if (!dbl) {  // c64: packed lane-pair accumulators (2 FFMA2 per amplitude pair)
+                        // two independent accumulator chains per sum (halves the FFMA2
+                        // dependency depth), merged with one FADD2; the final lane
+                        // combination is one FADD2 + one FADD
                         const auto prs = pairs(op.rb0);
-                        o("    { V P, M;");
+                        const int na = (prs.size() >= 4 && !env_flag("QF_JIT_TAPACC1")) ? 2 : 1;
+                        o("    { V P0, M0, P1, M1; (void)P1; (void)M1;");
                         for (size_t q = 0; q < prs.size(); ++q) {
-                            const int f = prs[q].first, g = prs[q].second;
+                            const int f = prs[q].first, g = prs[q].second, ai = (int)(q % na);
+                            const bool first = q < (size_t)na;
                             if (op.kind == DK_TX) {  // Im(conj(y_f) x_g) + Im(conj(y_g) x_f)
-                                if (q == 0) o("      P = jim2(y%d, x%d); M = jim2(y%d, x%d);", f, g, g, f);
-                                else o("      P = jim2a(y%d, x%d, P); M = jim2a(y%d, x%d, M);", f, g, g, f);
+                                if (first) o("      P%d = jim2(y%d, x%d); M%d = jim2(y%d, x%d);", ai, f, g, ai, g, f);
+                                else o("      P%d = jim2a(y%d, x%d, P%d); M%d = jim2a(y%d, x%d, M%d);", ai, f, g, ai, ai, g, f, ai);
                             } else {  // Re(conj(y_g) x_f) - Re(conj(y_f) x_g)
-                                if (q == 0) o("      P = jre2(y%d, x%d); M = jre2(y%d, x%d);", g, f, f, g);
-                                else o("      P = jre2a(y%d, x%d, P); M = jre2a(y%d, x%d, M);", g, f, f, g);
+                                if (first) o("      P%d = jre2(y%d, x%d); M%d = jre2(y%d, x%d);", ai, g, f, ai, f, g);
+                                else o("      P%d = jre2a(y%d, x%d, P%d); M%d = jre2a(y%d, x%d, M%d);", ai, g, f, ai, ai, f, g, ai);
                             }
                         }
-                        if (op.kind == DK_TX)
-                            o("      stg[%d * %d + tid] = (P.x - P.y) + (M.x - M.y); }", op.tap % S, T);
-                        else if (cond[op.rb0].any())  // X Y X = -Y
-                            o("      const RT t_ = (P.x + P.y) - (M.x + M.y); stg[%d * %d + tid] = %s ? -t_ : t_; }", op.tap % S,
-                              T, cond_expr(cond[op.rb0]).c_str());
-                        else
-                            o("      stg[%d * %d + tid] = (P.x + P.y) - (M.x + M.y); }", op.tap % S, T);
+                        if (na == 2) o("      P0 = jadd2(P0, P1); M0 = jadd2(M0, M1);");
+                        if (op.kind == DK_TX) {
+                            o("      const V S_ = jadd2(P0, M0);");
+                            o("      stg[%d * %d + tid] = S_.x - S_.y; }", op.tap % S, T);
+                        } else {
+                            o("      const V D_ = jsub2(P0, M0); const RT t_ = D_.x + D_.y;");
+                            if (cond[op.rb0].any())  // X Y X = -Y
+                                o("      stg[%d * %d + tid] = %s ? -t_ : t_; }", op.tap % S, T, cond_expr(cond[op.rb0]).c_str());
+                            else
+                                o("      stg[%d * %d + tid] = t_; }", op.tap % S, T);
+                        }
                         emit_flush_if_full(op.tap);
                         break;
                     }
@@ -954,7 +980,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if (!sx.empty()) o("    const uint32_t s_w = s_t%s;", sx.c_str());
             const char* sb = sx.empty() ? "s_t" : "s_w";
             for (int l = 0; l < NR; ++l) {
-                if (bwd)
+                if (ilv)
+                    o("    tq[%s ^ %uu] = make_float4(x%d.x, x%d.y, y%d.x, y%d.y);", sb, offs[l], phys[l], phys[l],
+                      phys[l], phys[l]);
+                else if (bwd)
                     o("    tile[%s ^ %uu] = x%d; tile2[%s ^ %uu] = y%d;", sb, offs[l], phys[l], sb, offs[l], phys[l]);
                 else
                     o("    tile[%s ^ %uu] = x%d;", sb, offs[l], phys[l]);
@@ -965,7 +994,10 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     }
     if (!direct_last) {
         for (int j = 0; j < NR; ++j) {
-            if (bwd)
+            if (ilv)
+                o("  V v%d_o, w%d_o; { const float4 q_ = tq[swz<%d>(tid + %uu)]; v%d_o = make_float2(q_.x, q_.y); "
+                  "w%d_o = make_float2(q_.z, q_.w); }", j, j, W, (unsigned)(T * j), j, j);
+            else if (bwd)
                 o("  const V v%d_o = tile[swz<%d>(tid + %uu)]; const V w%d_o = tile2[swz<%d>(tid + %uu)];", j, W,
                   (unsigned)(T * j), j, W, (unsigned)(T * j));
             else

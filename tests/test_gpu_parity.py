@@ -228,9 +228,9 @@ def test_all_gate_kinds_state_and_expectation(ctx):
     for prec in ("c128", "c64"):
         prog = engine.Program(ctx, 15, ops, 0, prec, mats=np.array(mats))
         psi = engine.run_state(ctx, prog, np.zeros(0), 40)
-        assert np.abs(psi - ref).max() <= TOL[prec] * 10
+        assert np.abs(psi - ref).max() <= TOL[prec], (prec, np.abs(psi - ref).max())
         e = engine.expectation(ctx, prog, engine.Observable(ctx, 15, h.codes, h.wr + 1j * h.wi), np.zeros(0))
-        assert abs(e - eref) <= TOL[prec] * max(1.0, abs(eref)) * 10
+        assert abs(e - eref) <= TOL[prec] * max(1.0, abs(eref)), (prec, abs(e - eref))
 
 
 def test_pauli_sum_to_coo_matches_oracle(ctx):
@@ -278,8 +278,9 @@ def test_randomized_stress_regressions(ctx):
     arithmetic itself, the generic kernels agree)."""
     import os
     here = os.path.join(os.path.dirname(__file__), "cases")
-    for name, prec, tol in [("stress_case6.npz", "c128", 1e-10), ("stress_case6.npz", "c64", 1e-5),
-                            ("stress_case138.npz", "c128", 1e-10), ("stress_case138.npz", "c64", 5e-5)]:
+    for name, prec in [("stress_case6.npz", "c128"), ("stress_case6.npz", "c64"),
+                       ("stress_case138.npz", "c128"), ("stress_case138.npz", "c64")]:
+        tol = TOL[prec]
         d = np.load(os.path.join(here, name), allow_pickle=True)
         n, P = int(d["n"]), int(d["P"])
         ops = [tuple(o) for o in d["ops"]]
@@ -288,6 +289,9 @@ def test_randomized_stress_regressions(ctx):
         E_ref, G_ref = po.energy_grad_batch(po.Ansatz(n, ops, P, mats), d["th"], h, mode="adjoint")
         obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
         E, G = engine.energy_grad_batch(ctx, engine.Program(ctx, n, ops, P, prec, mats), obs, d["th"])
-        # absolute floor: these random Hamiltonians can vanish on the state (E, G ~ 1e-17)
-        scale = max(np.abs(E_ref).max(), np.abs(G_ref).max(), 1e-3 * np.abs(h.wr + 1j * h.wi).sum())
-        assert max(np.abs(E - E_ref).max(), np.abs(G - G_ref).max()) <= tol * scale, (name, prec)
+        # normwise relative error against ||H||_1 = sum |w_k| (>= ||H|| >= |E|, and
+        # |dE/dtheta_j| <= 2 |coef_j| ||H||): these random Hamiltonians can vanish on
+        # the state (E, G ~ 1e-17), where an error relative to |E| is undefined
+        scale = np.abs(h.wr + 1j * h.wi).sum() * max(1.0, max(abs(o[4]) for o in ops))
+        err = max(np.abs(E - E_ref).max(), np.abs(G - G_ref).max()) / scale
+        assert err <= tol, (name, prec, err)
