@@ -120,10 +120,12 @@ bool jit_pipe_mode(const PassPlan& pass, int si) {
     return std::strcmp(e, "light") == 0 && pass.sweeps[si].n_phases <= 2;
 }
 
-// complex64 adjoint sweeps exchange psi and lambda as interleaved float4 pairs
-// (QF_JIT_NOILV=1: two separate float2 tiles, the A/B baseline)
+// QF_JIT_ILV=1: complex64 adjoint sweeps exchange psi and lambda as interleaved
+// float4 pairs (one 128-bit STS/LDS per amplitude).  Measured slower on C2 (first
+// adjoint sweep 64.4 -> 68.0 ms at batch 1024): the phases are FMA-pipe bound and
+// the packing moves cost issue slots, so two float2 tiles stay the default.
 bool jit_interleaved(const ProgramPlan& P, const PassPlan& pass, int si, bool bwd) {
-    return bwd && P.prec == QF_C64 && !jit_pipe_mode(pass, si) && !env_flag("QF_JIT_NOILV");
+    return bwd && P.prec == QF_C64 && !jit_pipe_mode(pass, si) && env_flag("QF_JIT_ILV");
 }
 
 // Gradient taps are staged per thread in shared memory ([slots][T] reals) and
@@ -1025,7 +1027,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         size_t nf = 1;
         for (auto& f : stab_entries) nf = std::max(nf, f.size());
         const size_t ne = stab_entries.size();
-        std::string decl = "__device__ const unsigned short qf_stab_f[" + std::to_string(ne) + "][" +
+        std::string decl = "__constant__ unsigned short qf_stab_f[" + std::to_string(ne) + "][" +
                            std::to_string(nf) + "] = {";
         for (size_t e = 0; e < ne; ++e) {
             decl += e ? ",{" : "{";
@@ -1037,14 +1039,19 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
         decl += "};\n";
         char buf[1024];
+        // The factors come from the sweep's matrix block once it sits in shared
+        // memory (one barrier), not from global memory: a chain of dependent L2
+        // loads per entry stalled every CTA's prologue for microseconds.
         snprintf(buf, sizeof buf,
+                 "    __syncthreads();  // smat complete\n"
                  "    for (int e = (int)tid; e < %zu; e += %d) {  // diagonal-run tables (uniform per state)\n"
                  "      V acc; acc.x = 1; acc.y = 0;\n"
+                 "#pragma unroll\n"
                  "      for (int q = 0; q < %zu; ++q) {\n"
                  "        const unsigned i = qf_stab_f[e][q];\n"
                  "        if (i == 0xffffu) break;\n"
-                 "        if (i & 0x8000u) { V d0 = gm[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(gm[(i & 0x7fffu) + 1], d0)); }\n"
-                 "        else acc = cmul(acc, gm[i]);\n"
+                 "        if (i & 0x8000u) { V d0 = smat[i & 0x7fffu]; d0.y = -d0.y; acc = cmul(acc, cmul(smat[(i & 0x7fffu) + 1], d0)); }\n"
+                 "        else acc = cmul(acc, smat[i]);\n"
                  "      }\n"
                  "      stab[e] = acc;\n"
                  "    }\n",

@@ -463,10 +463,10 @@ std::string build_program_plan(int n, const std::vector<GateSpec>& ops, const do
         int g = G - 1 - i;
         for (int s : succs[g]) rpreds[i].push_back(G - 1 - s);
     }
-    // complex64 adjoint tiles hold psi and lambda interleaved (16-byte elements, like
-    // complex128): bank groups of 8, so the lane bits are spread mod 3
-    const char* noilv = std::getenv("QF_JIT_NOILV");
-    const int Wb = (prec == QF_C64 && !(noilv && noilv[0] == '1')) ? 3 : geo.W;
+    // interleaved complex64 adjoint tiles (QF_JIT_ILV) have 16-byte elements, like
+    // complex128: bank groups of 8, so the lane bits are spread mod 3
+    const char* ilv = std::getenv("QF_JIT_ILV");  // see jit_interleaved (jit.cpp)
+    const int Wb = (prec == QF_C64 && ilv && ilv[0] == '1') ? 3 : geo.W;
     lower_pass(P, rorder, rpreds, geo.kb, geo.Rb, geo.c, Wb, true, P.bwd);
     if (G > 0 && (P.fwd.sweeps.empty() || P.bwd.sweeps.empty()))
         return "program: scheduling failed";
