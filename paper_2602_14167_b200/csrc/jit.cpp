@@ -279,6 +279,21 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if (ph.thr_tl[j] < need) ++have;
         return have == need;
     };
+    // A phase change that keeps every warp-index thread bit (thread bits 5 and up)
+    // on the same tile bit moves data only inside each warp's own region of the
+    // tile: the region a warp stores before the change is exactly the one it loads
+    // after it, so a __syncwarp orders it.  Warps may then run phases apart; two
+    // warps in different phases of such a run still own disjoint regions (same
+    // warp bits, different values), and every other change, the tap flushes and
+    // the tile's final read-out stay CTA barriers.  (plan.cpp warp_bit_runs keeps
+    // the warp bits fixed over runs of phases.)  QF_JIT_WARPSYNC=0: always barriers.
+    static const bool warpsync_off = std::getenv("QF_JIT_WARPSYNC") && std::getenv("QF_JIT_WARPSYNC")[0] == '0';
+    auto warp_local_exchange = [&](const DevPhase& a, const DevPhase* b) {
+        if (warpsync_off || pipe || !b || T < 64) return false;
+        for (int j = 5; j < k - R; ++j)
+            if (a.thr_tl[j] != b->thr_tl[j]) return false;
+        return true;
+    };
     const bool direct_first = !pipe && allow_direct && nph > 0 && lanes_cover_low(phase(0));
     const bool direct_last = allow_direct && nph > 0 && lanes_cover_low(phase(nph - 1));
     // memory offset of register index l in phase f, and of the phase's thread base
@@ -990,7 +1005,8 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
                 else
                     o("    tile[%s ^ %uu] = x%d;", sb, offs[l], phys[l]);
             }
-            o("    __syncthreads();");
+            o("    %s", warp_local_exchange(ph, f + 1 < nph ? &phase(f + 1) : nullptr) ? "__syncwarp();"
+                                                                                     : "__syncthreads();");
             o("  }");
         }
     }

@@ -216,6 +216,63 @@ static int mat_size(uint8_t kind) {
     }
 }
 
+// Warp-index bits of every phase of a sweep (tile-local bit mask; 0 = no choice).
+// Greedy runs: a run of phases keeps one set of nwb warp bits, taken from the
+// tile bits none of the run's phases needs in registers (and never the `low`
+// lowest tile bits, which must stay lanes for the direct HBM phases).  Within a
+// run's candidates the set whose leftover lane bits cover the most distinct
+// residues mod W (shared-memory bank spread) wins, then the highest bits.
+// QF_WARP_RUNS=0 turns it off (development A/B).
+static std::vector<uint64_t> warp_bit_runs(const std::vector<Group>& phases, int k, int R, int W, int low) {
+    std::vector<uint64_t> out(phases.size(), 0);
+    const int nwb = (k - R) - 5;
+    static const bool off = std::getenv("QF_WARP_RUNS") && std::getenv("QF_WARP_RUNS")[0] == '0';
+    if (off || nwb <= 0 || phases.size() < 2) return out;
+    const uint64_t tile = (1ull << k) - 1, lowm = (1ull << low) - 1;
+    size_t f = 0;
+    while (f < phases.size()) {
+        uint64_t allowed = tile & ~phases[f].bits & ~lowm;
+        size_t g = f;
+        while (g + 1 < phases.size() && popc(allowed & ~phases[g + 1].bits) >= nwb) allowed &= ~phases[++g].bits;
+        if (popc(allowed) < nwb) {  // cannot happen for k - R - low >= nwb; keep the default assignment
+            f = g + 1;
+            continue;
+        }
+        std::vector<int> cand;
+        for (int b = 0; b < k; ++b)
+            if (allowed >> b & 1) cand.push_back(b);
+        uint64_t best = 0;
+        long best_score = -1;
+        const size_t m = cand.size();
+        for (uint64_t sel = 0; sel < (1ull << m); ++sel) {  // m <= k - R - low (small)
+            if (popc(sel) != nwb) continue;
+            uint64_t w = 0;
+            for (size_t i = 0; i < m; ++i)
+                if (sel >> i & 1) w |= 1ull << cand[i];
+            long score = 0;
+            for (size_t h = f; h <= g; ++h) {
+                // this phase's lanes: the free bits left after registers (padded high) and warps
+                uint64_t r = phases[h].bits;
+                for (int b = k - 1; b >= 0 && popc(r) < R; --b)
+                    if (!(w >> b & 1)) r |= 1ull << b;
+                const uint64_t lanes = tile & ~r & ~w;
+                uint32_t res = 0;
+                for (int b = 0; b < k; ++b)
+                    if (lanes >> b & 1) res |= 1u << (b % W);
+                score += popc(res);
+            }
+            score = score * 4096 + (long)(w >> 1);  // tie-break: higher bits
+            if (score > best_score) {
+                best_score = score;
+                best = w;
+            }
+        }
+        for (size_t h = f; h <= g; ++h) out[h] = best;
+        f = g + 1;
+    }
+    return out;
+}
+
 // Lower one pass (forward or adjoint) of an ordered gate list.
 static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
                        const std::vector<std::vector<int>>& preds_in_order, int k, int R,
@@ -309,14 +366,22 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             }
             ph.items.swap(order);
         }
+        // Warp-index thread bits (above the 5 lane bits) are held on the same tile
+        // bits over runs of phases: a phase change that keeps them permutes data
+        // only inside each warp's own region of the shared tile, so the generated
+        // kernel syncs that warp (__syncwarp) instead of the whole CTA there.
+        const std::vector<uint64_t> wbits = warp_bit_runs(phases, k, R, W, P.prec == QF_C128 ? 1 : 2);
         int moff = 0, ntap = 0;
-        for (auto& ph : phases) {
+        for (size_t fi = 0; fi < phases.size(); ++fi) {
+            auto& ph = phases[fi];
+            const uint64_t wb = wbits[fi];
             DevPhase dp{};
             for (int i = 0; i < kMaxReg; ++i) dp.reg_tl[i] = -1;
             for (int i = 0; i < kMaxThreadBits; ++i) dp.thr_tl[i] = -1;
             // register bits: the needed ones, padded with the highest free tile bits
             uint64_t rbits = ph.bits;
-            for (int b = k - 1; b >= 0 && popc(rbits) < R; --b) rbits |= 1ull << b;
+            for (int b = k - 1; b >= 0 && popc(rbits) < R; --b)
+                if (!(wb >> b & 1)) rbits |= 1ull << b;
             int r = 0;
             int rb_of_tl[kMaxTileBits];
             for (int b = 0; b < kMaxTileBits; ++b) rb_of_tl[b] = -1;
@@ -328,7 +393,7 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             // thread bits: lanes first, covering distinct residues mod W (bank spread)
             std::vector<int> free_bits;
             for (int b = 0; b < k; ++b)
-                if (!(rbits >> b & 1)) free_bits.push_back(b);
+                if (!(rbits >> b & 1) && !(wb >> b & 1)) free_bits.push_back(b);
             std::vector<int> lanes, rest;
             std::vector<bool> used(free_bits.size(), false);
             const int nl = std::min<int>(5, (int)free_bits.size());
@@ -350,6 +415,8 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             int ti = 0;
             for (int l : lanes) dp.thr_tl[ti++] = (int8_t)l;
             for (int l : rest) dp.thr_tl[ti++] = (int8_t)l;
+            for (int b = 0; b < k; ++b)  // the run's warp bits, in a fixed order
+                if (wb >> b & 1) dp.thr_tl[ti++] = (int8_t)b;
 
             dp.op_begin = (int)out.ops.size();
             auto rb_of_pos = [&](int p) { return rb_of_tl[tl_of_pos[p]]; };
