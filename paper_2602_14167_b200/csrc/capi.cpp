@@ -521,6 +521,7 @@ int qf_ctx_destroy(qf_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->comm) g_nccl.commDestroy(c->comm);
     for (auto& kv : c->basis_progs) qf_program_destroy(kv.second);
+    for (auto& kv : c->noise_progs) qf_program_destroy(kv.second);
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
                       &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_nodes, &c->coo_rows,
                       &c->coo_cols, &c->coo_vals})

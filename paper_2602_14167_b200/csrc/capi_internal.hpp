@@ -201,6 +201,7 @@ struct qf_ctx {
     DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_nodes, coo_rows, coo_cols, coo_vals;
     uint64_t coo_uid = 0;  // observable whose groups/terms/offsets coo_* currently hold (0: none)
     std::map<std::pair<int, int>, qf_program*> basis_progs;  // (n, precision) -> per-qubit basis rotation program
+    std::map<std::string, qf_program*> noise_progs;  // channel-free op runs of noise circuits (content key)
     int coo_n_groups = 0, coo_n_events = 0, coo_n_terms = 0;
     int64_t coo_total = 0;
     HostBuf pin;

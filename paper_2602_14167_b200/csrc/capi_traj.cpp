@@ -3,7 +3,6 @@
 // noise trajectories (qf_noise_trajectories), on the batched sweep engine plus the
 // measurement / sampling / local-operator kernels of traj.cu.
 #include <cublas_v2.h>
-#include <cusolverDn.h>
 
 #include <chrono>
 #include <complex>
@@ -102,96 +101,46 @@ int host_gate_matrix(const qf_op& o, const double* mats, int n_mats, int& D, cd 
     return QF_OK;
 }
 
-// cuBLAS / cuSOLVER, loaded at run time (only the trajectory entropy needs them)
+// cuBLAS, loaded at run time: the batched ZGEMM that forms rho = A^H A for the
+// trajectory entropy (the eigenvalues are our own kernels, eig.cu)
 struct LinAlg {
-    void *hb = nullptr, *hs = nullptr;
+    void* hb = nullptr;
     cublasHandle_t cb = nullptr;
-    cusolverDnHandle_t cs = nullptr;
     decltype(&cublasCreate_v2) bcreate = nullptr;
     decltype(&cublasSetStream_v2) bstream = nullptr;
-    decltype(&cublasZherk_v2) zherk = nullptr;
-    decltype(&cusolverDnCreate) screate = nullptr;
-    decltype(&cusolverDnSetStream) sstream = nullptr;
-    decltype(&cusolverDnZheevd_bufferSize) zheevd_ws = nullptr;
-    decltype(&cusolverDnZheevd) zheevd = nullptr;
+    decltype(&cublasZgemmStridedBatched) zgemm_sb = nullptr;
+    int device = -1;
     std::string err;
-    bool load() {
-        if (cb && cs) return true;
-        const char* bl[] = {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12",
-                            "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12"};
-        const char* sl[] = {"libcusolver.so.11", "libcusolver.so", "/usr/local/cuda/lib64/libcusolver.so.11",
-                            "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cusolver/lib/libcusolver.so.11"};
-        for (const char* nm : bl)
-            if ((hb = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
-        for (const char* nm : sl)
-            if ((hs = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
-        if (!hb || !hs) {
-            err = "cuBLAS / cuSOLVER unavailable (libcublas.so.12 / libcusolver.so.11)";
+    bool load(int dev) {
+        if (cb && device == dev) return true;
+        if (!hb) {
+            const char* bl[] = {"libcublas.so.12", "libcublas.so", "/usr/local/cuda/lib64/libcublas.so.12",
+                                "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12"};
+            for (const char* nm : bl)
+                if ((hb = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+            if (!hb) {
+                err = "cuBLAS unavailable (libcublas.so.12)";
+                return false;
+            }
+            bcreate = (decltype(bcreate))dlsym(hb, "cublasCreate_v2");
+            bstream = (decltype(bstream))dlsym(hb, "cublasSetStream_v2");
+            zgemm_sb = (decltype(zgemm_sb))dlsym(hb, "cublasZgemmStridedBatched");
+            if (!bcreate || !bstream || !zgemm_sb) {
+                err = "cuBLAS lacks required symbols";
+                return false;
+            }
+        }
+        cb = nullptr;  // a handle belongs to the device current at creation
+        if (bcreate(&cb) != CUBLAS_STATUS_SUCCESS) {
+            err = "cublasCreate failed";
             return false;
         }
-        bcreate = (decltype(bcreate))dlsym(hb, "cublasCreate_v2");
-        bstream = (decltype(bstream))dlsym(hb, "cublasSetStream_v2");
-        zherk = (decltype(zherk))dlsym(hb, "cublasZherk_v2");
-        screate = (decltype(screate))dlsym(hs, "cusolverDnCreate");
-        sstream = (decltype(sstream))dlsym(hs, "cusolverDnSetStream");
-        zheevd_ws = (decltype(zheevd_ws))dlsym(hs, "cusolverDnZheevd_bufferSize");
-        zheevd = (decltype(zheevd))dlsym(hs, "cusolverDnZheevd");
-        if (!bcreate || !bstream || !zherk || !screate || !sstream || !zheevd_ws || !zheevd) {
-            err = "cuBLAS / cuSOLVER lack required symbols";
-            return false;
-        }
-        if (bcreate(&cb) != CUBLAS_STATUS_SUCCESS || screate(&cs) != CUSOLVER_STATUS_SUCCESS) {
-            err = "cuBLAS / cuSOLVER handle creation failed";
-            return false;
-        }
+        device = dev;
         return true;
     }
 };
 LinAlg g_linalg;
 std::mutex g_linalg_mu;
-
-// One ZHEEVD of a 1024 x 1024 matrix is latency bound (~12 ms on one stream);
-// spectra run concurrently on kEigLanes host threads, each with its own stream,
-// cuBLAS / cuSOLVER handles and scratch.
-constexpr int kEigLanes = 8;
-struct EigLane {
-    int device = -1;
-    cudaStream_t st = nullptr;
-    cublasHandle_t cb = nullptr;
-    cusolverDnHandle_t cs = nullptr;
-    DevBuf conv, rho, work, info;
-    int64_t dk = 0;
-    int lwork = 0;
-};
-EigLane g_lanes[kEigLanes];
-
-int lane_setup(EigLane& L, const LinAlg& la, int device, int64_t dk, size_t N) {
-    if (L.device != device) {
-        if (L.st) {
-            cudaStreamDestroy(L.st);
-            L.st = nullptr;
-        }
-        L.cb = nullptr;
-        L.cs = nullptr;
-        L.device = device;
-    }
-    if (!L.st) QF_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
-    if (!L.cb && la.bcreate(&L.cb) != CUBLAS_STATUS_SUCCESS) return set_err(QF_ERUNTIME, "cublasCreate failed");
-    if (!L.cs && la.screate(&L.cs) != CUSOLVER_STATUS_SUCCESS) return set_err(QF_ERUNTIME, "cusolverDnCreate failed");
-    if (la.bstream(L.cb, L.st) != CUBLAS_STATUS_SUCCESS || la.sstream(L.cs, L.st) != CUSOLVER_STATUS_SUCCESS)
-        return set_err(QF_ERUNTIME, "cuBLAS / cuSOLVER stream binding failed");
-    QF_CUDA(L.conv.reserve(N * 16));
-    QF_CUDA(L.rho.reserve((size_t)dk * dk * 16));
-    QF_CUDA(L.info.reserve(16));
-    if (L.dk != dk) {
-        if (la.zheevd_ws(L.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
-                         (const cuDoubleComplex*)L.rho.p, (int)dk, nullptr, &L.lwork) != CUSOLVER_STATUS_SUCCESS)
-            return set_err(QF_ERUNTIME, "cusolverDnZheevd_bufferSize failed");
-        L.dk = dk;
-    }
-    QF_CUDA(L.work.reserve(std::max<size_t>(16, (size_t)L.lwork * 16)));
-    return QF_OK;
-}
 
 }  // namespace
 
@@ -315,14 +264,16 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     QF_CUDA(d_scale.reserve((size_t)bc * 8));
     QF_CUDA(d_out.reserve((size_t)bc * kMeasMax * 4));
     QF_CUDA(d_w.reserve((size_t)bc * dk * 8));
-    std::lock_guard<std::mutex> linalg_lock(g_linalg_mu);  // the eigen lanes are process-wide
-    if (!g_linalg.load()) return set_err(QF_ERUNTIME, g_linalg.err);
+    std::lock_guard<std::mutex> linalg_lock(g_linalg_mu);  // the cuBLAS handle is process-wide
+    if (!g_linalg.load(ctx->device)) return set_err(QF_ERUNTIME, g_linalg.err);
     LinAlg& la = g_linalg;
-    const int lanes = std::max(1, std::min(kEigLanes, bc));
-    for (int l = 0; l < lanes; ++l) {
-        int rc = lane_setup(g_lanes[l], la, ctx->device, dk, N);
-        if (rc) return rc;
-    }
+    // spectra in sub-batches: converted states (complex64) + rho + tridiagonals
+    const size_t per_eig = (precision == QF_C64 ? N * 16 : 0) + (size_t)dk * dk * 16 + (size_t)dk * 16;
+    const int esub = (int)std::max<size_t>(1, std::min<size_t>((size_t)bc, ((size_t)4 << 30) / per_eig));
+    LocalBuf d_conv, d_rho, d_tri;
+    if (precision == QF_C64) QF_CUDA(d_conv.reserve((size_t)esub * N * 16));
+    QF_CUDA(d_rho.reserve((size_t)esub * dk * dk * 16));
+    QF_CUDA(d_tri.reserve((size_t)esub * dk * 16));
     std::vector<double> w_host((size_t)bc * dk);
     std::vector<MeasRound> rounds(bc);
     for (int t0 = 0; t0 < trajectories; t0 += bc) {
@@ -397,48 +348,25 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
         }
         // half-chain entropy: eigenvalues of A^H A, A = psi as a (de x dk) column-major
         // matrix (same spectrum as the reference's SVD of psi reshaped to dk x de)
-        QF_CUDA(cudaStreamSynchronize(s));
-        {
-            std::vector<std::thread> pool;
-            std::vector<int> lane_rc(lanes, QF_OK);
-            std::vector<std::string> lane_err(lanes);
-            for (int l = 0; l < lanes; ++l)
-                pool.emplace_back([&, l] {
-                    EigLane& L = g_lanes[l];
-                    cudaSetDevice(ctx->device);
-                    const double one = 1.0, zero = 0.0;
-                    // double-precision spectrum for both state precisions: a complex64 CHEEVD
-                    // loses the small Schmidt values (n = 20: -0.22 bits of mean entropy)
-                    for (int b = l; b < nb; b += lanes) {
-                        cudaError_t e = launch_convert_state(
-                            precision, (const unsigned char*)ctx->psi.p + (size_t)b * N * vs, (double*)L.conv.p,
-                            (int64_t)N, L.st);
-                        if (e != cudaSuccess) {
-                            lane_rc[l] = QF_ECUDA;
-                            lane_err[l] = cudaGetErrorString(e);
-                            return;
-                        }
-                        if (la.zherk(L.cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, (int)dk, (int)de, &one,
-                                     (const cuDoubleComplex*)L.conv.p, (int)de, &zero, (cuDoubleComplex*)L.rho.p,
-                                     (int)dk) != CUBLAS_STATUS_SUCCESS ||
-                            la.zheevd(L.cs, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, (int)dk,
-                                      (cuDoubleComplex*)L.rho.p, (int)dk, (double*)d_w.p + (size_t)b * dk,
-                                      (cuDoubleComplex*)L.work.p, L.lwork, (int*)L.info.p) !=
-                                CUSOLVER_STATUS_SUCCESS) {
-                            lane_rc[l] = QF_ERUNTIME;
-                            lane_err[l] = "cuBLAS ZHERK / cuSOLVER ZHEEVD failed";
-                            return;
-                        }
-                    }
-                    cudaError_t e = cudaStreamSynchronize(L.st);
-                    if (e != cudaSuccess) {
-                        lane_rc[l] = QF_ECUDA;
-                        lane_err[l] = cudaGetErrorString(e);
-                    }
-                });
-            for (auto& th : pool) th.join();
-            for (int l = 0; l < lanes; ++l)
-                if (lane_rc[l]) return set_err(lane_rc[l], "qf_mipt_haar: " + lane_err[l]);
+        // (double precision for both state precisions: a complex64 spectrum loses
+        // the small Schmidt values, n = 20: -0.22 bits of mean entropy)
+        if (la.bstream(la.cb, s) != CUBLAS_STATUS_SUCCESS) return set_err(QF_ERUNTIME, "cublasSetStream failed");
+        for (int e0 = 0; e0 < nb; e0 += esub) {
+            const int ne = std::min(esub, nb - e0);
+            const cuDoubleComplex* A = (const cuDoubleComplex*)((const unsigned char*)ctx->psi.p + (size_t)e0 * N * vs);
+            if (precision == QF_C64) {
+                QF_CUDA(launch_convert_state(precision, A, (double*)d_conv.p, (int64_t)N * ne, s));
+                A = (const cuDoubleComplex*)d_conv.p;
+            }
+            const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+            if (la.zgemm_sb(la.cb, CUBLAS_OP_C, CUBLAS_OP_N, (int)dk, (int)dk, (int)de, &one, A, (int)de,
+                            (long long)N, A, (int)de, (long long)N, &zero, (cuDoubleComplex*)d_rho.p, (int)dk,
+                            (long long)dk * dk, ne) != CUBLAS_STATUS_SUCCESS)
+                return set_err(QF_ERUNTIME, "qf_mipt_haar: cuBLAS ZGEMM failed");
+            QF_CUDA(launch_hermitian_eigvals((double2*)d_rho.p, (int)dk, ne, (double*)d_tri.p,
+                                             (double*)d_tri.p + (size_t)ne * dk, (double*)d_w.p + (size_t)e0 * dk,
+                                             s));
+            ctx->launches += 3;
         }
         QF_CUDA(cudaMemcpyAsync(w_host.data(), d_w.p, (size_t)nb * dk * 8, cudaMemcpyDeviceToHost, s));
         QF_CUDA(cudaStreamSynchronize(s));
@@ -640,8 +568,49 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
         QF_CUDA(d_part.reserve((size_t)bc * tiles_h * 8));
         QF_CUDA(d_E.reserve((size_t)bc * 8));
     }
-    std::vector<double2> rho((size_t)bc * parts * 16), km((size_t)bc * 16);
-    std::vector<double> logp(bc);
+    // Channel-free runs of >= 2 ops go through compiled fused-sweep programs (one
+    // HBM pass per sweep instead of one per gate), cached on the context by content
+    // (n, precision, ops, their matrices) so repeated calls reuse the kernels.
+    struct Seg { int j0, j1; qf_program* prog; };
+    std::vector<Seg> segs;
+    size_t seg_mat = 16;
+    for (int j = 0; j < n_ops;) {
+        if (op_chan_ptr[j + 1] > op_chan_ptr[j]) { ++j; continue; }
+        int j1 = j;
+        while (j1 < n_ops && op_chan_ptr[j1 + 1] == op_chan_ptr[j1]) ++j1;
+        if (j1 - j >= 2) {
+            std::string key((const char*)&n, sizeof n);
+            key.append((const char*)&precision, sizeof precision);
+            for (int q = j; q < j1; ++q)  // every field but `reserved`
+                key.append((const char*)(ops + q), offsetof(qf_op, reserved));
+            for (int q = j; q < j1; ++q)
+                if (ops[q].mat >= 0 && mats && ops[q].mat < n_mats)
+                    key.append((const char*)(mats + 32 * (size_t)ops[q].mat), 32 * sizeof(double));
+            qf_program*& pg = ctx->noise_progs[key];
+            if (!pg) {
+                int rc = qf_program_create(ctx, n, j1 - j, ops + j, mats, n_mats, 0, precision, &pg);
+                if (rc) {
+                    ctx->noise_progs.erase(key);
+                    return rc;
+                }
+            }
+            segs.push_back({j, j1, pg});
+            seg_mat = std::max(seg_mat, (size_t)pg->plan.fwd.total_mat * vs);
+        }
+        j = j1;
+    }
+    if (!segs.empty()) QF_CUDA(ctx->gmat.reserve((size_t)bc * seg_mat));
+    // Kraus operators, uniforms, log-probabilities and the error flag live on the
+    // device: branch picks run in a kernel, so a chunk needs no host round trip
+    // until its results are read back.
+    LocalBuf d_kraus, d_u, d_logp, d_err;
+    const int n_kraus = n_apps > 0 ? chan_kraus_ptr[*std::max_element(op_chan, op_chan + n_apps) + 1] : 0;
+    QF_CUDA(d_kraus.reserve(std::max<size_t>(16, (size_t)n_kraus * 32 * 8)));
+    if (n_kraus) QF_CUDA(cudaMemcpyAsync(d_kraus.p, kraus, (size_t)n_kraus * 32 * 8, cudaMemcpyHostToDevice, s));
+    QF_CUDA(d_u.reserve(std::max<size_t>(16, (size_t)bc * n_apps * 8)));
+    QF_CUDA(d_logp.reserve((size_t)bc * 8));
+    QF_CUDA(d_err.reserve(16));
+    QF_CUDA(cudaMemsetAsync(d_err.p, 0, 4, s));
     std::vector<float> fbuf;
     for (int t0 = 0; t0 < trajectories; t0 += bc) {
         const int nb = std::min(bc, trajectories - t0);
@@ -649,74 +618,70 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
             QF_CUDA(launch_init_state(precision, ctx->lam.p, d_init.p, n, nb, s));
         else
             QF_CUDA(launch_set_basis0(precision, ctx->lam.p, n, nb, s));
-        std::fill(logp.begin(), logp.end(), 0.0);
+        QF_CUDA(cudaMemsetAsync(d_logp.p, 0, (size_t)nb * 8, s));
+        if (n_apps)
+            QF_CUDA(cudaMemcpyAsync(d_u.p, u + (size_t)t0 * n_apps, (size_t)nb * n_apps * 8, cudaMemcpyHostToDevice, s));
         int app = 0;
-        for (int j = 0; j < n_ops; ++j) {
-            const int D = Dg[j];
-            QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_gm.p + (size_t)j * 16,
-                                       false, s));
+        size_t si = 0;
+        for (int j = 0; j < n_ops;) {
+            if (si < segs.size() && segs[si].j0 == j) {  // fused channel-free run
+                qf_program* pg = segs[si].prog;
+                const ProgramPlan& PP = pg->plan;
+                SweepArgs sa{};
+                sa.psi = ctx->lam.p;
+                sa.n = n;
+                sa.gates = (const DevGate*)pg->gates.p;
+                sa.cmats = (const double*)pg->cmats.p;
+                sa.gmat = ctx->gmat.p;
+                sa.gmat_stride = PP.fwd.total_mat;
+                QF_CUDA(launch_mats(precision, false, (const DevOp*)pg->fwd.ops.p, (const int*)pg->goff_fwd.p,
+                                    (int)PP.fwd.ops.size(), sa.gates, sa.cmats, nullptr, 0, 0, ctx->gmat.p,
+                                    sa.gmat_stride, 0, nb, s));
+                sa.phases = (const DevPhase*)pg->fwd.phases.p;
+                sa.ops = (const DevOp*)pg->fwd.ops.p;
+                for (size_t i = 0; i < PP.fwd.sweeps.size(); ++i) {
+                    sa.sw = PP.fwd.sweeps[i];
+                    if (pg->use_jit)
+                        QF_CUDA((cudaError_t)jit_launch(pg->jf.sweeps[i], sa, 1 << (n - sa.sw.k), nb, s));
+                    else
+                        QF_CUDA(launch_sweep(precision, false, sa, nb, PP.fwd.max_mat, 0, s));
+                    ctx->launches++;
+                }
+                ctx->launches++;
+                j = segs[si++].j1;
+                continue;
+            }
+            const int c0 = op_chan_ptr[j], c1 = op_chan_ptr[j + 1];
+            const double2* g = (const double2*)d_gm.p + (size_t)j * 16;
+            if (c0 == c1) {
+                QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], g, false, s));
+                ctx->launches++;
+                ++j;
+                continue;
+            }
+            // gate, then per channel: rho of the current state on the gate's wires ->
+            // branch pick -> K / sqrt(p) (fused with the next channel's rho)
+            QF_CUDA(launch_apply_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], g, false, (double2*)d_rho.p, s));
             ctx->launches++;
-            for (int ci = op_chan_ptr[j]; ci < op_chan_ptr[j + 1]; ++ci, ++app) {
+            for (int ci = c0; ci < c1; ++ci, ++app) {
                 const int ch = op_chan[ci];
                 const int k0 = chan_kraus_ptr[ch], k1 = chan_kraus_ptr[ch + 1];
                 if (k1 <= k0) return set_err(QF_EINVAL, "KrausChannel: no operators");
-                QF_CUDA(launch_local_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], (double2*)d_rho.p, s));
-                QF_CUDA(cudaMemcpyAsync(rho.data(), d_rho.p, (size_t)nb * parts * D * D * 16, cudaMemcpyDeviceToHost,
-                                        s));
-                QF_CUDA(cudaStreamSynchronize(s));
-                for (int b = 0; b < nb; ++b) {
-                    double2 r[16];
-                    for (int e = 0; e < D * D; ++e) {  // parts summed in order
-                        double x = 0.0, y = 0.0;
-                        for (int pt = 0; pt < parts; ++pt) {
-                            x += rho[((size_t)b * parts + pt) * D * D + e].x;
-                            y += rho[((size_t)b * parts + pt) * D * D + e].y;
-                        }
-                        r[e] = make_double2(x, y);
-                    }
-                    std::vector<double> probs;
-                    double acc = 0.0;
-                    for (int k = k0; k < k1; ++k) {  // p_k = || K_k psi ||^2 = tr(K rho K^dagger)
-                        const double* K = kraus + 32 * (size_t)k;
-                        double pk = 0.0;
-                        for (int a = 0; a < D; ++a) {
-                            cd kr[4];
-                            for (int i = 0; i < D; ++i) kr[i] = cd(K[(a * 4 + i) * 2], K[(a * 4 + i) * 2 + 1]);
-                            cd sa = 0.0;
-                            for (int i = 0; i < D; ++i)
-                                for (int jj = 0; jj < D; ++jj)
-                                    sa += kr[i] * cd(r[i * D + jj].x, r[i * D + jj].y) * std::conj(kr[jj]);
-                            pk += sa.real();
-                        }
-                        probs.push_back(pk);
-                        acc += pk;
-                    }
-                    if (!(acc > 1e-14)) return set_err(QF_EINVAL, "mc_trajectory: all branch probabilities vanish");
-                    const double uu = u[(size_t)(t0 + b) * n_apps + app] * acc;
-                    size_t pick = probs.size() - 1;
-                    double run = 0.0;
-                    for (size_t i = 0; i < probs.size(); ++i) {
-                        run += probs[i];
-                        if (uu < run) {
-                            pick = i;
-                            break;
-                        }
-                    }
-                    const double pp = probs[pick], sc = 1.0 / std::sqrt(pp);
-                    const double* K = kraus + 32 * (size_t)(k0 + pick);
-                    for (int a = 0; a < D; ++a)
-                        for (int i = 0; i < D; ++i)
-                            km[(size_t)b * D * D + a * D + i] =
-                                make_double2(K[(a * 4 + i) * 2] * sc, K[(a * 4 + i) * 2 + 1] * sc);
-                    logp[b] += std::log(pp / acc) + std::log(acc);
-                }
-                QF_CUDA(cudaMemcpyAsync(d_k.p, km.data(), (size_t)nb * D * D * 16, cudaMemcpyHostToDevice, s));
-                QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true, s));
+                QF_CUDA(launch_kraus_pick((const double2*)d_rho.p, parts, Dg[j], (const double*)d_kraus.p, k0, k1,
+                                          (const double*)d_u.p, n_apps, app, (double2*)d_k.p, (double*)d_logp.p,
+                                          (int*)d_err.p, nb, s));
+                if (ci + 1 < c1)
+                    QF_CUDA(launch_apply_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true,
+                                             (double2*)d_rho.p, s));
+                else
+                    QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true,
+                                               s));
                 ctx->launches += 2;
             }
+            ++j;
         }
         if (log_probs)
-            for (int b = 0; b < nb; ++b) log_probs[t0 + b] = logp[b];
+            QF_CUDA(cudaMemcpyAsync(log_probs + t0, d_logp.p, (size_t)nb * 8, cudaMemcpyDeviceToHost, s));
         if (obs) {
             HArgs ha{};
             ha.psi = ctx->lam.p;
@@ -748,6 +713,9 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
             }
         }
         QF_CUDA(cudaStreamSynchronize(s));
+        int err = 0;
+        QF_CUDA(cudaMemcpy(&err, d_err.p, 4, cudaMemcpyDeviceToHost));
+        if (err) return set_err(QF_EINVAL, "mc_trajectory: all branch probabilities vanish");
     }
     return QF_OK;
 }

@@ -98,12 +98,23 @@ cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const dou
 // on every state; m = [D][D] complex row-major, shared or one per state
 cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                                cudaStream_t s);
-// reduced density matrix of every state on those wires, as local_rho_parts(n)
-// fixed-order partials: rho [batch][parts][D][D] (the caller sums the parts in order)
+// number of fixed-order rho partials per state of launch_apply_rho
 int local_rho_parts(int n);
-cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
-                             cudaStream_t s);
 cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);
+// noise step: operator m on wires (p0[, p1]) then the local rho partials of the
+// result on those wires ([batch][local_rho_parts(n)][D][D], fixed order)
+cudaError_t launch_apply_rho(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
+                             double2* rho, cudaStream_t s);
+// per-trajectory Kraus branch pick for one channel application (kraus: [k][4][4]
+// complex, channel = k0 .. k1-1; u[b * u_stride + app]); kout [batch][D][D],
+// logp[b] += log p_pick; err = 1 if all branch probabilities vanish
+cudaError_t launch_kraus_pick(const double2* rho, int parts, int D, const double* kraus, int k0, int k1, const double* u,
+                              int u_stride, int app, double2* kout, double* logp, int* err, int batch, cudaStream_t s);
+
+// eigenvalues (ascending) of `batch` Hermitian m x m matrices (column-major, both
+// triangles, overwritten): Householder tridiagonalisation + Sturm bisection (eig.cu);
+// d, e: [batch][m] scratch each, w: [batch][m]; m <= 4096
+cudaError_t launch_hermitian_eigvals(double2* A, int m, int batch, double* d, double* e, double* w, cudaStream_t s);
 
 // rows / cols ascending per row, complex128 values
 cudaError_t launch_coo_write(const CooGroup* g, int n_groups, const CooTerm* t, int n_terms, const CooEvent* ev,

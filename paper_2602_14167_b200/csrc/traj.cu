@@ -176,7 +176,7 @@ __global__ void sample_pick_kernel(const V* psi, int n, int chunk_bits, const do
 
 // Local operator on wires (w0[, w1]) of every state: amplitude quads / pairs in
 // the local basis (w0 most significant), matrix shared (mstride = 0) or per state.
-// Used by the noise trajectories, where every gate / Kraus branch is its own pass.
+// Used by the noise trajectories for gates without channels and final Kraus branches.
 template <typename V, int D>
 __global__ void apply_local_kernel(V* psi, int n, int p0, int p1, const double2* m, int mstride) {
     const int b = blockIdx.y;
@@ -216,42 +216,80 @@ __global__ void apply_local_kernel(V* psi, int n, int p0, int p1, const double2*
     }
 }
 
-// rho partials [b][part][i][j] = sum over part of the other wires' indices of
-// psi_i conj(psi_j) on wires (w0[, w1]); fixed order (the caller sums the parts)
+// Noise step pass: a D x D operator (the gate, shared, or a per-trajectory Kraus
+// branch K/sqrt(p)) on wires (w0[, w1]) of every state, and the local density
+// matrix of the RESULT on the same wires as fixed-order partials [b][part][D][D]
+// (the next channel on that gate picks its branch from it).  One read + one write
+// of the state replaces the separate operator and reduction passes.
 template <typename V, int D>
-__global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int p0, int p1, double2* rho) {
+__global__ void __launch_bounds__(256) apply_rho_kernel(V* psi, int n, int p0, int p1, const double2* m, int mstride,
+                                                        double2* rho) {
     __shared__ double red[8][2 * D * D];
     const int b = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
+    const double2* mb = m + (size_t)b * mstride;
+    double2 mm[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) mm[i] = mb[i];
     const uint32_t N = 1u << n, R = N / D;
     const uint32_t mask = D == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
     const uint32_t free = (N - 1) & ~mask;
-    const V* ps = psi + (size_t)b * N;
+    V* ps = psi + (size_t)b * N;
     double acc[2 * D * D];
 #pragma unroll
     for (int i = 0; i < 2 * D * D; ++i) acc[i] = 0.0;
     const uint32_t r0 = (uint32_t)((uint64_t)R * part / parts), r1 = (uint32_t)((uint64_t)R * (part + 1) / parts);
-    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        const uint32_t base = pdep32(r, free);
-        double2 a[D];
+    // two amplitude groups per iteration, both loaded before either is stored
+    // (the stores would otherwise order every next load behind them)
+    constexpr int U = 2;
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += U * blockDim.x) {
+        uint32_t idx[U][D];
+        double2 a[U][D];
+        bool live[U];
 #pragma unroll
-        for (int i = 0; i < D; ++i) {
-            const uint32_t x = base | (D == 2 ? (i ? (1u << p0) : 0u)
-                                              : (((i >> 1) & 1) ? (1u << p0) : 0u) | ((i & 1) ? (1u << p1) : 0u));
-            const V v = ps[x];
-            a[i] = make_double2((double)v.x, (double)v.y);
+        for (int u = 0; u < U; ++u) {
+            const uint32_t ru = r + u * blockDim.x;
+            live[u] = ru < r1;
+            const uint32_t base = pdep32(live[u] ? ru : r, free);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                idx[u][i] = base | (D == 2 ? (i ? (1u << p0) : 0u)
+                                           : (((i >> 1) & 1) ? (1u << p0) : 0u) | ((i & 1) ? (1u << p1) : 0u));
+                const V v = ps[idx[u][i]];
+                a[u][i] = make_double2((double)v.x, (double)v.y);
+            }
         }
 #pragma unroll
-        for (int i = 0; i < D; ++i)
+        for (int u = 0; u < U; ++u) {
+            if (!live[u]) continue;
+            double2 o[D];
 #pragma unroll
-            for (int j = 0; j < D; ++j) {
-                acc[2 * (i * D + j)] += a[i].x * a[j].x + a[i].y * a[j].y;
-                acc[2 * (i * D + j) + 1] += a[i].y * a[j].x - a[i].x * a[j].y;
+            for (int i = 0; i < D; ++i) {
+                double re = 0.0, im = 0.0;
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    const double2 c = mm[i * D + j];
+                    re += c.x * a[u][j].x - c.y * a[u][j].y;
+                    im += c.x * a[u][j].y + c.y * a[u][j].x;
+                }
+                V w;
+                w.x = (decltype(w.x))re;
+                w.y = (decltype(w.y))im;
+                ps[idx[u][i]] = w;
+                o[i] = make_double2((double)w.x, (double)w.y);  // the stored (rounded) amplitude
             }
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    acc[2 * (i * D + j)] += o[i].x * o[j].x + o[i].y * o[j].y;
+                    acc[2 * (i * D + j) + 1] += o[i].y * o[j].x - o[i].x * o[j].y;
+                }
+        }
     }
 #pragma unroll
     for (int i = 0; i < 2 * D * D; ++i) {
         double v = acc[i];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = v;
     }
     __syncthreads();
@@ -262,7 +300,108 @@ __global__ void __launch_bounds__(256) local_rho_kernel(const V* psi, int n, int
     }
 }
 
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// branch probability p_k = tr(K_k rho K_k^dagger) (reference noise.cpp:178-185)
+__device__ double kraus_prob(const double* K, const double2* r, int D) {
+    double pk = 0.0;
+    for (int a = 0; a < D; ++a) {
+        double2 sa = make_double2(0.0, 0.0);
+        for (int i = 0; i < D; ++i) {
+            const double2 ki = make_double2(K[(a * 4 + i) * 2], K[(a * 4 + i) * 2 + 1]);
+            for (int j = 0; j < D; ++j) {
+                const double2 kj = make_double2(K[(a * 4 + j) * 2], -K[(a * 4 + j) * 2 + 1]);
+                const double2 t = zmul(zmul(ki, r[i * D + j]), kj);
+                sa.x += t.x;
+                sa.y += t.y;
+            }
+        }
+        pk += sa.x;
+    }
+    return pk;
+}
+
+// One warp per trajectory: the reference's branch pick for one channel
+// application (noise.cpp:186-195: first k with u * sum(p) < running sum, else the
+// last), from the rho partials (lane l sums parts l, l + 32, ... in order, then a
+// fixed xor-shuffle tree: the order depends only on n); writes K_pick / sqrt(p_pick)
+// and accumulates log p.  err = 1 when every branch probability vanishes.
+__global__ void __launch_bounds__(128) kraus_pick_kernel(const double2* rho, int parts, int D, const double* kraus,
+                                                         int k0, int k1, const double* u, int u_stride, int app,
+                                                         double2* kout, double* logp, int* err, int batch) {
+    const int b = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (b >= batch) return;
+    double2 r[16];
+    for (int e = 0; e < 16; ++e) r[e] = make_double2(0.0, 0.0);
+    for (int pt = lane; pt < parts; pt += 32)
+        for (int e = 0; e < D * D; ++e) {
+            const double2 v = rho[((size_t)b * parts + pt) * D * D + e];
+            r[e].x += v.x;
+            r[e].y += v.y;
+        }
+    for (int e = 0; e < D * D; ++e)
+        for (int o = 16; o > 0; o >>= 1) {
+            r[e].x += __shfl_xor_sync(0xffffffffu, r[e].x, o);
+            r[e].y += __shfl_xor_sync(0xffffffffu, r[e].y, o);
+        }
+    if (lane) return;
+    double acc = 0.0;
+    for (int k = k0; k < k1; ++k) acc += kraus_prob(kraus + 32 * (size_t)k, r, D);
+    if (!(acc > 1e-14)) {
+        atomicExch(err, 1);
+        for (int e = 0; e < D * D; ++e) kout[(size_t)b * D * D + e] = make_double2(0.0, 0.0);
+        return;
+    }
+    const double uu = u[(size_t)b * u_stride + app] * acc;
+    int pick = k1 - 1;
+    double pp = 0.0, run = 0.0;
+    bool hit = false;
+    for (int k = k0; k < k1; ++k) {
+        const double pk = kraus_prob(kraus + 32 * (size_t)k, r, D);
+        run += pk;
+        pp = pk;
+        if (uu < run) {
+            pick = k;
+            hit = true;
+            break;
+        }
+    }
+    if (!hit) pp = kraus_prob(kraus + 32 * (size_t)pick, r, D);
+    const double sc = 1.0 / sqrt(pp);
+    const double* K = kraus + 32 * (size_t)pick;
+    for (int a = 0; a < D; ++a)
+        for (int i = 0; i < D; ++i)
+            kout[(size_t)b * D * D + a * D + i] = make_double2(K[(a * 4 + i) * 2] * sc, K[(a * 4 + i) * 2 + 1] * sc);
+    logp[b] += log(pp / acc) + log(acc);
+}
+
 }  // namespace
+
+cudaError_t launch_apply_rho(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
+                             double2* rho, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    const int D = p1 >= 0 ? 4 : 2;
+    const dim3 grid(local_rho_parts(n), batch);
+    const int ms = per_state ? D * D : 0;
+    if (prec == 1) {
+        if (D == 2) apply_rho_kernel<double2, 2><<<grid, 256, 0, s>>>((double2*)psi, n, p0, p1, m, ms, rho);
+        else apply_rho_kernel<double2, 4><<<grid, 256, 0, s>>>((double2*)psi, n, p0, p1, m, ms, rho);
+    } else {
+        if (D == 2) apply_rho_kernel<float2, 2><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms, rho);
+        else apply_rho_kernel<float2, 4><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms, rho);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_kraus_pick(const double2* rho, int parts, int D, const double* kraus, int k0, int k1, const double* u,
+                              int u_stride, int app, double2* kout, double* logp, int* err, int batch, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    kraus_pick_kernel<<<(batch + 3) / 4, 128, 0, s>>>(rho, parts, D, kraus, k0, k1, u, u_stride, app, kout, logp,
+                                                          err, batch);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                                cudaStream_t s) {
@@ -281,21 +420,8 @@ cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, in
     return cudaGetLastError();
 }
 
-int local_rho_parts(int n) { return n >= 14 ? 16 : 1; }
-
-cudaError_t launch_local_rho(int prec, const void* psi, int n, int batch, int p0, int p1, double2* rho,
-                             cudaStream_t s) {
-    if (batch == 0) return cudaSuccess;
-    const dim3 grid(local_rho_parts(n), batch);
-    if (prec == 1) {
-        if (p1 < 0) local_rho_kernel<double2, 2><<<grid, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
-        else local_rho_kernel<double2, 4><<<grid, 256, 0, s>>>((const double2*)psi, n, p0, p1, rho);
-    } else {
-        if (p1 < 0) local_rho_kernel<float2, 2><<<grid, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
-        else local_rho_kernel<float2, 4><<<grid, 256, 0, s>>>((const float2*)psi, n, p0, p1, rho);
-    }
-    return cudaGetLastError();
-}
+// fixed number of rho partials per state (one CTA each): ~2^(n-9) amplitudes per CTA
+int local_rho_parts(int n) { return n < 10 ? 1 : 1 << std::min(8, n - 10); }
 
 int sample_chunk_bits(int n) { return n > 10 ? 10 : n; }
 

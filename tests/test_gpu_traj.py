@@ -11,7 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("n,depth,p,traj", [(2, 3, 0.5, 4), (5, 6, 0.3, 6), (6, 10, 0.2, 8), (8, 8, 0.1, 5),
-                                            (10, 3, 1.0, 3), (7, 0, 0.5, 2), (9, 5, 0.0, 3)])
+                                            (10, 3, 1.0, 3), (7, 0, 0.5, 2), (9, 5, 0.0, 3), (12, 6, 0.1, 3),
+                                            (14, 4, 0.2, 2)])
 @pytest.mark.parametrize("prec,tol", [("c128", 1e-9), ("c64", 2e-4)])
 def test_mipt_haar_matches_oracle(ctx, n, depth, p, traj, prec, tol):
     ref = po.mipt_haar(n, depth, p, traj, 1234 + n)
@@ -109,6 +110,24 @@ def test_noise_trajectories_match_oracle(ctx, n, depth):
         ref_s, ref_l = po.mc_trajectory(n, ops, op_ch, chans, u[t])
         assert np.abs(states[t] - ref_s).max() < 1e-10 and abs(logp[t] - ref_l) < 1e-10
         assert abs(ev[t] - po.expectation(n, ref_s, h).real) < 1e-10
+
+
+@pytest.mark.parametrize("n,depth,prec,tol", [(6, 2, "c128", 1e-10), (14, 2, "c128", 1e-10), (14, 1, "c64", 2e-5)])
+def test_noise_sparse_channels_fused_runs(ctx, n, depth, prec, tol):
+    """Channels only on cx: the channel-free h/rx runs between them go through
+    compiled fused-sweep programs, the cx channels through the device-side branch
+    picks (n = 14 uses 16 rho partials per state).  Same uniforms as the oracle."""
+    rng = po.Rng(70 + n)
+    ops = _noisy_circuit(n, depth, rng)
+    op_ch, chans = _channels_for(ops)
+    op_ch = [ch if op[0] == po.GID["cx"] else [] for ch, op in zip(op_ch, ops)]
+    T = 6
+    n_apps = sum(len(x) for x in op_ch)
+    u = np.array([[rng.uniform() for _ in range(n_apps)] for _ in range(T)])
+    states, logp, _ = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, prec)
+    for t in range(T):
+        ref_s, ref_l = po.mc_trajectory(n, ops, op_ch, chans, u[t])
+        assert np.abs(states[t] - ref_s).max() < tol and abs(logp[t] - ref_l) < tol * 10
 
 
 def test_noise_trajectory_reference_cases(ctx):

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Batched noise trajectories (qf_noise_trajectories): HEA-like circuit with a
 channel after every gate (depolarizing on cx, amplitude damping on ry, phase
-damping on rz), T trajectories, per-trajectory time; CPU baseline: the numpy
+damping on rz) or on cx only (the rotation runs between go through fused sweeps), T trajectories, per-trajectory time; CPU baseline: the numpy
 oracle restatement on one trajectory."""
 import json
 import os
@@ -17,7 +17,7 @@ from paper_2602_14167_b200 import engine  # noqa: E402
 from paper_2602_14167_b200 import qforge as qf  # noqa: E402
 
 ctx = engine.default_context(0)
-for n, layers, T in [(16, 4, 1000), (20, 4, 256)]:
+for n, layers, T, sparse in [(16, 4, 1000, False), (20, 4, 256, False), (16, 4, 1000, True), (20, 4, 256, True)]:
     rng = po.Rng(9)
     ops = []
     for _ in range(layers):
@@ -29,8 +29,8 @@ for n, layers, T in [(16, 4, 1000), (20, 4, 256)]:
     chans = [qf.depolarizing_channel(0.01, 2).operators, qf.amplitude_damping_channel(0.02).operators,
              qf.phase_damping_channel(0.02).operators]
     by = {po.GID["cx"]: [0], po.GID["ry"]: [1], po.GID["rz"]: [2]}
-    op_ch = [by[o[0]] for o in ops]
-    n_apps = len(ops)
+    op_ch = [by[o[0]] if (not sparse or o[0] == po.GID["cx"]) else [] for o in ops]
+    n_apps = sum(len(c) for c in op_ch)
     u = np.array([[rng.uniform() for _ in range(n_apps)] for _ in range(T)])
     h = po.tfim(n, 1.0)
     obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
@@ -38,7 +38,7 @@ for n, layers, T in [(16, 4, 1000), (20, 4, 256)]:
     t0 = time.perf_counter()
     _, logp, ev = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, "c64", obs=obs, want_states=False)
     dt = time.perf_counter() - t0
-    rec = {"n": n, "layers": layers, "gates": len(ops), "channel_applications": n_apps, "trajectories": T,
+    rec = {"n": n, "layers": layers, "gates": len(ops), "channel_applications": n_apps, "channels": "cx only (rotation runs fused)" if sparse else "after every gate", "trajectories": T,
            "precision": "c64", "seconds": dt, "s_per_traj": dt / T, "mean_energy": float(ev.mean())}
     if n <= 16:
         t0 = time.perf_counter()
