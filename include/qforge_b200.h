@@ -210,11 +210,18 @@ int qf_sparse_energy(qf_ctx* ctx, const qf_program* prog, int batch, const doubl
  * qubit measured with probability p (measure_collapse, circuit.cpp:391-429),
  * then entropies[t] = subsystem_entropy(psi, {0 .. n/2 - 1}) in bits.  Gates run
  * as batched sweeps with per-trajectory matrices, measurements as batched
- * histogram / collapse passes; the entropy spectrum uses cuBLAS + cuSOLVER
- * (loaded at run time).  n in [2, 20], p in [0, 1], trajectories >= 1.
+ * histogram / collapse passes; the entropy spectrum is rho = A^H A (cuBLAS
+ * batched ZGEMM, loaded at run time) reduced by our own batched Householder
+ * tridiagonalisation + Sturm bisection kernels (eig.cu, double precision).
+ * n in [2, 20], p in [0, 1], trajectories >= 1.
  * n_measurements (optional) receives the total number of collapses. */
 int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint64_t seed, int precision,
                  double* entropies, long long* n_measurements);
+
+/* Eigenvalues (ascending) of `batch` Hermitian m x m matrices a[b] (host,
+ * column-major complex128 as interleaved doubles, both triangles), through the
+ * device kernels the MIPT entropy uses (m <= 2048).  Exposed for testing. */
+int qf_hermitian_eigvals(qf_ctx* ctx, int m, int batch, const double* a, double* w);
 
 /* Classical-shadow snapshots (reference shadows.cpp:50-85): the state of `prep`
  * (at theta) rotated, per snapshot r, into bases[r][0..n) (1 = X, 2 = Y, 3 = Z;

@@ -269,7 +269,12 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
     LinAlg& la = g_linalg;
     // spectra in sub-batches: converted states (complex64) + rho + tridiagonals
     const size_t per_eig = (precision == QF_C64 ? N * 16 : 0) + (size_t)dk * dk * 16 + (size_t)dk * 16;
-    const int esub = (int)std::max<size_t>(1, std::min<size_t>((size_t)bc, ((size_t)4 << 30) / per_eig));
+    // (one CTA per matrix, one CTA per SM: sub-batches are whole waves of the SM count)
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, ctx->device);
+    size_t cap = ((size_t)6 << 30) / per_eig;
+    if (cap > (size_t)n_sm) cap -= cap % (size_t)n_sm;
+    const int esub = (int)std::max<size_t>(1, std::min<size_t>((size_t)bc, cap));
     LocalBuf d_conv, d_rho, d_tri;
     if (precision == QF_C64) QF_CUDA(d_conv.reserve((size_t)esub * N * 16));
     QF_CUDA(d_rho.reserve((size_t)esub * dk * dk * 16));
@@ -384,6 +389,26 @@ int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint
         }
     }
     if (tm) fprintf(stderr, "qf_mipt_haar: host randomness %.3f s, circuits %.3f s, entropy %.3f s\n", t_gen, t_circ, t_ent);
+    return QF_OK;
+}
+
+int qf_hermitian_eigvals(qf_ctx* ctx, int m, int batch, const double* a, double* w) {
+    if (!ctx || m < 1 || m > 2048 || batch < 0 || (batch > 0 && (!a || !w)))
+        return set_err(QF_EINVAL, "qf_hermitian_eigvals: bad arguments");
+    if (batch == 0) return QF_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    LocalBuf d_a, d_t, d_w;
+    const size_t mm = (size_t)m * m;
+    QF_CUDA(d_a.reserve((size_t)batch * mm * 16));
+    QF_CUDA(d_t.reserve((size_t)batch * m * 16));
+    QF_CUDA(d_w.reserve((size_t)batch * m * 8));
+    QF_CUDA(cudaMemcpyAsync(d_a.p, a, (size_t)batch * mm * 16, cudaMemcpyHostToDevice, s));
+    QF_CUDA(launch_hermitian_eigvals((double2*)d_a.p, m, batch, (double*)d_t.p, (double*)d_t.p + (size_t)batch * m,
+                                     (double*)d_w.p, s));
+    ctx->launches += 2;
+    QF_CUDA(cudaMemcpyAsync(w, d_w.p, (size_t)batch * m * 8, cudaMemcpyDeviceToHost, s));
+    QF_CUDA(cudaStreamSynchronize(s));
     return QF_OK;
 }
 

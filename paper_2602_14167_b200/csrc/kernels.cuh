@@ -113,7 +113,7 @@ cudaError_t launch_kraus_pick(const double2* rho, int parts, int D, const double
 
 // eigenvalues (ascending) of `batch` Hermitian m x m matrices (column-major, both
 // triangles, overwritten): Householder tridiagonalisation + Sturm bisection (eig.cu);
-// d, e: [batch][m] scratch each, w: [batch][m]; m <= 4096
+// d, e: [batch][m] scratch each, w: [batch][m]; m <= 2048
 cudaError_t launch_hermitian_eigvals(double2* A, int m, int batch, double* d, double* e, double* w, cudaStream_t s);
 
 // rows / cols ascending per row, complex128 values

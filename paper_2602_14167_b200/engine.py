@@ -364,6 +364,19 @@ def mipt_haar(ctx: Context, n: int, depth: int, p: float, trajectories: int, see
     return out, int(cnt.value)
 
 
+def hermitian_eigvals(ctx: Context, a) -> np.ndarray:
+    """Ascending eigenvalues of a batch of Hermitian matrices [batch, m, m] through the
+    device tridiagonalisation + bisection kernels (qf_hermitian_eigvals)."""
+    a = np.asarray(a, np.complex128)
+    if a.ndim == 2:
+        a = a[None]
+    B, m = int(a.shape[0]), int(a.shape[1])
+    buf = np.ascontiguousarray(np.transpose(a, (0, 2, 1))).view(np.float64)  # column-major per matrix
+    w = np.zeros((B, m))
+    check(ctx.lib.qf_hermitian_eigvals(ctx.handle, m, B, dptr(buf), dptr(w)))
+    return w
+
+
 def shadow_snapshots(ctx: Context, prep: Program, theta, bases, u) -> np.ndarray:
     """Classical-shadow outcomes (qf_shadow_snapshots, shadows.cpp:50-85):
     bases [m, n] codes 1/2/3, u [m] uniforms -> outcomes [m, n] bits (int8)."""

@@ -161,3 +161,28 @@ def test_noise_trajectory_reference_cases(ctx):
         z0 = engine.Observable(ctx, 4, np.array([[3, 0, 0, 0]], np.int8), np.array([1.0]))
         _, _, ev = engine.noise_trajectories(ctx, 4, ops, None, op_ch, chans, u, "c128", obs=z0, want_states=False)
         assert abs(ev.mean() - exact) < 3.0 / np.sqrt(T)
+
+
+@pytest.mark.parametrize("m,batch", [(1, 2), (2, 3), (33, 2), (256, 2), (1024, 2), (1500, 1)])
+def test_hermitian_eigvals_kernel(ctx, m, batch):
+    """The MIPT entropy's own eigen-solver (Householder tridiagonalisation + Sturm
+    bisection, eig.cu) against numpy eigvalsh: random Hermitian matrices and
+    rank-deficient density matrices rho = A^H A (the MIPT case: many zero or tiny
+    eigenvalues), absolute error <= 1e-12 * ||rho||."""
+    rng = np.random.default_rng(m)
+    mats = []
+    for b in range(batch):
+        if b % 2 == 0:
+            x = rng.normal(size=(m, m)) + 1j * rng.normal(size=(m, m))
+            mats.append((x + x.conj().T) / 2)
+        else:
+            r = max(1, m // 8)
+            a = rng.normal(size=(r, m)) + 1j * rng.normal(size=(r, m))
+            rho = a.conj().T @ a
+            mats.append(rho / np.trace(rho).real)
+    mats = np.array(mats)
+    got = engine.hermitian_eigvals(ctx, mats)
+    for b in range(batch):
+        ref = np.linalg.eigvalsh(mats[b])
+        scale = max(1.0, np.abs(ref).max())
+        assert np.abs(got[b] - ref).max() <= 1e-12 * scale * max(1, m / 64), (b, np.abs(got[b] - ref).max())

@@ -21,7 +21,7 @@ T = int(os.environ.get("MIPT_T", 1000))
 p = float(os.environ.get("MIPT_P", 0.1))
 prec = os.environ.get("MIPT_PREC", "c64")
 ctx = engine.default_context(0)
-engine.mipt_haar(ctx, n, 2, p, 4, 7, prec)  # warm-up: JIT kernels, cuBLAS / cuSOLVER handles
+engine.mipt_haar(ctx, n, 2, p, 4, 7, prec)  # warm-up: JIT kernels, cuBLAS handle
 best = None
 for rep in range(2):
     t0 = time.perf_counter()
