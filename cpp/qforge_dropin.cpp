@@ -330,12 +330,14 @@ void apply_local_unitary(StateVector& psi, const ComplexMatrix& u, const std::ve
     require(u.rows() == ((std::int64_t)1 << k) && u.cols() == ((std::int64_t)1 << k),
             "apply_local_unitary: wrong gate size");
     for (int w : wires) require(w >= 0 && w < psi.n, "apply_local_unitary: wire out of range");
-    require(k == 1 || k == 2, "apply_local_unitary: the device path supports 1- and 2-qubit gates");
-    Circuit c(psi.n);
-    c.ops.push_back({Gate::unitary, wires, {}, u});
-    c.initial_state = psi.amps;
-    auto prog = make_program(circuit_template(c, nullptr), 0);
-    check(qf_run_state(ctx(), prog->p, nullptr, 64, reinterpret_cast<double*>(psi.amps.data())));
+    std::vector<double> um;  // row-major for the C-ABI (ComplexMatrix is column-major, like Eigen)
+    um.reserve((size_t)u.size() * 2);
+    for (std::int64_t r = 0; r < u.rows(); ++r)
+        for (std::int64_t c = 0; c < u.cols(); ++c) {
+            um.push_back(u(r, c).real());
+            um.push_back(u(r, c).imag());
+        }
+    check(qf_apply_unitary(ctx(), psi.n, reinterpret_cast<double*>(psi.amps.data()), k, wires.data(), um.data()));
 }
 
 cplx expectation_pauli(const StateVector& psi, const PauliSum& obs) {  // circuit.cpp:319-347
@@ -827,7 +829,8 @@ AnsatzSpec hea_ansatz(int n, int layers) {
 
 namespace {
 
-bool same_matrix(const ComplexMatrix& x, const ComplexMatrix& y) {
+template <class D>
+bool same_matrix(const D& x, const D& y) {
     if (x.rows() != y.rows() || x.cols() != y.cols()) return false;
     for (std::int64_t i = 0; i < x.size(); ++i)
         if (x.data()[i] != y.data()[i]) return false;

@@ -248,6 +248,23 @@ int main() {
         z.add(1.0, {3});
         CHECK(approx(expectation_pauli(psi, z).real(), 1.0, 1e-12));
     });
+    test_case("apply_local_unitary on three wires", [] {  // circuit.cpp:147-175 (generic k)
+        // X (x) X (x) X on wires {2, 0, 1} maps |000> to |111>; a permutation
+        // unitary on wires {0, 2, 1} checks the local-bit order (wires[0] most significant)
+        StateVector psi = StateVector::zero_state(3);
+        ComplexMatrix x3 = ComplexMatrix::Zero(8, 8);
+        for (int i = 0; i < 8; ++i) x3(7 - i, i) = 1.0;
+        apply_local_unitary(psi, x3, {2, 0, 1});
+        CHECK(std::abs(psi.amps[7] - 1.0) < 1e-12);
+        StateVector e = StateVector::zero_state(3);
+        e.amps[0] = 0.0;
+        e.amps[1] = 1.0;  // |001>: qubit 2 set
+        ComplexMatrix shift = ComplexMatrix::Zero(8, 8);
+        for (int i = 0; i < 8; ++i) shift((i + 1) % 8, i) = 1.0;  // local index l -> l + 1
+        apply_local_unitary(e, shift, {0, 2, 1});  // local index of |001> = (q0, q2, q1) = 010 = 2 -> 3 = 011
+        CHECK(std::abs(e.amps[3] - 1.0) < 1e-12);  // (q0, q2, q1) = (0, 1, 1) -> q1 = q2 = 1 = |011>
+        CHECK_THROWS(apply_local_unitary(e, shift, {0, 0, 1}));
+    });
     test_case("rzz lowering", [] {  // test_circuit.cpp:302-314
         StateVector a = run(Circuit(2).h(0).h(1).rzz(0, 1, 0.9));
         StateVector b = run(Circuit(2).h(0).h(1).cx(0, 1).rz(1, 0.9).cx(0, 1));

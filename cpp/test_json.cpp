@@ -10,6 +10,7 @@
 #include <cstring>
 #include <iostream>
 #include <stdexcept>
+#include <type_traits>
 
 #include "qforge/circuit.hpp"
 #include "qforge/pauli.hpp"
@@ -55,6 +56,23 @@ int main(int argc, char** argv) {
     if (argc > 1 && std::strcmp(argv[1], "dump") == 0) {
         std::cout << fixed_circuit().to_json() << "\n" << fixed_sum().to_json() << "\n";
         return 0;
+    }
+    {  // Eigen-compatible shim: column-major data(), row-order comma init, real cwiseAbs,
+       // distinct matrix / vector types, matrix * vector -> vector
+        ComplexMatrix m(2, 3);
+        m << cplx(1, 0), cplx(2, 0), cplx(3, 0), cplx(4, 0), cplx(5, 0), cplx(6, 1);
+        CHECK(m(0, 1) == cplx(2, 0) && m(1, 0) == cplx(4, 0) && m(1, 2) == cplx(6, 1));
+        CHECK(m.data()[0] == cplx(1, 0) && m.data()[1] == cplx(4, 0) && m.data()[2] == cplx(2, 0));  // columns
+        const double mx = m.cwiseAbs().maxCoeff();
+        CHECK(std::abs(mx - std::abs(cplx(6, 1))) < 1e-15);
+        ComplexVector v = ComplexVector::Zero(3);
+        v[0] = 1.0;
+        v[2] = cplx(0, 1);
+        const ComplexVector mv = m * v;
+        CHECK(mv.size() == 2 && mv[0] == cplx(1, 3) && mv[1] == cplx(4, 0) + cplx(6, 1) * cplx(0, 1));
+        static_assert(!std::is_same_v<ComplexMatrix, ComplexVector>, "distinct types, as in Eigen");
+        const ComplexMatrix a = m.adjoint();
+        CHECK(a.rows() == 3 && a.cols() == 2 && a(2, 1) == cplx(6, -1));
     }
     {  // round trips preserve every field exactly
         Circuit c = fixed_circuit();

@@ -218,6 +218,12 @@ int qf_sparse_energy(qf_ctx* ctx, const qf_program* prog, int batch, const doubl
 int qf_mipt_haar(qf_ctx* ctx, int n, int depth, double p, int trajectories, uint64_t seed, int precision,
                  double* entropies, long long* n_measurements);
 
+/* apply_local_unitary (reference circuit.cpp:78-176) on a host complex128 state
+ * (2^n interleaved re/im, in place): U row-major 2^k x 2^k complex128 on
+ * wires[0..k) (wires[0] = most significant local bit), 1 <= k <= 13 distinct
+ * wires.  One copy in, one kernel, one copy out (no program is built). */
+int qf_apply_unitary(qf_ctx* ctx, int n, double* state, int k, const int* wires, const double* u);
+
 /* Eigenvalues (ascending) of `batch` Hermitian m x m matrices a[b] (host,
  * column-major complex128 as interleaved doubles, both triangles), through the
  * device kernels the MIPT entropy uses (m <= 2048).  Exposed for testing. */

@@ -68,6 +68,7 @@ SIGNATURES = {
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _I, _D]),
     "qf_mipt_haar": (_I, [ctypes.c_void_p, _I, _I, ctypes.c_double, _I, ctypes.c_uint64, _I, _D,
                          ctypes.POINTER(ctypes.c_longlong)]),
+    "qf_apply_unitary": (_I, [ctypes.c_void_p, _I, _D, _I, ctypes.POINTER(_I), _D]),
     "qf_hermitian_eigvals": (_I, [ctypes.c_void_p, _I, _I, _D, _D]),
     "qf_shadow_snapshots": (_I, [ctypes.c_void_p, ctypes.c_void_p, _D, _I, ctypes.c_void_p, _D, ctypes.c_void_p]),
     "qf_noise_trajectories": (_I, [ctypes.c_void_p, _I, _I, ctypes.POINTER(QfOp), _D, _I, ctypes.POINTER(_I),

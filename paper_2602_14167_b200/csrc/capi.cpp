@@ -523,7 +523,7 @@ int qf_ctx_destroy(qf_ctx* c) {
     for (auto& kv : c->basis_progs) qf_program_destroy(kv.second);
     for (auto& kv : c->noise_progs) qf_program_destroy(kv.second);
     for (DevBuf* b : {&c->psi, &c->lam, &c->tap_part, &c->tapsum, &c->epart, &c->thetas, &c->out, &c->zero_init,
-                      &c->gmat, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_nodes, &c->coo_rows,
+                      &c->gmat, &c->ul_state, &c->ul_aux, &c->coo_off, &c->coo_scratch, &c->coo_groups, &c->coo_terms, &c->coo_nodes, &c->coo_rows,
                       &c->coo_cols, &c->coo_vals})
         b->release();
     c->pin.release();

@@ -198,6 +198,7 @@ struct qf_ctx {
     cudaStream_t stream = nullptr;
     size_t budget = 0;
     DevBuf psi, lam, tap_part, tapsum, epart, thetas, out, zero_init, gmat;
+    DevBuf ul_state, ul_aux;  // apply_local_unitary scratch (one host state at a time)
     DevBuf coo_off, coo_scratch, coo_groups, coo_terms, coo_nodes, coo_rows, coo_cols, coo_vals;
     uint64_t coo_uid = 0;  // observable whose groups/terms/offsets coo_* currently hold (0: none)
     std::map<std::pair<int, int>, qf_program*> basis_progs;  // (n, precision) -> per-qubit basis rotation program

@@ -5,6 +5,7 @@
 #include <cublas_v2.h>
 
 #include <chrono>
+#include <cstring>
 #include <complex>
 #include <thread>
 
@@ -408,6 +409,45 @@ int qf_hermitian_eigvals(qf_ctx* ctx, int m, int batch, const double* a, double*
                                      (double*)d_w.p, s));
     ctx->launches += 2;
     QF_CUDA(cudaMemcpyAsync(w, d_w.p, (size_t)batch * m * 8, cudaMemcpyDeviceToHost, s));
+    QF_CUDA(cudaStreamSynchronize(s));
+    return QF_OK;
+}
+
+int qf_apply_unitary(qf_ctx* ctx, int n, double* state, int k, const int* wires, const double* u) {
+    // reference circuit.cpp:78-176 (apply_local_unitary) on a host complex128 state:
+    // one H2D copy, one kernel (no program, no JIT), one D2H copy
+    if (!ctx || !state || !wires || !u || n < 1 || n > 30) return set_err(QF_EINVAL, "qf_apply_unitary: bad arguments");
+    for (int i = 0; i < k; ++i)
+        if (wires[i] < 0 || wires[i] >= n) return set_err(QF_EINVAL, "apply_local_unitary: wire out of range");
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < i; ++j)
+            if (wires[i] == wires[j]) return set_err(QF_EINVAL, "apply_local_unitary: wires must be distinct");
+    if (k < 1 || k > 13) return set_err(QF_EINVAL, "apply_local_unitary: 1 to 13 wires on the device path");
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const size_t N = size_t(1) << n, DK = size_t(1) << k;
+    QF_CUDA(ctx->ul_state.reserve(N * 16));
+    QF_CUDA(ctx->ul_aux.reserve(64 + DK * DK * 16));
+    int pos[13];
+    for (int i = 0; i < k; ++i) pos[i] = n - 1 - wires[i];
+    std::vector<double> buf(16 + DK * DK * 2, 0.0);
+    std::memcpy(buf.data(), pos, sizeof(int) * k);
+    double* um = buf.data() + 8;  // 64-byte header for the positions
+    if (k <= 4) {
+        std::memcpy(um, u, DK * DK * 16);
+    } else {
+        for (size_t i = 0; i < DK; ++i)  // column-major for the large-k kernel
+            for (size_t j = 0; j < DK; ++j) {
+                um[(j * DK + i) * 2] = u[(i * DK + j) * 2];
+                um[(j * DK + i) * 2 + 1] = u[(i * DK + j) * 2 + 1];
+            }
+    }
+    QF_CUDA(cudaMemcpyAsync(ctx->ul_aux.p, buf.data(), 64 + DK * DK * 16, cudaMemcpyHostToDevice, s));
+    QF_CUDA(cudaMemcpyAsync(ctx->ul_state.p, state, N * 16, cudaMemcpyHostToDevice, s));
+    const double2* dm = (const double2*)((const char*)ctx->ul_aux.p + 64);
+    QF_CUDA(launch_apply_unitary((double2*)ctx->ul_state.p, n, k, (const int*)ctx->ul_aux.p, dm, dm, s));
+    ctx->launches++;
+    QF_CUDA(cudaMemcpyAsync(state, ctx->ul_state.p, N * 16, cudaMemcpyDeviceToHost, s));
     QF_CUDA(cudaStreamSynchronize(s));
     return QF_OK;
 }

@@ -98,6 +98,11 @@ cudaError_t launch_sample(int prec, const void* psi, int n, int batch, const dou
 // on every state; m = [D][D] complex row-major, shared or one per state
 cudaError_t launch_apply_local(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                                cudaStream_t s);
+// k-wire operator on one complex128 state (apply_local_unitary): d_pos[k] = memory
+// bit positions (wires[0] first = most significant local bit), d_u = U row-major
+// (k <= 4), d_ut = U column-major (k >= 5, k <= 13)
+cudaError_t launch_apply_unitary(double2* psi, int n, int k, const int* d_pos, const double2* d_u, const double2* d_ut,
+                                 cudaStream_t s);
 // number of fixed-order rho partials per state of launch_apply_rho
 int local_rho_parts(int n);
 cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_t s);

@@ -377,7 +377,103 @@ __global__ void __launch_bounds__(128) kraus_pick_kernel(const double2* rho, int
     logp[b] += log(pp / acc) + log(acc);
 }
 
+// Generic k-wire operator on one complex128 state (apply_local_unitary,
+// reference circuit.cpp:147-175: wires[0] most significant local bit).
+// Small k: a thread per amplitude group, the 2^K amplitudes in registers, U in
+// shared memory.  pos[i] = memory bit position of wires[i].
+template <int K>
+__global__ void __launch_bounds__(256) apply_unitary_small_kernel(double2* psi, int n, const int* pos_g,
+                                                                  const double2* u) {
+    constexpr int DK = 1 << K;
+    __shared__ double2 su[DK * DK];
+    __shared__ int pos[K];
+    for (int i = threadIdx.x; i < DK * DK; i += blockDim.x) su[i] = u[i];
+    if (threadIdx.x < K) pos[threadIdx.x] = pos_g[threadIdx.x];
+    __syncthreads();
+    uint32_t mask = 0;
+    for (int i = 0; i < K; ++i) mask |= 1u << pos[i];
+    const uint32_t N = 1u << n, free = (N - 1) & ~mask, G = N >> K;
+    uint32_t off[DK];
+#pragma unroll
+    for (int j = 0; j < DK; ++j) {
+        uint32_t o = 0;
+        for (int i = 0; i < K; ++i)
+            if ((j >> (K - 1 - i)) & 1) o |= 1u << pos[i];
+        off[j] = o;
+    }
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        const uint32_t base = pdep32(g, free);
+        double2 a[DK];
+#pragma unroll
+        for (int j = 0; j < DK; ++j) a[j] = psi[base | off[j]];
+#pragma unroll
+        for (int i = 0; i < DK; ++i) {
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int j = 0; j < DK; ++j) {
+                const double2 c = su[i * DK + j];
+                re += c.x * a[j].x - c.y * a[j].y;
+                im += c.x * a[j].y + c.y * a[j].x;
+            }
+            psi[base | off[i]] = make_double2(re, im);
+        }
+    }
+}
+
+// Large k: a CTA per amplitude group, the group in shared memory, thread i ->
+// output rows i, i + T, ...; U column-major (ut[j * DK + i] = U[i][j]) so a
+// column read is coalesced across the rows.
+__global__ void __launch_bounds__(256) apply_unitary_large_kernel(double2* psi, int n, int k, const int* pos_g,
+                                                                  const double2* ut) {
+    extern __shared__ double2 grp[];
+    const uint32_t DK = 1u << k, N = 1u << n;
+    uint32_t mask = 0;
+    for (int i = 0; i < k; ++i) mask |= 1u << pos_g[i];
+    const uint32_t free = (N - 1) & ~mask, G = N >> k;
+    auto offset = [&](uint32_t j) {
+        uint32_t o = 0;
+        for (int i = 0; i < k; ++i)
+            if ((j >> (k - 1 - i)) & 1) o |= 1u << pos_g[i];
+        return o;
+    };
+    for (uint32_t g = blockIdx.x; g < G; g += gridDim.x) {
+        const uint32_t base = pdep32(g, free);
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < DK; j += blockDim.x) grp[j] = psi[base | offset(j)];
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < DK; i += blockDim.x) {
+            double re = 0.0, im = 0.0;
+            for (uint32_t j = 0; j < DK; ++j) {
+                const double2 c = ut[(size_t)j * DK + i], x = grp[j];
+                re += c.x * x.x - c.y * x.y;
+                im += c.x * x.y + c.y * x.x;
+            }
+            psi[base | offset(i)] = make_double2(re, im);
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_apply_unitary(double2* psi, int n, int k, const int* d_pos, const double2* d_u, const double2* d_ut,
+                                 cudaStream_t s) {
+    const uint32_t G = (1u << n) >> k;
+    const unsigned grid_small = std::max(1u, std::min<uint32_t>((G + 255) / 256, 2048));
+    switch (k) {
+        case 1: apply_unitary_small_kernel<1><<<grid_small, 256, 0, s>>>(psi, n, d_pos, d_u); break;
+        case 2: apply_unitary_small_kernel<2><<<grid_small, 256, 0, s>>>(psi, n, d_pos, d_u); break;
+        case 3: apply_unitary_small_kernel<3><<<grid_small, 256, 0, s>>>(psi, n, d_pos, d_u); break;
+        case 4: apply_unitary_small_kernel<4><<<grid_small, 256, 0, s>>>(psi, n, d_pos, d_u); break;
+        default: {
+            const size_t sm = ((size_t)1 << k) * sizeof(double2);
+            cudaError_t e = cudaFuncSetAttribute(apply_unitary_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sm);
+            if (e != cudaSuccess) return e;
+            apply_unitary_large_kernel<<<std::max(1u, std::min<uint32_t>(G, 4096)), 256, sm, s>>>(psi, n, k, d_pos, d_ut);
+        }
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_apply_rho(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                              double2* rho, cudaStream_t s) {

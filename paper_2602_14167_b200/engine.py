@@ -364,6 +364,16 @@ def mipt_haar(ctx: Context, n: int, depth: int, p: float, trajectories: int, see
     return out, int(cnt.value)
 
 
+def apply_unitary(ctx: Context, amps: np.ndarray, u, wires: Sequence[int]) -> np.ndarray:
+    """apply_local_unitary on a complex128 state (qf_apply_unitary): returns the new amplitudes."""
+    st = np.ascontiguousarray(np.asarray(amps, np.complex128)).copy()
+    n = int(st.size).bit_length() - 1
+    um = np.ascontiguousarray(np.asarray(u, np.complex128)).view(np.float64)
+    w = (ctypes.c_int * max(1, len(wires)))(*[int(x) for x in wires])
+    check(ctx.lib.qf_apply_unitary(ctx.handle, n, dptr(st.view(np.float64)), len(wires), w, dptr(um)))
+    return st
+
+
 def hermitian_eigvals(ctx: Context, a) -> np.ndarray:
     """Ascending eigenvalues of a batch of Hermitian matrices [batch, m, m] through the
     device tridiagonalisation + bisection kernels (qf_hermitian_eigvals)."""

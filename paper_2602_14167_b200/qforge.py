@@ -299,15 +299,9 @@ def apply_local_unitary(psi: StateVector, u: np.ndarray, wires: Sequence[int]) -
     _require(u.shape == (2 ** k, 2 ** k), "apply_local_unitary: wrong gate size")
     for w in wires:
         _require(0 <= w < psi.n, "apply_local_unitary: wire out of range")
-    _require(k in (1, 2), "apply_local_unitary: the device path supports 1- and 2-qubit gates")
-    c = Circuit(psi.n)
-    c.ops.append(GateInstruction(Gate.unitary, list(wires), [], u))
-    c.initial_state = psi.amps
-    ops, mats = _circuit_ops(c)
-    ctx = _eng.default_context()
-    prog = _eng.Program(ctx, psi.n, ops, 0, _precision, mats)
-    prog.set_initial_state(psi.amps)
-    psi.amps = _eng.run_state(ctx, prog, np.zeros(0), 64)
+    _require(len(set(wires)) == k, "apply_local_unitary: wires must be distinct")
+    _require(1 <= k <= 13, "apply_local_unitary: 1 to 13 wires on the device path")
+    psi.amps = _eng.apply_unitary(_eng.default_context(), psi.amps, u, list(wires))
 
 
 # ---------------------------------------------------------------- Pauli sums

@@ -230,6 +230,27 @@ def test_apply_local_unitary_and_rzz_lowering(ctx):
     assert psi.amps[0] == pytest.approx(math.cos(0.2)) and psi.amps[2] == pytest.approx(math.sin(0.2))
 
 
+@pytest.mark.parametrize("n,k", [(6, 1), (6, 2), (7, 3), (8, 4), (8, 5), (9, 7), (10, 10)])
+def test_apply_local_unitary_any_arity(ctx, n, k):
+    """apply_local_unitary (circuit.cpp:78-176) for every arity through the one-kernel
+    device path (k <= 4 registers, k >= 5 shared-memory groups): random unitary on
+    random distinct wires (wires[0] most significant) against numpy; C++ drop-in
+    shares the C-ABI entry."""
+    rng = np.random.default_rng(n * 31 + k)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    q, _ = np.linalg.qr(rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k)))
+    wires = [int(w) for w in rng.permutation(n)[:k]]
+    t = np.moveaxis(psi0.reshape([2] * n), wires, list(range(k)))
+    sh = t.shape
+    ref = np.moveaxis((q @ t.reshape(1 << k, -1)).reshape(sh), list(range(k)), wires).reshape(-1)
+    psi = qf.StateVector(n, 2, psi0.copy())
+    qf.apply_local_unitary(psi, q, wires)
+    assert np.abs(psi.amps - ref).max() < 1e-12
+    with pytest.raises(ValueError, match="distinct"):
+        qf.apply_local_unitary(qf.StateVector(n, 2, psi0.copy()), np.eye(4), [0, 0])
+
+
 def test_complex64_mode(ctx):
     qf.set_precision("c64")
     try:
