@@ -48,6 +48,12 @@ Geometry geometry(int prec, int n) {
 
 static int popc(uint64_t x) { return __builtin_popcountll(x); }
 
+// development A/B toggles: VAR=0 turns the feature off
+static bool env_flag_off(const char* name) {
+    const char* e = std::getenv(name);
+    return e && e[0] == '0';
+}
+
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
                                    uint64_t fixed_bits, int budget, int max_items) {
@@ -412,6 +418,26 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             for (size_t i = 0; i < free_bits.size(); ++i)
                 if (!used[i]) rest.push_back(free_bits[i]);
             std::sort(lanes.begin(), lanes.end());
+            // One shared-memory wavefront serves 2^W consecutive lanes (128 B of 8- or
+            // 16-byte amplitudes), so the first W lane slots must land in distinct bank
+            // groups: under the XOR-fold swizzle tile bit b moves bank group b mod W.
+            // Distinct residues go first; a repeated residue takes a higher lane bit,
+            // where it only selects the wavefront.  (Global coalescing does not care
+            // about lane order: the warp still covers the same sectors.)
+            if (!env_flag_off("QF_LANE_ORDER")) {
+                std::vector<int> first, later;
+                uint32_t seen = 0;
+                for (int l : lanes) {
+                    if ((int)first.size() < W && !(seen >> (l % W) & 1)) {
+                        seen |= 1u << (l % W);
+                        first.push_back(l);
+                    } else {
+                        later.push_back(l);
+                    }
+                }
+                lanes = first;
+                lanes.insert(lanes.end(), later.begin(), later.end());
+            }
             int ti = 0;
             for (int l : lanes) dp.thr_tl[ti++] = (int8_t)l;
             for (int l : rest) dp.thr_tl[ti++] = (int8_t)l;
