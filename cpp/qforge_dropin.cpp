@@ -855,6 +855,15 @@ std::uint64_t template_key(const Template& t, int n_params) {
     return f.h;
 }
 
+// The builder cannot be mapped to one fixed template: energies then take the
+// per-parameter-set path (per_theta_energies), the adjoint gradient rethrows.
+struct TemplateUnavailable : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+void require_template(bool cond, const char* msg) {
+    if (!cond) throw TemplateUnavailable(msg);
+}
+
 // Parameter-slot discovery: probe the opaque builder.  The
 // builder is probed on every call and the compiled program is reused only
 // while the discovered template (ops, slots, matrices, initial state) and
@@ -877,8 +886,8 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
         bool same = c->n == c0.n && c->ops.size() == c0.ops.size();
         for (size_t i = 0; same && i < c0.ops.size(); ++i)
             same = c->ops[i].name == c0.ops[i].name && c->ops[i].wires == c0.ops[i].wires;
-        require(same, "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)");
-        require(same_init(c->initial_state, c0.initial_state),
+        require_template(same, "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)");
+        require_template(same_init(c->initial_state, c0.initial_state),
                 "AnsatzSpec: theta feeds the initial state (not supported on the device path)");
     }
     std::vector<SlotMap> slots(c0.ops.size());
@@ -886,7 +895,7 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
         const GateInstruction& op = c0.ops[i];
         if (!is_rotation(op.name)) {
             for (const Circuit* c : {&ca, &cb, &cc})
-                require(c->ops[i].params == op.params && same_matrix(c->ops[i].matrix, op.matrix),
+                require_template(c->ops[i].params == op.params && same_matrix(c->ops[i].matrix, op.matrix),
                         "AnsatzSpec: theta feeds a gate without a Pauli generator "
                         "(su4/unitary parameters are not supported on the device path)");
             continue;
@@ -894,10 +903,10 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
         const double o = op.params.at(0);
         const double da = ca.ops[i].params.at(0) - o, db = cb.ops[i].params.at(0) - o;
         if (da == 0.0 && db == 0.0) {
-            require(cc.ops[i].params.at(0) == o, "AnsatzSpec: builder is not affine in theta");
+            require_template(cc.ops[i].params.at(0) == o, "AnsatzSpec: builder is not affine in theta");
             continue;
         }
-        require(da != 0.0 && P > 0, "AnsatzSpec: builder is not affine in theta");
+        require_template(da != 0.0 && P > 0, "AnsatzSpec: builder is not affine in theta");
         int s = 0;
         double best = INFINITY;
         for (int j = 0; j < P; ++j) {
@@ -909,7 +918,7 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
         }
         const double coef = da / ta[s];
         const double pred = coef * tc[s] + o;
-        require(std::abs(pred - cc.ops[i].params.at(0)) <= 1e-9 * std::max(1.0, std::abs(pred)),
+        require_template(std::abs(pred - cc.ops[i].params.at(0)) <= 1e-9 * std::max(1.0, std::abs(pred)),
                 "AnsatzSpec: builder is not affine in a single theta slot");
         slots[i] = {s, coef, o};
     }
@@ -929,9 +938,40 @@ std::shared_ptr<ProgramHandle> ansatz_program(const AnsatzSpec& a) {
     return prog;
 }
 
+// The reference's own energy path (variational.cpp:38-52: build, run,
+// expectation) for builders without a fixed template, one parameter set at a
+// time, on the device: each circuit is a constant program whose generated
+// kernels do not depend on angle values (they come from the kernel cache).
+void per_theta_energies(const AnsatzSpec& a, const std::vector<double>& flat, int batch, const PauliSum* h,
+                        const SparseCOO* hs, std::vector<double>& E) {
+    const int P = a.n_params;
+    E.assign(batch, 0.0);
+    for (int b = 0; b < batch; ++b) {
+        RealVector th(P);
+        for (int j = 0; j < P; ++j) th[j] = flat[(size_t)b * P + j];
+        const Circuit c = a.builder(th);
+        auto prog = make_program(circuit_template(c, nullptr), 0);
+        const double none = 0.0;
+        if (h) {
+            require(h->n == c.n, "expectation_pauli: size mismatch");
+            check(qf_energy_grad_batch(ctx(), prog->p, observable(*h), 1, &none, &E[b], nullptr));
+        } else {
+            check(qf_sparse_energy(ctx(), prog->p, 1, &none, hs->dim, (std::int64_t)hs->nnz(), hs->rows.data(),
+                                   hs->cols.data(), reinterpret_cast<const double*>(hs->vals.data()), 0, &E[b]));
+        }
+    }
+}
+
 void batch_eval(const AnsatzSpec& a, const std::vector<double>& flat, int batch, const PauliSum& h,
                 std::vector<double>& E, std::vector<double>* G) {
-    auto prog = ansatz_program(a);
+    std::shared_ptr<ProgramHandle> prog;
+    try {
+        prog = ansatz_program(a);
+    } catch (const TemplateUnavailable&) {
+        if (G) throw;  // the adjoint gradient needs the template
+        per_theta_energies(a, flat, batch, &h, nullptr, E);
+        return;
+    }
     E.assign(batch, 0.0);
     if (G) G->assign((size_t)batch * a.n_params, 0.0);
     if (batch == 0) return;
@@ -951,7 +991,14 @@ double energy(const AnsatzSpec& ansatz, const RealVector& theta, const PauliSum&
 double energy(const AnsatzSpec& ansatz, const RealVector& theta, const SparseCOO& h) {  // variational.cpp:45-52
     ansatz.validate();
     require(theta.size() == ansatz.n_params, "energy: parameter count mismatch");
-    auto prog = ansatz_program(ansatz);
+    std::shared_ptr<ProgramHandle> prog;
+    try {
+        prog = ansatz_program(ansatz);
+    } catch (const TemplateUnavailable&) {
+        std::vector<double> flat(theta.data(), theta.data() + theta.size()), Es;
+        per_theta_energies(ansatz, flat, 1, nullptr, &h, Es);
+        return Es[0];
+    }
     double E = 0.0;
     check(qf_sparse_energy(ctx(), prog->p, 1, theta.data(), h.dim, (std::int64_t)h.nnz(), h.rows.data(),
                            h.cols.data(), reinterpret_cast<const double*>(h.vals.data()), 0, &E));
@@ -1041,7 +1088,36 @@ VqeResult vqe_run(const AnsatzSpec& ansatz, const std::vector<RealVector>& theta
         require(theta0_batch[b].size() == P, "gradient: parameter count mismatch");
         std::memcpy(flat.data() + (size_t)b * P, theta0_batch[b].data(), sizeof(double) * P);
     }
-    auto prog = ansatz_program(ansatz);
+    std::shared_ptr<ProgramHandle> prog;
+    try {
+        prog = ansatz_program(ansatz);
+    } catch (const TemplateUnavailable&) {
+        if (grad_mode == GradMode::adjoint) throw;
+        // no fixed template: the reference's loop (variational.cpp:118-141) over
+        // the per-parameter-set energy path
+        VqeResult out;
+        out.traces.assign(B, {});
+        out.final_thetas.assign(B, RealVector(P));
+        for (int b = 0; b < B; ++b) {
+            RealVector theta = theta0_batch[b];
+            AdamState adam;
+            for (int st = 0; st < steps; ++st) {
+                out.traces[b].push_back(energy(ansatz, theta, h));
+                adam_step(adam, theta, gradient(ansatz, theta, h, grad_mode, 1e-5, 1), lr);
+            }
+            out.final_thetas[b] = theta;
+        }
+        out.best_energy = INFINITY;
+        for (int b = 0; b < B; ++b) {
+            const double e = energy(ansatz, out.final_thetas[b], h);
+            out.traces[b].push_back(e);
+            if (e < out.best_energy) {
+                out.best_energy = e;
+                out.best_index = b;
+            }
+        }
+        return out;
+    }
     // theta, the Adam moments and the traces stay on the device for all steps
     // (one native call; the batch advances in lock step, one host copy at the end)
     std::vector<double> tr((size_t)B * (steps + 1)), fin((size_t)B * P);

@@ -248,6 +248,32 @@ int main() {
         z.add(1.0, {3});
         CHECK(approx(expectation_pauli(psi, z).real(), 1.0, 1e-12));
     });
+    test_case("builder without a fixed template (per-theta path)", [] {
+        // structure depends on theta: energies and shift gradients still evaluate
+        // (per parameter set, on the device); the adjoint gradient needs the template
+        AnsatzSpec a;
+        a.n_params = 2;
+        a.shift_eligible = {true, true};
+        a.builder = [](const RealVector& th) {
+            Circuit c(2);
+            c.ry(0, th[0]);
+            if (th[0] > 0) c.rx(1, th[1]);
+            else c.ry(1, th[1]);
+            c.cx(0, 1);
+            return c;
+        };
+        PauliSum zz;
+        zz.n = 2;
+        zz.add(1.0, {3, 3});
+        RealVector t = RealVector::Zero(2);
+        t[0] = 0.4;
+        t[1] = -0.3;
+        // ry(0.4) x rx(-0.3) then cx: <Z0 Z1> = <Z1> before cx = cos(-0.3)
+        CHECK(approx(energy(a, t, zz), std::cos(-0.3), 1e-12));
+        RealVector g = gradient(a, t, zz, GradMode::parameter_shift);
+        CHECK(approx(g[0], 0.0, 1e-12) && approx(g[1], -std::sin(-0.3), 1e-12));
+        CHECK_THROWS(gradient(a, t, zz, GradMode::adjoint));
+    });
     test_case("apply_local_unitary on three wires", [] {  // circuit.cpp:147-175 (generic k)
         // X (x) X (x) X on wires {2, 0, 1} maps |000> to |111>; a permutation
         // unitary on wires {0, 2, 1} checks the local-bit order (wires[0] most significant)

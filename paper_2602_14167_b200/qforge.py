@@ -517,6 +517,17 @@ class AnsatzSpec:  # variational.hpp:14-21
         return per_ctx[key]
 
 
+class TemplateUnavailable(ValueError):
+    """The builder cannot be mapped to one fixed template (structure or initial
+    state depends on theta, non-affine angles, theta feeding su4/unitary): the
+    energy-only paths then evaluate it per parameter set (_per_theta_energies)."""
+
+
+def _require_template(cond: bool, msg: str) -> None:
+    if not cond:
+        raise TemplateUnavailable(msg)
+
+
 def _probe(builder, P: int, values: np.ndarray) -> Circuit:
     return builder(values.copy())
 
@@ -536,16 +547,20 @@ def ansatz_template(a: AnsatzSpec):
     tc = np.cos(3.7 * j + 0.3) * 2.1 + 0.05
     c0, ca, cb, cc = (_probe(a.builder, P, t) for t in (t0, ta, tb, tc))
     for c in (ca, cb, cc):
-        _require(len(c.ops) == len(c0.ops) and c.n == c0.n and
+        _require_template(len(c.ops) == len(c0.ops) and c.n == c0.n and
                  all(x.name == y.name and x.wires == y.wires for x, y in zip(c.ops, c0.ops)),
                  "AnsatzSpec: builder structure depends on theta (device path needs a fixed structure)")
+        _require_template((c.initial_state is None) == (c0.initial_state is None) and
+                          (c.initial_state is None or np.array_equal(np.asarray(c.initial_state),
+                                                                     np.asarray(c0.initial_state))),
+                          "AnsatzSpec: theta feeds the initial state (not supported on the device path)")
     _check_qubits(c0)
     slot_of = []
     ratios = tb / ta if P else np.zeros(0)
     for i, op in enumerate(c0.ops):
         if Gate(op.name) not in (Gate.rx, Gate.ry, Gate.rz, Gate.rzz):
             for c in (ca, cb, cc):
-                _require(np.array_equal(np.asarray(c.ops[i].params, dtype=float), np.asarray(op.params, dtype=float)) and
+                _require_template(np.array_equal(np.asarray(c.ops[i].params, dtype=float), np.asarray(op.params, dtype=float)) and
                          (op.matrix is None or np.array_equal(c.ops[i].matrix, op.matrix)),
                          "AnsatzSpec: theta feeds a gate without a Pauli generator "
                          "(su4/unitary parameters are not supported on the device path)")
@@ -555,14 +570,14 @@ def ansatz_template(a: AnsatzSpec):
         da = float(ca.ops[i].params[0]) - o
         db = float(cb.ops[i].params[0]) - o
         if da == 0.0 and db == 0.0:
-            _require(float(cc.ops[i].params[0]) == o, "AnsatzSpec: builder is not affine in theta")
+            _require_template(float(cc.ops[i].params[0]) == o, "AnsatzSpec: builder is not affine in theta")
             slot_of.append(None)
             continue
-        _require(da != 0.0 and P > 0, "AnsatzSpec: builder is not affine in theta")
+        _require_template(da != 0.0 and P > 0, "AnsatzSpec: builder is not affine in theta")
         s = int(np.argmin(np.abs(ratios - db / da)))
         coef = da / ta[s]
         pred = coef * tc[s] + o
-        _require(abs(pred - float(cc.ops[i].params[0])) <= 1e-9 * max(1.0, abs(pred)),
+        _require_template(abs(pred - float(cc.ops[i].params[0])) <= 1e-9 * max(1.0, abs(pred)),
                  "AnsatzSpec: builder is not affine in a single theta slot")
         slot_of.append((s, coef, o))
     ops, mats = _circuit_ops(c0, slot_of)
@@ -619,9 +634,34 @@ def hea_ansatz(n: int, layers: int) -> AnsatzSpec:
     return AnsatzSpec(P, builder, [True] * P)
 
 
+def _per_theta_energies(ansatz: AnsatzSpec, th: np.ndarray, h, precision: Optional[str] = None) -> np.ndarray:
+    """The reference's own energy path (variational.cpp:38-52: build, run,
+    expectation) for builders without a fixed template, one parameter set at a
+    time, on the device: each circuit becomes a constant program (the generated
+    kernels do not depend on angle values, so they come from the kernel cache)."""
+    ctx = _eng.default_context()
+    precision = precision or _precision
+    E = np.zeros(th.shape[0])
+    for b in range(th.shape[0]):
+        c = ansatz.builder(th[b].copy())
+        _check_qubits(c)
+        ops, mats = _circuit_ops(c)
+        prog = _eng.Program(ctx, c.n, ops, 0, precision, mats)
+        if c.initial_state is not None:
+            prog.set_initial_state(c.initial_state)
+        if isinstance(h, SparseCOO):
+            E[b] = _eng.sparse_energy(ctx, prog, np.zeros((1, 0)), h.dim, h.rows, h.cols, h.vals)[0]
+        else:
+            _require(h.n == c.n, "expectation_pauli: size mismatch")
+            E[b] = _eng.energy_grad_batch(ctx, prog, h.observable(ctx), np.zeros((1, 0)), False)[0][0]
+    return E
+
+
 def energy_gradient_batch(ansatz: AnsatzSpec, thetas, h: PauliSum, grads: bool = True,
                           precision: Optional[str] = None):
-    """Batched energy + adjoint gradient: (E[B], G[B, P])."""
+    """Batched energy + adjoint gradient: (E[B], G[B, P]).  Energies of builders
+    without a fixed template fall back to per-parameter-set evaluation; the
+    adjoint gradient needs the template and raises its error."""
     ansatz.validate()
     th = np.asarray(thetas, dtype=np.float64)
     if ansatz.n_params == 0:
@@ -629,7 +669,12 @@ def energy_gradient_batch(ansatz: AnsatzSpec, thetas, h: PauliSum, grads: bool =
     else:
         th = th.reshape(-1, ansatz.n_params)
     ctx = _eng.default_context()
-    prog = ansatz.program(precision, ctx)
+    try:
+        prog = ansatz.program(precision, ctx)
+    except TemplateUnavailable:
+        if grads:
+            raise
+        return _per_theta_energies(ansatz, th, h, precision), None
     _require(h.n == prog.n, "expectation_pauli: size mismatch")
     return _eng.energy_grad_batch(ctx, prog, h.observable(ctx), th, grads)
 
@@ -640,7 +685,11 @@ def energy(ansatz: AnsatzSpec, theta, h) -> float:  # variational.cpp:38-43 (Pau
     _require(theta.size == ansatz.n_params, "energy: parameter count mismatch")
     if isinstance(h, SparseCOO):
         ctx = _eng.default_context()
-        E = _eng.sparse_energy(ctx, ansatz.program(None, ctx), theta[None, :], h.dim, h.rows, h.cols, h.vals)
+        try:
+            prog = ansatz.program(None, ctx)
+        except TemplateUnavailable:
+            return float(_per_theta_energies(ansatz, theta[None, :], h)[0])
+        E = _eng.sparse_energy(ctx, prog, theta[None, :], h.dim, h.rows, h.cols, h.vals)
         return float(E[0])
     E, _ = energy_gradient_batch(ansatz, theta[None, :], h, grads=False)
     return float(E[0])
@@ -714,7 +763,36 @@ def vqe_run(ansatz: AnsatzSpec, theta0_batch, h: PauliSum, steps: int, lr: float
     theta, Adam m/v stay resident; one batched energy+gradient per step."""
     from .vqe import vqe_run_device
 
+    try:
+        ansatz.program(None, _eng.default_context())
+    except TemplateUnavailable:
+        if grad_mode == GradMode.adjoint:
+            raise
+        return _vqe_run_per_theta(ansatz, theta0_batch, h, steps, lr, grad_mode)
     return vqe_run_device(ansatz, theta0_batch, h, steps, lr, grad_mode)
+
+
+def _vqe_run_per_theta(ansatz, theta0_batch, h, steps, lr, grad_mode) -> VqeResult:
+    """variational.cpp:103-143 step for step (trace energy, gradient, Adam per
+    seed) for builders without a fixed template; energies on the device."""
+    _require(len(theta0_batch) > 0, "vqe_run: empty batch")
+    _require(steps >= 1, "vqe_run: steps must be >= 1")
+    traces, finals = [], []
+    for th0 in theta0_batch:
+        th = np.asarray(th0, dtype=np.float64).copy()
+        st = AdamState()
+        tr = []
+        for _ in range(steps):
+            tr.append(energy(ansatz, th, h))
+            adam_step(st, th, gradient(ansatz, th, h, grad_mode), lr)
+        tr.append(energy(ansatz, th, h))
+        traces.append(tr)
+        finals.append(th)
+    res = VqeResult(traces, finals)
+    for i, tr in enumerate(traces):
+        if res.best_index < 0 or tr[-1] < res.best_energy:
+            res.best_energy, res.best_index = tr[-1], i
+    return res
 
 
 # ---------------------------------------------------------------- noise (noise.hpp / noise.cpp)

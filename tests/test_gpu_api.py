@@ -437,3 +437,52 @@ def test_device_entry_shards_with_communicator(ctx):
         torch.cuda.synchronize()
         assert np.array_equal(E_d.cpu().numpy(), Eh) and np.array_equal(G_d.cpu().numpy(), Gh)
     c2.set_comm(0, 1, None)
+
+
+def test_builder_without_fixed_template_per_theta_path(ctx):
+    """builders the slot probe cannot map -- structure that
+    depends on theta, angles not affine in theta -- still evaluate, one parameter
+    set at a time on the device (the reference's build -> run -> expectation):
+    energies, parameter-shift gradients and a short vqe_run equal the oracle run
+    of every built circuit; the adjoint gradient (needs the template) raises."""
+    n = 6
+
+    def b_struct(th):  # an extra gate when theta[0] > 0
+        c = qf.Circuit(n)
+        for q in range(n):
+            c.ry(q, th[q])
+        if th[0] > 0:
+            c.rx(1, th[1])
+        for q in range(n - 1):
+            c.cx(q, q + 1)
+        c.rz(2, th[2])
+        return c
+
+    def b_square(th):  # not affine: angle = theta^2 + 0.1
+        c = qf.Circuit(n)
+        for q in range(n):
+            c.ry(q, th[q] * th[q] + 0.1)
+        for q in range(n - 1):
+            c.cx(q, q + 1)
+        return c
+
+    h, ho = chain(n, 0.8), po.tfim(n, 0.8)
+
+    def oracle_energy(builder, th):
+        c = builder(np.asarray(th, float).copy())
+        ops, mats = qf._circuit_ops(c)
+        return po.expectation(n, po.run(n, ops, mats=mats), ho).real
+
+    for builder in (b_struct, b_square):
+        a = qf.AnsatzSpec(n, builder, [True] * n)
+        for th in (np.linspace(-0.9, 1.1, n), np.linspace(0.7, -1.3, n)):
+            assert qf.energy(a, th, h) == pytest.approx(oracle_energy(builder, th), abs=1e-11)
+            g = qf.gradient(a, th, h, qf.GradMode.parameter_shift)
+            ref = [(oracle_energy(builder, th + np.pi / 2 * np.eye(n)[j]) -
+                    oracle_energy(builder, th - np.pi / 2 * np.eye(n)[j])) / 2 for j in range(n)]
+            assert np.abs(g - ref).max() < 1e-11
+            with pytest.raises(ValueError, match="AnsatzSpec"):
+                qf.gradient(a, th, h, qf.GradMode.adjoint)
+        r = qf.vqe_run(a, [np.linspace(-0.5, 0.5, n)], h, 2, 0.05, qf.GradMode.finite_diff)
+        assert len(r.traces[0]) == 3 and r.best_index == 0
+        assert r.traces[0][-1] == pytest.approx(oracle_energy(builder, r.final_thetas[0]), abs=1e-11)
