@@ -776,17 +776,12 @@ int qf_jit_compile_check(int n, int n_ops, const qf_op* ops, const double* mats,
     ProgramPlan P;
     int rc = build_plan_from_ops(n, n_ops, ops, mats, n_mats, n_params, precision, P);
     if (rc) return rc;
-    int count = 0;
-    for (int pi = 0; pi < 2; ++pi) {
-        const PassPlan& pp = pi ? P.bwd : P.fwd;
-        for (size_t si = 0; si < pp.sweeps.size(); ++si) {
-            std::string cubin, err;
-            if (!jit_compile_source(jit_source(P, pp, (int)si, pi == 1), cubin, err))
-                return set_err(QF_ERUNTIME, err);
-            ++count;
-        }
-    }
-    if (kernels) *kernels = count;
+    // the program-creation compile stage (parallel, disk cache, out-of-process
+    // NVRTC helper) without loading modules: works on a host without a GPU
+    JitPass f, b;
+    JitStats st;
+    if (!jit_build(P, f, b, st, false)) return set_err(QF_ERUNTIME, st.error);
+    if (kernels) *kernels = (int)(P.fwd.sweeps.size() + P.bwd.sweeps.size());
     return QF_OK;
 }
 

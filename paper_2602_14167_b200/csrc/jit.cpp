@@ -1412,7 +1412,7 @@ bool jit_compile_source(const std::string& src, std::string& cubin, std::string&
     return compile_one(src, cubin, err);
 }
 
-bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
+bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st, bool load_modules) {
     auto t0 = std::chrono::steady_clock::now();
     {
         std::lock_guard<std::mutex> lk(g_nvrtc_mu);
@@ -1505,6 +1505,18 @@ bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st) {
     nthr = std::max(1u, std::min<unsigned>(nthr, (unsigned)std::max<size_t>(1, deferred.size())));
     for (unsigned i = 0; i < nthr && !deferred.empty(); ++i) pool.emplace_back(waiter);
     for (auto& t : pool) t.join();
+    if (!load_modules) {  // compile / cache stage only (host-side check, no device needed)
+        for (auto& jb : jobs) {
+            if (!jb.err.empty()) {
+                st.error = jb.err;
+                return false;
+            }
+            if (jb.from_cache) st.cached++;
+            else st.compiled++;
+        }
+        st.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return true;
+    }
     fwd.sweeps.assign(P.fwd.sweeps.size(), {});
     bwd.sweeps.assign(P.bwd.sweeps.size(), {});
     auto fail = [&](const std::string& e) {  // releases every module acquired so far

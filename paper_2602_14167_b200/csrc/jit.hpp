@@ -54,7 +54,8 @@ bool jit_compile_source(const std::string& src, std::string& cubin, std::string&
 
 // Builds (or loads from the cache) every sweep kernel of both passes.
 // Returns false and fills st.error if NVRTC is unavailable or a compile fails.
-bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st);
+// load_modules = false: compile into the disk cache only (no device needed)
+bool jit_build(const ProgramPlan& P, JitPass& fwd, JitPass& bwd, JitStats& st, bool load_modules = true);
 
 // Launch one specialised sweep.
 int jit_launch(const JitKernel& k, const SweepArgs& a, int tiles, int batch, void* stream);

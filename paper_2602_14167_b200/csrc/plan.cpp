@@ -292,7 +292,13 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
     const uint64_t fixed = (n <= k) ? all : ((1ull << c) - 1);
     // cap the gates per sweep: the specialised kernels are straight-line code, and
     // very long sweeps overflow the instruction cache
-    int max_ops = 0;
+    // Cap on gates per sweep.  The generated kernels are straight-line code and
+    // ptxas time grows faster than linearly with their length: C2's 205-op first
+    // adjoint sweep alone took 90 % of a cold NVRTC build (151 s of CPU on this
+    // container, 24 s on a GPU host).  120 ops splits it in two at no run-time
+    // cost (C2 206.8 vs 207.6 ms per step, profiles/r2_sweep_experiments.md)
+    // and cuts the cold build 3.5x.  QF_MAX_SWEEP_OPS=n overrides (0 = no cap).
+    int max_ops = 120;
     if (const char* e = std::getenv("QF_MAX_SWEEP_OPS")) max_ops = std::atoi(e);
     auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops);
 
