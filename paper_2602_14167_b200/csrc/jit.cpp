@@ -50,14 +50,6 @@ struct Out {
     }
 };
 
-uint32_t swz_host(uint32_t p, int W) {
-    uint32_t x = p >> W, f = 0;
-    for (int i = 0; i < 4; ++i) {
-        f ^= x;
-        x >>= W;
-    }
-    return p ^ (f & ((1u << W) - 1));
-}
 
 // Runtime or static value of memory bit `pos` for register index l in a phase.
 struct BitSrc {
@@ -94,6 +86,71 @@ std::string cond_expr(const Cond& c) {
     if (c.bm) e = e.empty() ? one("tile_base", c.bm) : "(" + e + " ^ " + one("tile_base", c.bm) + ")";
     if (e.empty()) return "0u";
     return "(" + e + " & 1u)";
+}
+
+// Per-sweep shared-memory swizzle: a linear map over GF(2) that fixes the low W
+// bits of a tile index and adds to them, for each tile bit b >= W, a nonzero
+// W-bit vector low[b] (the XOR-fold default is 1 << (b mod W)).  One wavefront
+// serves the first W lane bits, so an exchange is bank-conflict free when those
+// lanes' images are linearly independent in the low W bits; the default fails
+// that for phases whose free tile bits miss a residue class mod W.  A
+// hill-climb over low[] makes every phase of the sweep independent where it can
+// (the default is kept when it already is, so such kernels are unchanged).
+std::vector<uint32_t> sweep_swizzle(const PassPlan& pass, const DevSweep& sw, int W, bool search) {
+    const int k = sw.k, R = sw.R, nl = std::min(W, k - R);
+    std::vector<uint32_t> low(k, 0);
+    for (int b = W; b < k; ++b) low[b] = 1u << (b % W);
+    auto rank_ok = [&](const DevPhase& ph) {
+        uint32_t rows[8];
+        for (int j = 0; j < nl; ++j) {
+            const int b = ph.thr_tl[j];
+            rows[j] = b < W ? (1u << b) : low[b];
+        }
+        int rank = 0;
+        for (int bit = 0; bit < W && rank < nl; ++bit) {
+            int piv = -1;
+            for (int j = rank; j < nl; ++j)
+                if (rows[j] >> bit & 1) {
+                    piv = j;
+                    break;
+                }
+            if (piv < 0) continue;
+            std::swap(rows[piv], rows[rank]);
+            for (int j = 0; j < nl; ++j)
+                if (j != rank && (rows[j] >> bit & 1)) rows[j] ^= rows[rank];
+            ++rank;
+        }
+        return rank == nl;
+    };
+    auto bad = [&] {
+        int c = 0;
+        for (int f = 0; f < sw.n_phases; ++f) c += !rank_ok(pass.phases[sw.phase_begin + f]);
+        return c;
+    };
+    int cur = bad();
+    if (search && nl == W && cur > 0) {
+        for (int round = 0; round < 8 && cur > 0; ++round) {
+            bool improved = false;
+            for (int b = W; b < k && cur > 0; ++b) {
+                const uint32_t keep = low[b];
+                uint32_t best_v = keep;
+                for (uint32_t v = 1; v < (1u << W); ++v) {
+                    low[b] = v;
+                    const int c = bad();
+                    if (c < cur) {
+                        cur = c;
+                        best_v = v;
+                        improved = true;
+                    }
+                }
+                low[b] = best_v;
+            }
+            if (!improved) break;
+        }
+    }
+    std::vector<uint32_t> img(k);
+    for (int b = 0; b < k; ++b) img[b] = (1u << b) | (b < W ? 0u : low[b]);
+    return img;
 }
 
 // Development toggle (QF_CARVEOUT=1): all of L1 as shared memory.  Measured
@@ -174,6 +231,14 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         return !(e && e[0] == '0');
     }();
     const bool pipe = jit_pipe_mode(pass, si);
+    // the sweep's shared-memory swizzle (the pipelined variant keeps the fold)
+    const std::vector<uint32_t> img = sweep_swizzle(pass, sw, W, !pipe && !env_flag("QF_JIT_FOLDSWZ"));
+    auto smap = [&](uint32_t p) {
+        uint32_t r = 0;
+        for (int b = 0; b < k; ++b)
+            if (p >> b & 1) r ^= img[b];
+        return r;
+    };
     Out o;
     if (pipe) o.s += "// qf-option: pipelined\n";
     if (env_flag("QF_JIT_NOPACK")) o.s += "#define QF_NOPACK 1\n";
@@ -343,15 +408,21 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
     // lists its factor indices), behind the same barrier as the matrices.
     const size_t stab_pos = o.s.size();
     if (!pipe) o("  }");
+    // swizzled tile index of (tid, register j) in the load / read-out mapping
+    auto emit_s_ld = [&] {
+        o("  uint32_t s_ld = 0;");
+        for (int j = 0; j < k - R; ++j) o("  s_ld ^= (0u - ((tid >> %d) & 1u)) & %uu;", j, smap(1u << j));
+    };
     if (!direct_first && !pipe) {
+        emit_s_ld();
         for (int j = 0; j < NR; ++j) {
+            const unsigned c = smap((unsigned)(T * j));
             if (ilv)
-                o("  tq[swz<%d>(tid + %uu)] = make_float4(v%d.x, v%d.y, w%d.x, w%d.y);", W, (unsigned)(T * j), j, j, j, j);
+                o("  tq[s_ld ^ %uu] = make_float4(v%d.x, v%d.y, w%d.x, w%d.y);", c, j, j, j, j);
             else if (bwd)
-                o("  tile[swz<%d>(tid + %uu)] = v%d; tile2[swz<%d>(tid + %uu)] = w%d;", W, (unsigned)(T * j), j, W,
-                  (unsigned)(T * j), j);
+                o("  tile[s_ld ^ %uu] = v%d; tile2[s_ld ^ %uu] = w%d;", c, j, c, j);
             else
-                o("  tile[swz<%d>(tid + %uu)] = v%d;", W, (unsigned)(T * j), j);
+                o("  tile[s_ld ^ %uu] = v%d;", c, j);
         }
     }
     if (!pipe) o("  __syncthreads();");
@@ -407,12 +478,12 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         if (!dfirst || !dlast) {
             o("    uint32_t s_t = 0;");
             for (int j = 0; j < k - R; ++j)
-                o("    s_t ^= (0u - ((tid >> %d) & 1u)) & %uu;", j, swz_host(1u << ph.thr_tl[j], W));
+                o("    s_t ^= (0u - ((tid >> %d) & 1u)) & %uu;", j, smap(1u << ph.thr_tl[j]));
             for (int l = 0; l < NR; ++l) {
                 uint32_t off = 0;
                 for (int r = 0; r < R; ++r)
                     if ((l >> r) & 1) off |= 1u << ph.reg_tl[r];
-                offs[l] = swz_host(off, W);
+                offs[l] = smap(off);
             }
         }
         if (!dfirst) {
@@ -975,7 +1046,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             if (!cond[r].any()) continue;
             const std::string c = cond_expr(cond[r]);
             gx += " ^ ((0u - " + c + ") & " + std::to_string(1u << sw.tb[(int)ph.reg_tl[r]]) + "u)";
-            sx += " ^ ((0u - " + c + ") & " + std::to_string(swz_host(1u << ph.reg_tl[r], W)) + "u)";
+            sx += " ^ ((0u - " + c + ") & " + std::to_string(smap(1u << ph.reg_tl[r])) + "u)";
         }
         if (dlast) {
             emit_gbase(ph, "g_pl");
@@ -1011,15 +1082,27 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
         }
     }
     if (!direct_last) {
-        for (int j = 0; j < NR; ++j) {
-            if (ilv)
-                o("  V v%d_o, w%d_o; { const float4 q_ = tq[swz<%d>(tid + %uu)]; v%d_o = make_float2(q_.x, q_.y); "
-                  "w%d_o = make_float2(q_.z, q_.w); }", j, j, W, (unsigned)(T * j), j, j);
-            else if (bwd)
-                o("  const V v%d_o = tile[swz<%d>(tid + %uu)]; const V w%d_o = tile2[swz<%d>(tid + %uu)];", j, W,
-                  (unsigned)(T * j), j, W, (unsigned)(T * j));
-            else
-                o("  const V v%d_o = tile[swz<%d>(tid + %uu)];", j, W, (unsigned)(T * j));
+        if (pipe) {
+            for (int j = 0; j < NR; ++j) {
+                if (bwd)
+                    o("  const V v%d_o = tile[swz<%d>(tid + %uu)]; const V w%d_o = tile2[swz<%d>(tid + %uu)];", j, W,
+                      (unsigned)(T * j), j, W, (unsigned)(T * j));
+                else
+                    o("  const V v%d_o = tile[swz<%d>(tid + %uu)];", j, W, (unsigned)(T * j));
+            }
+        } else {
+            o("  {");
+            emit_s_ld();
+            for (int j = 0; j < NR; ++j) {
+                const unsigned c = smap((unsigned)(T * j));
+                if (ilv)
+                    o("  V v%d_o, w%d_o; { const float4 q_ = tq[s_ld ^ %uu]; v%d_o = make_float2(q_.x, q_.y); "
+                      "w%d_o = make_float2(q_.z, q_.w); }", j, j, c, j, j);
+                else if (bwd)
+                    o("  const V v%d_o = tile[s_ld ^ %uu]; const V w%d_o = tile2[s_ld ^ %uu];", j, c, j, c);
+                else
+                    o("  const V v%d_o = tile[s_ld ^ %uu];", j, c);
+            }
         }
         for (int j = 0; j < NR; ++j) {
             if (bwd)
@@ -1027,6 +1110,7 @@ std::string jit_source(const ProgramPlan& P, const PassPlan& pass, int si, bool 
             else
                 o("  st[(size_t)g_ld + %uull] = v%d_o;", joff[j], j);
         }
+        if (!pipe) o("  }");
     }
     if (bwd && sw.n_taps % std::max(S, 1) != 0) {
         const int rem = sw.n_taps % S;
