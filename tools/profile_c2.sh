@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round profile of the C2 headline: bench line, ncu launch list of the same command,
-psi> at batch 1024.|psi> at batch 1024.
+# full captures of the first adjoint sweep (second evaluation: 24 sweeps per
+# evaluation, 10 forward, so launch 24 + 10 = 34) and of H|psi> at batch 1024.
 python bench.py --steps 3 --warmup 3 > gpurun_out/prof_bench.json 2> gpurun_out/prof_bench.err; echo BENCH $?
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/prof_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/prof_ncu_launch.log 2>&1; echo LAUNCH $?
