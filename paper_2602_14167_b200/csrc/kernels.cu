@@ -402,7 +402,8 @@ static cudaError_t dispatch_hpsi(const HArgs& a, int batch, cudaStream_t s) {
     // launch vs 216 with the dispatch); complex64: the jump-table dispatch with
     // immediate offsets (C4: 2.82 s vs 2.93 branch-free, 3.19 runtime offsets)
     constexpr bool SW = sizeof(RT) == 4;
-    if (TS == 2048) return launch_hpsi_t<RT, 16, 128, SW>(a, batch, 128, s);
+    static const bool na8 = std::getenv("QF_HPSI_NA8") && std::getenv("QF_HPSI_NA8")[0] == '1';  // development A/B
+    if (TS == 2048 && !na8) return launch_hpsi_t<RT, 16, 128, SW>(a, batch, 128, s);
     const int T = TS < 256 ? TS : 256;
     switch (TS / T) {
         case 1: return launch_hpsi_t<RT, 1, 256, SW>(a, batch, T, s);
