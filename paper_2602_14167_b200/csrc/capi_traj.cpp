@@ -639,6 +639,11 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
     struct Seg { int j0, j1; qf_program* prog; };
     std::vector<Seg> segs;
     size_t seg_mat = 16;
+    if (ctx->noise_progs.size() > 256) {  // bound the cache (between calls, never inside one)
+        QF_CUDA(cudaStreamSynchronize(s));
+        for (auto& kv : ctx->noise_progs) qf_program_destroy(kv.second);
+        ctx->noise_progs.clear();
+    }
     for (int j = 0; j < n_ops;) {
         if (op_chan_ptr[j + 1] > op_chan_ptr[j]) { ++j; continue; }
         int j1 = j;
