@@ -1395,6 +1395,17 @@ bool compile_one(const std::string& src, std::string& cubin, std::string& err) {
         std::ofstream(base + ".cu") << src;
     }
     std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DQF_JIT=1"};
+    // development: QF_JIT_OPTS = extra space-separated NVRTC options (A/B of compiler knobs)
+    static const std::vector<std::string> extra = [] {
+        std::vector<std::string> v;
+        if (const char* e = std::getenv("QF_JIT_OPTS")) {
+            std::istringstream is(e);
+            std::string t;
+            while (is >> t) v.push_back(t);
+        }
+        return v;
+    }();
+    for (const auto& x : extra) opts.push_back(x.c_str());
     nvrtcProgram prog = nullptr;
     if (g_nvrtc.create(&prog, src.c_str(), "qf_sweep.cu", 0, nullptr, nullptr) != 0) {
         err = "nvrtcCreateProgram failed";
