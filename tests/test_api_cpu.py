@@ -133,6 +133,25 @@ def test_slot_discovery_affine_maps_and_errors():
         qf.ansatz_template(qf.AnsatzSpec(1, structural, [True]))
     with pytest.raises(ValueError, match="eligibility tags"):
         qf.ansatz_template(qf.AnsatzSpec(2, builder, [True]))
+    # the template failures are TemplateUnavailable (the energy paths then evaluate
+    # per parameter set); spec validation errors are plain ValueErrors
+    for bad in (nonaffine, structural):
+        with pytest.raises(qf.TemplateUnavailable):
+            qf.ansatz_template(qf.AnsatzSpec(1, bad, [True]))
+
+    def init_feed(th):
+        c = qf.Circuit(1)
+        c.initial_state = np.array([math.cos(th[0]), math.sin(th[0])], complex)
+        return c.rx(0, 0.3)
+
+    with pytest.raises(qf.TemplateUnavailable, match="initial state"):
+        qf.ansatz_template(qf.AnsatzSpec(1, init_feed, [True]))
+    try:
+        qf.ansatz_template(qf.AnsatzSpec(2, builder, [True]))
+    except qf.TemplateUnavailable:
+        pytest.fail("a spec validation error must not select the per-theta path")
+    except ValueError:
+        pass
 
 
 def test_adam_step_mirror():
