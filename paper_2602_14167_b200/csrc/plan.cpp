@@ -56,33 +56,42 @@ static bool env_flag_off(const char* name) {
 
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items) {
+                                   uint64_t fixed_bits, int budget, int max_items, bool search) {
     const int n = (int)need.size();
-    std::vector<int> indeg(n, 0);
+    struct State {
+        std::set<int> ready;
+        std::vector<int> indeg;
+        int remaining = 0;
+    };
     std::vector<std::vector<int>> succ(n);
+    State st;
+    st.indeg.assign(n, 0);
     for (int j = 0; j < n; ++j) {
-        indeg[j] = (int)preds[j].size();
+        st.indeg[j] = (int)preds[j].size();
         for (int p : preds[j]) succ[p].push_back(j);
     }
-    std::set<int> ready;
     for (int j = 0; j < n; ++j)
-        if (indeg[j] == 0) ready.insert(j);
-    std::vector<Group> out;
-    int remaining = n;
-    while (remaining > 0) {
+        if (st.indeg[j] == 0) st.ready.insert(j);
+    st.remaining = n;
+    auto take = [&](State& S, Group& g, int it) {
+        S.ready.erase(it);
+        g.items.push_back(it);
+        --S.remaining;
+        for (int s : succ[it])
+            if (--S.indeg[s] == 0) S.ready.insert(s);
+    };
+    // greedy: absorb every ready item that fits, then widen the group's bits by the
+    // ready item that needs the fewest extra bits, until the budget is spent
+    auto greedy = [&](State& S) {
         Group g;
         g.bits = fixed_bits;
         for (;;) {
             bool progress = true;
             while (progress && (max_items <= 0 || (int)g.items.size() < max_items)) {
                 progress = false;
-                for (int it : ready) {
+                for (int it : S.ready) {
                     if ((need[it] & ~g.bits) == 0) {
-                        ready.erase(it);
-                        g.items.push_back(it);
-                        --remaining;
-                        for (int s : succ[it])
-                            if (--indeg[s] == 0) ready.insert(s);
+                        take(S, g, it);
                         progress = true;
                         break;
                     }
@@ -90,7 +99,7 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
             }
             int best = -1, best_cost = 1 << 30;
             if (max_items > 0 && (int)g.items.size() >= max_items) break;
-            for (int it : ready) {
+            for (int it : S.ready) {
                 int extra = popc(need[it] & ~g.bits);
                 if (popc(g.bits) + extra <= budget && extra < best_cost) {
                     best = it;
@@ -100,7 +109,72 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
             if (best < 0) break;
             g.bits |= need[best];
         }
+        return g;
+    };
+    // closure of fixed bits: every item reachable through items that fit
+    auto absorb = [&](State& S, uint64_t bits) {
+        Group g;
+        g.bits = bits;
+        bool progress = true;
+        while (progress) {
+            progress = false;
+            for (auto itr = S.ready.begin(); itr != S.ready.end();) {
+                const int it = *itr;
+                if ((need[it] & ~bits) == 0) {
+                    take(S, g, it);
+                    progress = true;
+                    itr = S.ready.lower_bound(it);
+                } else {
+                    ++itr;
+                }
+            }
+        }
+        return g;
+    };
+    uint64_t all_bits = fixed_bits;
+    for (uint64_t m : need) all_bits |= m;
+    const int nb = all_bits ? 64 - __builtin_clzll(all_bits) : 0;
+    const int win = budget - popc(fixed_bits);
+    std::vector<Group> out;
+    while (st.remaining > 0) {
+        State s_best = st;
+        Group g = greedy(s_best);
+        if (search && max_items <= 0 && win > 0) {
+            // window search: every run of `win` consecutive bits (above the fixed
+            // ones) is a candidate; the closure with the most items wins, ties keep
+            // the greedy group
+            auto consider = [&](uint64_t wbits) {
+                State s2 = st;
+                Group gw = absorb(s2, fixed_bits | wbits);
+                if (gw.items.size() > g.items.size()) {
+                    g = std::move(gw);
+                    s_best = std::move(s2);
+                }
+            };
+            const uint64_t freeb = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) & ~fixed_bits;
+            static const bool exhaustive = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == 'w');
+            if (exhaustive && popc(freeb) <= 14) {
+                // every win-subset of the free bits (C(13, 5) = 1287 at most here)
+                std::vector<int> fb;
+                for (int b = 0; b < nb; ++b)
+                    if (freeb >> b & 1) fb.push_back(b);
+                const int m = (int)fb.size();
+                for (uint32_t sel = 0; sel < (1u << m); ++sel) {
+                    if (__builtin_popcount(sel) != win) continue;
+                    uint64_t wbits = 0;
+                    for (int i = 0; i < m; ++i)
+                        if (sel >> i & 1) wbits |= 1ull << fb[i];
+                    consider(wbits);
+                }
+            } else {
+                for (int s0 = 0; s0 + win <= nb; ++s0) {
+                    const uint64_t wbits = (((win >= 64) ? ~0ull : ((1ull << win) - 1)) << s0);
+                    if (!(wbits & fixed_bits)) consider(wbits);
+                }
+            }
+        }
         if (g.items.empty()) return {};  // an item needs more bits than the budget
+        st = std::move(s_best);
         out.push_back(std::move(g));
     }
     return out;
@@ -339,7 +413,13 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
                 if (f != local.end()) lpreds[i].push_back(f->second);
             }
         }
-        auto phases = schedule_groups(lneed, lpreds, 0, R);
+        // phases: each one takes the register-bit set whose closure holds the most
+        // gates (every R-subset of the tile bits; the greedy choice wins ties):
+        // fewer phases means fewer shared-memory exchanges, C2 36 + 39 -> 30 + 36
+        // phases and 205.2 -> 198.0 ms per step.  QF_PHASE_SEARCH=0: greedy only,
+        // =w: windows of consecutive tile bits only (development A/B).
+        static const bool phase_search = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == '0');
+        auto phases = schedule_groups(lneed, lpreds, 0, R, 0, phase_search);
         // Inside a phase, issue ready non-diagonal gates first and release the
         // diagonal ones (which commute with each other) in batches: long runs of
         // diagonal gates and Z taps are fused by the kernel generator.

@@ -84,6 +84,6 @@ struct Group {
 };
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items = 0);
+                                   uint64_t fixed_bits, int budget, int max_items = 0, bool search = false);
 
 }  // namespace qfb
