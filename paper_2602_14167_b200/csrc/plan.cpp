@@ -56,7 +56,7 @@ static bool env_flag_off(const char* name) {
 
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items, bool search) {
+                                   uint64_t fixed_bits, int budget, int max_items, bool search, int lookahead) {
     const int n = (int)need.size();
     struct State {
         std::set<int> ready;
@@ -119,6 +119,7 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
         while (progress) {
             progress = false;
             for (auto itr = S.ready.begin(); itr != S.ready.end();) {
+                if (max_items > 0 && (int)g.items.size() >= max_items) return g;
                 const int it = *itr;
                 if ((need[it] & ~bits) == 0) {
                     take(S, g, it);
@@ -139,22 +140,16 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
     while (st.remaining > 0) {
         State s_best = st;
         Group g = greedy(s_best);
-        if (search && max_items <= 0 && win > 0) {
+        if (search && win > 0) {
             // window search: every run of `win` consecutive bits (above the fixed
             // ones) is a candidate; the closure with the most items wins, ties keep
             // the greedy group
-            auto consider = [&](uint64_t wbits) {
-                State s2 = st;
-                Group gw = absorb(s2, fixed_bits | wbits);
-                if (gw.items.size() > g.items.size()) {
-                    g = std::move(gw);
-                    s_best = std::move(s2);
-                }
-            };
+            // candidate bit sets: every win-subset of the free bits when there are few
+            // (C(13, 5) = 1287 at most for phases), else windows of consecutive bits
+            std::vector<uint64_t> cands;
             const uint64_t freeb = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) & ~fixed_bits;
             static const bool exhaustive = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == 'w');
             if (exhaustive && popc(freeb) <= 14) {
-                // every win-subset of the free bits (C(13, 5) = 1287 at most here)
                 std::vector<int> fb;
                 for (int b = 0; b < nb; ++b)
                     if (freeb >> b & 1) fb.push_back(b);
@@ -164,13 +159,48 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                     uint64_t wbits = 0;
                     for (int i = 0; i < m; ++i)
                         if (sel >> i & 1) wbits |= 1ull << fb[i];
-                    consider(wbits);
+                    cands.push_back(wbits);
                 }
             } else {
                 for (int s0 = 0; s0 + win <= nb; ++s0) {
                     const uint64_t wbits = (((win >= 64) ? ~0ull : ((1ull << win) - 1)) << s0);
-                    if (!(wbits & fixed_bits)) consider(wbits);
+                    if (!(wbits & fixed_bits)) cands.push_back(wbits);
                 }
+            }
+            std::vector<std::pair<int, uint64_t>> scored;  // (closure size, bits)
+            for (uint64_t wb : cands) {
+                State s2 = st;
+                scored.push_back({(int)absorb(s2, fixed_bits | wb).items.size(), wb});
+            }
+            if (lookahead > 0 && !scored.empty()) {
+                // two-level: among the best `lookahead` first choices, the one whose
+                // closure plus the best next closure covers the most items
+                std::stable_sort(scored.begin(), scored.end(),
+                                 [](const auto& a, const auto& b) { return a.first > b.first; });
+                int best_total = -1;
+                for (size_t c = 0; c < scored.size() && (int)c < lookahead; ++c) {
+                    State s2 = st;
+                    Group g1 = absorb(s2, fixed_bits | scored[c].second);
+                    int second = 0;
+                    if (s2.remaining > 0)
+                        for (uint64_t wb : cands) {
+                            State s3 = s2;
+                            second = std::max(second, (int)absorb(s3, fixed_bits | wb).items.size());
+                        }
+                    const int total = (int)g1.items.size() + second;
+                    if (total > best_total && g1.items.size() >= g.items.size()) {
+                        best_total = total;
+                        g = std::move(g1);
+                        s_best = std::move(s2);
+                    }
+                }
+            } else {
+                for (auto& sc : scored)
+                    if (sc.first > (int)g.items.size()) {
+                        State s2 = st;
+                        g = absorb(s2, fixed_bits | sc.second);
+                        s_best = std::move(s2);
+                    }
             }
         }
         if (g.items.empty()) return {};  // an item needs more bits than the budget
@@ -367,14 +397,26 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
     // cap the gates per sweep: the specialised kernels are straight-line code, and
     // very long sweeps overflow the instruction cache
     // Cap on gates per sweep.  The generated kernels are straight-line code and
-    // ptxas time grows faster than linearly with their length: C2's 205-op first
-    // adjoint sweep alone took 90 % of a cold NVRTC build (151 s of CPU on this
-    // container, 24 s on a GPU host).  120 ops splits it in two at no run-time
-    // cost (C2 206.8 vs 207.6 ms per step, profiles/r2_sweep_experiments.md)
-    // and cuts the cold build 3.5x.  QF_MAX_SWEEP_OPS=n overrides (0 = no cap).
-    int max_ops = 120;
+    // ptxas time grows faster than linearly with their length.  With the tile and
+    // phase searches, 200 ops costs nothing at run time against no cap (C2 181.6
+    // vs 181.1 ms per step) and bounds pathological sweeps; 120 would halve C2's
+    // cold NVRTC build (21.0 -> 8.5 s on the GPU host) for 2.5 % C2 / 1.7 % C5
+    // throughput (tools/r2_p11.sh).  QF_MAX_SWEEP_OPS=n overrides (0 = no cap).
+    int max_ops = 200;
     if (const char* e = std::getenv("QF_MAX_SWEEP_OPS")) max_ops = std::atoi(e);
-    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops);
+    // Sweep tiles: besides the greedy tile, every window of consecutive memory
+    // bits above the fixed ones; the tile whose closure holds the most gates wins.
+    // For the layered ansatz this follows the light-cone staircase (C2: 6 + 7
+    // sweeps instead of 10 + 14 under the 120-op cap).  Together with the phase
+    // search it pays: C2 194.7 -> 184.5 ms per step, C3 +11 %, C5 +3 %; alone
+    // (greedy phases) it did not (profiles/r2_sweep_experiments.md).
+    // QF_SWEEP_SEARCH=0: greedy only; QF_SWEEP_LOOKAHEAD=K: two-level choice.
+    static const bool sweep_search = !(std::getenv("QF_SWEEP_SEARCH") && std::getenv("QF_SWEEP_SEARCH")[0] == '0');
+    static const int sweep_look = [] {
+        const char* e = std::getenv("QF_SWEEP_LOOKAHEAD");
+        return e ? std::atoi(e) : 0;
+    }();
+    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops, sweep_search, sweep_look);
 
     for (auto& sw : sweeps) {
         // pad the tile to exactly k bits with the lowest free positions
@@ -419,7 +461,11 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
         // phases and 205.2 -> 198.0 ms per step.  QF_PHASE_SEARCH=0: greedy only,
         // =w: windows of consecutive tile bits only (development A/B).
         static const bool phase_search = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == '0');
-        auto phases = schedule_groups(lneed, lpreds, 0, R, 0, phase_search);
+        static const int phase_look = [] {
+            const char* e = std::getenv("QF_PHASE_LOOKAHEAD");
+            return e ? std::atoi(e) : 0;
+        }();
+        auto phases = schedule_groups(lneed, lpreds, 0, R, 0, phase_search, phase_look);
         // Inside a phase, issue ready non-diagonal gates first and release the
         // diagonal ones (which commute with each other) in batches: long runs of
         // diagonal gates and Z taps are fused by the kernel generator.

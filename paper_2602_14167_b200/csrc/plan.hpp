@@ -84,6 +84,7 @@ struct Group {
 };
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items = 0, bool search = false);
+                                   uint64_t fixed_bits, int budget, int max_items = 0, bool search = false,
+                                   int lookahead = 0);
 
 }  // namespace qfb
