@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <complex>
+#include <functional>
 #include <map>
 #include <set>
 
@@ -56,7 +57,8 @@ static bool env_flag_off(const char* name) {
 
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items, bool search, int lookahead) {
+                                   uint64_t fixed_bits, int budget, int max_items, bool search, int lookahead,
+                                   const std::function<double(const Group&)>* score) {
     const int n = (int)need.size();
     struct State {
         std::set<int> ready;
@@ -191,6 +193,19 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                     if (total > best_total && g1.items.size() >= g.items.size()) {
                         best_total = total;
                         g = std::move(g1);
+                        s_best = std::move(s2);
+                    }
+                }
+            } else if (score) {
+                // caller's cost model (e.g. gates per phase of the resulting sweep)
+                double best = (*score)(g);
+                for (auto& sc : scored) {
+                    State s2 = st;
+                    Group gw = absorb(s2, fixed_bits | sc.second);
+                    const double v = (*score)(gw);
+                    if (v > best) {
+                        best = v;
+                        g = std::move(gw);
                         s_best = std::move(s2);
                     }
                 }
@@ -416,7 +431,36 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
         const char* e = std::getenv("QF_SWEEP_LOOKAHEAD");
         return e ? std::atoi(e) : 0;
     }();
-    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops, sweep_search, sweep_look);
+    // QF_SWEEP_OBJ=ratio: score a candidate tile by gates per phase of the sweep it
+    // would make (its closure scheduled into phases), cost floored at 1.5 phases
+    // for the HBM pass (development A/B)
+    static const char* obj_env = std::getenv("QF_SWEEP_OBJ");
+    const bool ratio_obj = obj_env && (std::string(obj_env) == "ratio" || (std::string(obj_env) == "ratio_fwd" && !adjoint));
+    std::function<double(const Group&)> ratio_score = [&](const Group& gw) -> double {
+        if (gw.items.empty()) return -1.0;
+        uint64_t bits = gw.bits;
+        for (int p = 0; p < n && popc(bits) < k; ++p) bits |= 1ull << p;
+        int tl[64];
+        int t = 0;
+        for (int p = 0; p < 64; ++p) tl[p] = (bits >> p & 1) ? t++ : -1;
+        std::map<int, int> loc;
+        for (size_t i = 0; i < gw.items.size(); ++i) loc[gw.items[i]] = (int)i;
+        std::vector<uint64_t> ln(gw.items.size());
+        std::vector<std::vector<int>> lp(gw.items.size());
+        for (size_t i = 0; i < gw.items.size(); ++i) {
+            const int it = gw.items[i];
+            for (int p = 0; p < n; ++p)
+                if (need[it] >> p & 1) ln[i] |= 1ull << tl[p];
+            for (int pr : preds_in_order[it]) {
+                auto f = loc.find(pr);
+                if (f != loc.end()) lp[i].push_back(f->second);
+            }
+        }
+        const auto ph = schedule_groups(ln, lp, 0, R, 0, true);
+        return (double)gw.items.size() / std::max(1.5, (double)ph.size());
+    };
+    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops, sweep_search, sweep_look,
+                                  ratio_obj ? &ratio_score : nullptr);
 
     for (auto& sw : sweeps) {
         // pad the tile to exactly k bits with the lowest free positions

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "plan.h"
@@ -85,6 +86,6 @@ struct Group {
 std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                                    const std::vector<std::vector<int>>& preds,
                                    uint64_t fixed_bits, int budget, int max_items = 0, bool search = false,
-                                   int lookahead = 0);
+                                   int lookahead = 0, const std::function<double(const Group&)>* score = nullptr);
 
 }  // namespace qfb
