@@ -31,14 +31,24 @@ Geometry geometry(int prec, int n) {
         g.kf = 13; g.Rf = 5; g.kb = 12; g.Rb = 4; g.kh = 12; g.c = 4; g.W = 4;
     }
     // development override: QF_GEOM_C64 / QF_GEOM_C128 = "kf,Rf,kb,Rb"
+    bool overridden = false;
     if (const char* e = std::getenv(prec == QF_C128 ? "QF_GEOM_C128" : "QF_GEOM_C64")) {
         int a, b, c, d;
         if (std::sscanf(e, "%d,%d,%d,%d", &a, &b, &c, &d) == 4) {
             g.kf = a; g.Rf = b; g.kb = c; g.Rb = d;
+            overridden = true;
         }
     }
     g.kf = std::min(g.kf, n);
     g.kb = std::min(g.kb, n);
+    // Small states (one tile, or a few, per state): a tile's 2^(k - R) threads are
+    // all the parallelism a state gets, so keep >= 256 threads per tile by trading
+    // register bits for threads (more phases, each cheaper).  C1 (n = 10, batch
+    // 16): 271 k -> 533 k evals/s (tools/r2_c1g.sh).
+    if (!overridden && n <= 12) {
+        g.Rf = std::max(2, std::min(g.Rf, g.kf - 8));
+        g.Rb = std::max(2, std::min(g.Rb, g.kb - 8));
+    }
     g.kh = std::min(g.kh, n);
     g.Rf = std::min(g.Rf, g.kf);
     g.Rb = std::min(g.Rb, g.kb);
