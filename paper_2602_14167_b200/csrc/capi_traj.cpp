@@ -693,8 +693,27 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
             QF_CUDA(cudaMemcpyAsync(d_u.p, u + (size_t)t0 * n_apps, (size_t)nb * n_apps * 8, cudaMemcpyHostToDevice, s));
         int app = 0;
         size_t si = 0;
+        // The last channel's branch K / sqrt(p) of an op stays pending in d_k and is
+        // folded into the next noisy op's pass when their wires are disjoint
+        // (apply2_rho: one state pass instead of two); otherwise it is applied alone.
+        int pend = -1;
+        auto flush = [&]() -> cudaError_t {
+            if (pend < 0) return cudaSuccess;
+            const cudaError_t e = launch_apply_local(precision, ctx->lam.p, n, nb, P0[pend], P1[pend],
+                                                     (const double2*)d_k.p, true, s);
+            ctx->launches++;
+            pend = -1;
+            return e;
+        };
+        auto disjoint = [&](int a, int b) {
+            const uint32_t ma = (1u << P0[a]) | (P1[a] >= 0 ? 1u << P1[a] : 0u);
+            const uint32_t mb = (1u << P0[b]) | (P1[b] >= 0 ? 1u << P1[b] : 0u);
+            return (ma & mb) == 0;
+        };
+        static const bool fold = !(std::getenv("QF_NOISE_FOLD") && std::getenv("QF_NOISE_FOLD")[0] == '0');
         for (int j = 0; j < n_ops;) {
             if (si < segs.size() && segs[si].j0 == j) {  // fused channel-free run
+                QF_CUDA(flush());
                 qf_program* pg = segs[si].prog;
                 const ProgramPlan& PP = pg->plan;
                 SweepArgs sa{};
@@ -724,6 +743,7 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
             const int c0 = op_chan_ptr[j], c1 = op_chan_ptr[j + 1];
             const double2* g = (const double2*)d_gm.p + (size_t)j * 16;
             if (c0 == c1) {
+                QF_CUDA(flush());
                 QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], g, false, s));
                 ctx->launches++;
                 ++j;
@@ -731,7 +751,14 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
             }
             // gate, then per channel: rho of the current state on the gate's wires ->
             // branch pick -> K / sqrt(p) (fused with the next channel's rho)
-            QF_CUDA(launch_apply_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], g, false, (double2*)d_rho.p, s));
+            if (fold && pend >= 0 && disjoint(pend, j)) {
+                QF_CUDA(launch_apply2_rho(precision, ctx->lam.p, n, nb, P0[pend], P1[pend], (const double2*)d_k.p,
+                                          P0[j], P1[j], g, (double2*)d_rho.p, s));
+                pend = -1;
+            } else {
+                QF_CUDA(flush());
+                QF_CUDA(launch_apply_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], g, false, (double2*)d_rho.p, s));
+            }
             ctx->launches++;
             for (int ci = c0; ci < c1; ++ci, ++app) {
                 const int ch = op_chan[ci];
@@ -740,16 +767,18 @@ int qf_noise_trajectories(qf_ctx* ctx, int n, int n_ops, const qf_op* ops, const
                 QF_CUDA(launch_kraus_pick((const double2*)d_rho.p, parts, Dg[j], (const double*)d_kraus.p, k0, k1,
                                           (const double*)d_u.p, n_apps, app, (double2*)d_k.p, (double*)d_logp.p,
                                           (int*)d_err.p, nb, s));
-                if (ci + 1 < c1)
+                if (ci + 1 < c1) {
                     QF_CUDA(launch_apply_rho(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true,
                                              (double2*)d_rho.p, s));
-                else
-                    QF_CUDA(launch_apply_local(precision, ctx->lam.p, n, nb, P0[j], P1[j], (const double2*)d_k.p, true,
-                                               s));
-                ctx->launches += 2;
+                    ctx->launches += 2;
+                } else {
+                    pend = j;  // applied by the next pass (or flushed)
+                    ctx->launches += 1;
+                }
             }
             ++j;
         }
+        QF_CUDA(flush());
         if (log_probs)
             QF_CUDA(cudaMemcpyAsync(log_probs + t0, d_logp.p, (size_t)nb * 8, cudaMemcpyDeviceToHost, s));
         if (obs) {

@@ -110,6 +110,10 @@ cudaError_t launch_set_basis0(int prec, void* psi, int n, int batch, cudaStream_
 // result on those wires ([batch][local_rho_parts(n)][D][D], fixed order)
 cudaError_t launch_apply_rho(int prec, void* psi, int n, int batch, int p0, int p1, const double2* m, bool per_state,
                              double2* rho, cudaStream_t s);
+// the same with a pending per-trajectory operator kp ([batch][DP][DP]) on the
+// disjoint wires (q0[, q1]) applied first, in the same pass
+cudaError_t launch_apply2_rho(int prec, void* psi, int n, int batch, int q0, int q1, const double2* kp, int p0,
+                              int p1, const double2* g, double2* rho, cudaStream_t s);
 // per-trajectory Kraus branch pick for one channel application (kraus: [k][4][4]
 // complex, channel = k0 .. k1-1; u[b * u_stride + app]); kout [batch][D][D],
 // logp[b] += log p_pick; err = 1 if all branch probabilities vanish

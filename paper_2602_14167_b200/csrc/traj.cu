@@ -300,6 +300,111 @@ __global__ void __launch_bounds__(256) apply_rho_kernel(V* psi, int n, int p0, i
     }
 }
 
+// Noise step with the previous channel's branch folded in: the pending
+// per-trajectory K/sqrt(p) on wires Wp, then the gate on the disjoint wires Wj,
+// then the local rho partials on Wj -- one state pass instead of two.  Local
+// amplitude index l = (ip << log2 DJ) | ij (wires[0] most significant in each).
+template <typename V, int DP, int DJ>
+__global__ void __launch_bounds__(256) apply2_rho_kernel(V* psi, int n, int q0, int q1, const double2* kp, int p0,
+                                                         int p1, const double2* g, double2* rho) {
+    __shared__ double red[8][2 * DJ * DJ];
+    const int b = blockIdx.y, part = blockIdx.x, parts = gridDim.x;
+    const double2* kb = kp + (size_t)b * DP * DP;
+    double2 km[DP * DP], gm[DJ * DJ];
+#pragma unroll
+    for (int i = 0; i < DP * DP; ++i) km[i] = kb[i];
+#pragma unroll
+    for (int i = 0; i < DJ * DJ; ++i) gm[i] = g[i];
+    const uint32_t N = 1u << n, R = N / (DP * DJ);
+    const uint32_t mp = DP == 2 ? (1u << q0) : ((1u << q0) | (1u << q1));
+    const uint32_t mj = DJ == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
+    const uint32_t free = (N - 1) & ~(mp | mj);
+    V* ps = psi + (size_t)b * N;
+    double acc[2 * DJ * DJ];
+#pragma unroll
+    for (int i = 0; i < 2 * DJ * DJ; ++i) acc[i] = 0.0;
+    auto dep = [](int i, int D, int w0, int w1) -> uint32_t {
+        return D == 2 ? (i ? (1u << w0) : 0u) : ((((i >> 1) & 1) ? (1u << w0) : 0u) | ((i & 1) ? (1u << w1) : 0u));
+    };
+    const uint32_t r0 = (uint32_t)((uint64_t)R * part / parts), r1 = (uint32_t)((uint64_t)R * (part + 1) / parts);
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const uint32_t base = pdep32(r, free);
+        uint32_t idx[DP * DJ];
+        double2 a[DP * DJ];
+#pragma unroll
+        for (int ip = 0; ip < DP; ++ip)
+#pragma unroll
+            for (int ij = 0; ij < DJ; ++ij) {
+                const int l = ip * DJ + ij;
+                idx[l] = base | dep(ip, DP, q0, q1) | dep(ij, DJ, p0, p1);
+                const V v = ps[idx[l]];
+                a[l] = make_double2((double)v.x, (double)v.y);
+            }
+        // pending Kraus branch on Wp (same arithmetic as apply_local_kernel)
+#pragma unroll
+        for (int ij = 0; ij < DJ; ++ij) {
+            double2 t[DP];
+#pragma unroll
+            for (int i = 0; i < DP; ++i) {
+                double re = 0.0, im = 0.0;
+#pragma unroll
+                for (int j = 0; j < DP; ++j) {
+                    const double2 c = km[i * DP + j], x = a[j * DJ + ij];
+                    re += c.x * x.x - c.y * x.y;
+                    im += c.x * x.y + c.y * x.x;
+                }
+                t[i] = make_double2(re, im);
+            }
+#pragma unroll
+            for (int i = 0; i < DP; ++i) {  // round to the state precision, as a separate pass would store
+                V w;
+                w.x = (decltype(w.x))t[i].x;
+                w.y = (decltype(w.y))t[i].y;
+                a[i * DJ + ij] = make_double2((double)w.x, (double)w.y);
+            }
+        }
+        // gate on Wj, store, rho partials of the result
+#pragma unroll
+        for (int ip = 0; ip < DP; ++ip) {
+            double2 o[DJ];
+#pragma unroll
+            for (int i = 0; i < DJ; ++i) {
+                double re = 0.0, im = 0.0;
+#pragma unroll
+                for (int j = 0; j < DJ; ++j) {
+                    const double2 c = gm[i * DJ + j], x = a[ip * DJ + j];
+                    re += c.x * x.x - c.y * x.y;
+                    im += c.x * x.y + c.y * x.x;
+                }
+                V w;
+                w.x = (decltype(w.x))re;
+                w.y = (decltype(w.y))im;
+                ps[idx[ip * DJ + i]] = w;
+                o[i] = make_double2((double)w.x, (double)w.y);
+            }
+#pragma unroll
+            for (int i = 0; i < DJ; ++i)
+#pragma unroll
+                for (int j = 0; j < DJ; ++j) {
+                    acc[2 * (i * DJ + j)] += o[i].x * o[j].x + o[i].y * o[j].y;
+                    acc[2 * (i * DJ + j) + 1] += o[i].y * o[j].x - o[i].x * o[j].y;
+                }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * DJ * DJ; ++i) {
+        double v = acc[i];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * DJ * DJ) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+        reinterpret_cast<double*>(rho + ((size_t)b * parts + part) * DJ * DJ)[threadIdx.x] = t;
+    }
+}
+
 __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -488,6 +593,27 @@ cudaError_t launch_apply_rho(int prec, void* psi, int n, int batch, int p0, int 
         if (D == 2) apply_rho_kernel<float2, 2><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms, rho);
         else apply_rho_kernel<float2, 4><<<grid, 256, 0, s>>>((float2*)psi, n, p0, p1, m, ms, rho);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply2_rho(int prec, void* psi, int n, int batch, int q0, int q1, const double2* kp, int p0,
+                              int p1, const double2* g, double2* rho, cudaStream_t s) {
+    if (batch == 0) return cudaSuccess;
+    const int DP = q1 >= 0 ? 4 : 2, DJ = p1 >= 0 ? 4 : 2;
+    const dim3 grid(local_rho_parts(n), batch);
+#define QF_A2(T, A, B) apply2_rho_kernel<T, A, B><<<grid, 256, 0, s>>>((T*)psi, n, q0, q1, kp, p0, p1, g, rho)
+    if (prec == 1) {
+        if (DP == 2 && DJ == 2) QF_A2(double2, 2, 2);
+        else if (DP == 2) QF_A2(double2, 2, 4);
+        else if (DJ == 2) QF_A2(double2, 4, 2);
+        else QF_A2(double2, 4, 4);
+    } else {
+        if (DP == 2 && DJ == 2) QF_A2(float2, 2, 2);
+        else if (DP == 2) QF_A2(float2, 2, 4);
+        else if (DJ == 2) QF_A2(float2, 4, 2);
+        else QF_A2(float2, 4, 4);
+    }
+#undef QF_A2
     return cudaGetLastError();
 }
 
