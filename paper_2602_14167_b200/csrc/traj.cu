@@ -18,6 +18,12 @@ __device__ __forceinline__ uint32_t pdep32(uint32_t t, uint32_t m) {
     return r;
 }
 
+// pdep32(t + k, m) from x = pdep32(t, m) and step = pdep32(k, m): the carry runs
+// through the masked-out bits (no per-element bit loop)
+__device__ __forceinline__ uint32_t pdep_add(uint32_t x, uint32_t step, uint32_t m) {
+    return ((x | ~m) + step) & m;
+}
+
 // block (beta, b): sum of |psi[x]|^2 over x whose measured bits spell beta
 template <typename V>
 __global__ void __launch_bounds__(256) meas_hist_kernel(const V* psi, int n, const MeasRound* rounds, double* hist) {
@@ -188,8 +194,9 @@ __global__ void apply_local_kernel(V* psi, int n, int p0, int p1, const double2*
     const uint32_t mask = D == 2 ? (1u << p0) : ((1u << p0) | (1u << p1));
     const uint32_t free = (N - 1) & ~mask;
     V* ps = psi + (size_t)b * N;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-        const uint32_t base = pdep32(r, free);
+    const uint32_t stride = gridDim.x * blockDim.x, step = pdep32(stride, free);
+    uint32_t base = pdep32(blockIdx.x * blockDim.x + threadIdx.x, free);
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += stride, base = pdep_add(base, step, free)) {
         uint32_t idx[D];
         double2 a[D];
 #pragma unroll
@@ -241,7 +248,9 @@ __global__ void __launch_bounds__(256) apply_rho_kernel(V* psi, int n, int p0, i
     // two amplitude groups per iteration, both loaded before either is stored
     // (the stores would otherwise order every next load behind them)
     constexpr int U = 2;
-    for (uint32_t r = r0 + threadIdx.x; r < r1; r += U * blockDim.x) {
+    const uint32_t step1 = pdep32(blockDim.x, free), stepU = pdep32(U * blockDim.x, free);
+    uint32_t base0 = pdep32(r0 + threadIdx.x, free);
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += U * blockDim.x, base0 = pdep_add(base0, stepU, free)) {
         uint32_t idx[U][D];
         double2 a[U][D];
         bool live[U];
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(256) apply_rho_kernel(V* psi, int n, int p0, i
         for (int u = 0; u < U; ++u) {
             const uint32_t ru = r + u * blockDim.x;
             live[u] = ru < r1;
-            const uint32_t base = pdep32(live[u] ? ru : r, free);
+            const uint32_t base = (u == 0 || !live[u]) ? base0 : pdep_add(base0, step1, free);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 idx[u][i] = base | (D == 2 ? (i ? (1u << p0) : 0u)
@@ -327,8 +336,9 @@ __global__ void __launch_bounds__(256) apply2_rho_kernel(V* psi, int n, int q0, 
         return D == 2 ? (i ? (1u << w0) : 0u) : ((((i >> 1) & 1) ? (1u << w0) : 0u) | ((i & 1) ? (1u << w1) : 0u));
     };
     const uint32_t r0 = (uint32_t)((uint64_t)R * part / parts), r1 = (uint32_t)((uint64_t)R * (part + 1) / parts);
-    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        const uint32_t base = pdep32(r, free);
+    const uint32_t step = pdep32(blockDim.x, free);
+    uint32_t base = pdep32(r0 + threadIdx.x, free);
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += blockDim.x, base = pdep_add(base, step, free)) {
         uint32_t idx[DP * DJ];
         double2 a[DP * DJ];
 #pragma unroll

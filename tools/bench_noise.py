@@ -35,9 +35,11 @@ for n, layers, T, sparse in [(16, 4, 1000, False), (20, 4, 256, False), (16, 4, 
     h = po.tfim(n, 1.0)
     obs = engine.Observable(ctx, n, h.codes, h.wr + 1j * h.wi)
     engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u[:2], "c64", obs=obs, want_states=False)
-    t0 = time.perf_counter()
-    _, logp, ev = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, "c64", obs=obs, want_states=False)
-    dt = time.perf_counter() - t0
+    dt = None
+    for _rep in range(3):  # best of three calls (wall clock of one call is noisy)
+        t0 = time.perf_counter()
+        _, logp, ev = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, "c64", obs=obs, want_states=False)
+        dt = min(dt, time.perf_counter() - t0) if dt is not None else time.perf_counter() - t0
     rec = {"n": n, "layers": layers, "gates": len(ops), "channel_applications": n_apps, "channels": "cx only (rotation runs fused)" if sparse else "after every gate", "trajectories": T,
            "precision": "c64", "seconds": dt, "s_per_traj": dt / T, "mean_energy": float(ev.mean())}
     if n <= 16:
