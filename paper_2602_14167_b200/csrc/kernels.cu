@@ -109,6 +109,29 @@ __device__ __forceinline__ void hp_cp_async(double2* dst, const double2* src) {
                  "l"(src) : "memory");
 }
 
+// TMA bulk copy (cp.async.bulk, sm_90+) of one contiguous partner tile into shared
+// memory, completion counted in bytes on an mbarrier
+__device__ __forceinline__ void hp_mbar_init(uint64_t* mb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(mb)) : "memory");
+}
+__device__ __forceinline__ void hp_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+    const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(m), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(m)
+                 : "memory");
+}
+__device__ __forceinline__ void hp_mbar_wait(uint64_t* mb, uint32_t parity) {
+    const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\n"
+                     : "=r"(done)
+                     : "r"(m), "r"(parity)
+                     : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // lambda = H psi and E = Re<psi|lambda>, output-stationary per tile.  Partner
 // tiles (flip groups above the tile) are double-buffered: the next group's tile
@@ -146,15 +169,30 @@ __global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
         while (from < a.n_groups && a.groups[from].f_out == 0) ++from;
         return from;
     };
-    auto prefetch = [&](int gi, V* buf) {
+    // Partner tiles are contiguous (the tile is the low kh bits), so with a.tma one
+    // thread moves each with a single TMA bulk copy on the buffer's mbarrier;
+    // otherwise every thread issues cp.async for its amplitudes.
+    __shared__ __align__(8) uint64_t mbar[2];
+    uint32_t par[2] = {0u, 0u};
+    if (a.tma && tid == 0) {
+        hp_mbar_init(&mbar[0]);
+        hp_mbar_init(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    auto prefetch = [&](int gi, V* buf, int slot) {
         const V* pp = ps + (base ^ a.groups[gi].f_out);
+        if (a.tma) {
+            if (tid == 0) hp_bulk_load(buf, pp, TS * (uint32_t)sizeof(V), &mbar[slot]);
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < NA; ++i) hp_cp_async(buf + tid + T * i, pp + tid + T * i);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     int k = 0;  // outer groups seen
     const int first = next_outer(0);
-    if (a.prefetch && first < a.n_groups) prefetch(first, part);
+    if (a.tma) __syncthreads();  // barriers initialised before any use
+    if (a.prefetch && first < a.n_groups) prefetch(first, part, 0);
     __syncthreads();
     for (int gi = 0; gi < a.n_groups; ++gi) {
         const DevGroup g = a.groups[gi];
@@ -162,10 +200,15 @@ __global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
         if (g.f_out && a.prefetch) {
             // this group's tile (buffer k & 1) has landed for every thread, and every
             // thread is done with buffer (k + 1) & 1 (the previous outer group)
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            if (a.tma) {
+                hp_mbar_wait(&mbar[k & 1], par[k & 1]);
+                par[k & 1] ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            }
             __syncthreads();
             const int nn = next_outer(gi + 1);
-            if (nn < a.n_groups) prefetch(nn, part + TS * ((k + 1) & 1));
+            if (nn < a.n_groups) prefetch(nn, part + TS * ((k + 1) & 1), (k + 1) & 1);
             src = part + TS * (k & 1);
             ++k;
         } else if (g.f_out) {  // compute-heavy groups: plain staged load

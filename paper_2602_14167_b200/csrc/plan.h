@@ -141,6 +141,7 @@ struct HArgs {
     int use_imag;
     double* epart;             // [B][tiles]
     int prefetch;              // generic kernel: double-buffer partner tiles (few terms per group)
+    int tma;                   // generic kernel, with prefetch: partner tiles by TMA bulk copy + mbarrier
 };
 
 // Kernel arguments of one sweep launch (AOT interpreter and NVRTC kernels).
