@@ -187,7 +187,7 @@ int eval_chunk(qf_ctx* ctx, qf_program* prog, ObsDev* od, int b0, int bc, const 
     ha.epart = (double*)ctx->epart.p;
     ha.prefetch = od->plan.terms.size() <= 4 * std::max<size_t>(1, od->plan.groups.size()) ? 1 : 0;
     static const bool hpsi_tma = !(std::getenv("QF_HPSI_TMA") && std::getenv("QF_HPSI_TMA")[0] == '0');
-    ha.tma = ha.prefetch && hpsi_tma ? 1 : 0;
+    ha.tma = hpsi_tma ? 1 : 0;
     ltick();
     if (od->hj_state == 1)
         QF_CUDA((cudaError_t)jit_launch_hpsi(od->hj, ha, tiles_h, bc, s));

@@ -211,12 +211,18 @@ __global__ void __launch_bounds__(TPB, 3) hpsi_kernel(const HArgs a) {
             if (nn < a.n_groups) prefetch(nn, part + TS * ((k + 1) & 1), (k + 1) & 1);
             src = part + TS * (k & 1);
             ++k;
-        } else if (g.f_out) {  // compute-heavy groups: plain staged load
-            __syncthreads();
+        } else if (g.f_out) {  // compute-heavy groups: one staged partner tile
+            __syncthreads();  // every thread is done with the previous partner tile
             const V* pp = ps + (base ^ g.f_out);
+            if (a.tma) {
+                if (tid == 0) hp_bulk_load(part, pp, TS * (uint32_t)sizeof(V), &mbar[0]);
+                hp_mbar_wait(&mbar[0], par[0]);
+                par[0] ^= 1u;
+            } else {
 #pragma unroll
-            for (int i = 0; i < NA; ++i) part[tid + T * i] = pp[tid + T * i];
-            __syncthreads();
+                for (int i = 0; i < NA; ++i) part[tid + T * i] = pp[tid + T * i];
+                __syncthreads();
+            }
             src = part;
         }
         if constexpr (!SW) {
