@@ -21,6 +21,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -57,7 +58,7 @@ __device__ void block_sum(double (&x)[NV], double (*red)[NV]) {
 
 // RPT rows per thread (m <= RPT * blockDim.x).  smem: v (reflector of this step),
 // w (its rank-2 partner), vn (next reflector), p (tau A22 v of this step).
-template <int RPT>
+template <int RPT, int UN>
 __global__ void __launch_bounds__(1024, 1) hetrd_kernel(double2* A, int m, double* d_out, double* e_out) {
     extern __shared__ __align__(16) double2 hsm[];
     __shared__ double red[32][2];
@@ -198,17 +199,17 @@ __global__ void __launch_bounds__(1024, 1) hetrd_kernel(double2* A, int m, doubl
 #pragma unroll
         for (int q = 0; q < RPT; ++q) acc[q] = make_double2(0.0, 0.0);
         int j = 1;
-        for (; j + 4 <= L; j += 4) {
-            double2 a[RPT][4];
+        for (; j + UN <= L; j += UN) {
+            double2 a[RPT][UN];
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
                 const int r = tid + q * T;
                 if (r < L)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) a[q][u] = A22[(size_t)(j + u) * m + r];
+                    for (int u = 0; u < UN; ++u) a[q][u] = A22[(size_t)(j + u) * m + r];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < UN; ++u) {
                 const double2 wj = w[j + u], vj = v[j + u], vnj = nxt ? vn[j + u - 1] : make_double2(0.0, 0.0);
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
@@ -332,15 +333,27 @@ cudaError_t launch_hermitian_eigvals(double2* A, int m, int batch, double* d, do
     const int rpt = (m + T - 1) / T;
     const size_t hs = 4 * (size_t)m * sizeof(double2);
     cudaError_t err = cudaSuccess;
+    static const int un = [] {  // columns in flight per thread in the fused sweep (development A/B)
+        const char* e = std::getenv("QF_HETRD_UNROLL");
+        return e && std::atoi(e) == 8 ? 8 : e && std::atoi(e) == 2 ? 2 : 4;
+    }();
+#define QF_HT(R_, U_)                                                                                     \
+    do {                                                                                                  \
+        err = cudaFuncSetAttribute(hetrd_kernel<R_, U_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs); \
+        if (err == cudaSuccess) hetrd_kernel<R_, U_><<<batch, T, hs, s>>>(A, m, d, e);                     \
+    } while (0)
     if (rpt <= 1) {
-        err = cudaFuncSetAttribute(hetrd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
-        if (err == cudaSuccess) hetrd_kernel<1><<<batch, T, hs, s>>>(A, m, d, e);
+        if (un == 8) QF_HT(1, 8);
+        else if (un == 2) QF_HT(1, 2);
+        else QF_HT(1, 4);
     } else if (rpt <= 2) {
-        err = cudaFuncSetAttribute(hetrd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
-        if (err == cudaSuccess) hetrd_kernel<2><<<batch, T, hs, s>>>(A, m, d, e);
+        if (un == 8) QF_HT(2, 8);
+        else if (un == 2) QF_HT(2, 2);
+        else QF_HT(2, 4);
     } else {
         return cudaErrorInvalidValue;  // m > 2048 (v, w, v', p staged in shared memory)
     }
+#undef QF_HT
     if (err != cudaSuccess) return err;
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
