@@ -1178,8 +1178,21 @@ int jit_hpsi_threads(const ObservablePlan& O) {
     return TS < 256 ? TS : 256;
 }
 
+// QF_JIT_HPSI_TMA=1: partner tiles of the specialised H|psi> by TMA bulk copy,
+// double-buffered on two mbarriers.  Measured slower than the default direct
+// register loads (C2 H|psi> 6.83 vs 5.73 ms, C3 46.9 vs 43.6 ms: the per-group
+// barrier costs more than the L2 latency it hides; tools/r2_t3.sh), so opt-in.
+static bool jit_hpsi_tma(const ObservablePlan& O) {
+    static const bool on = std::getenv("QF_JIT_HPSI_TMA") && std::getenv("QF_JIT_HPSI_TMA")[0] == '1';
+    if (!on) return false;
+    for (const DevGroup& g : O.groups)
+        if (g.f_out) return true;
+    return false;
+}
+
 size_t jit_hpsi_smem(const ObservablePlan& O, int prec) {
-    return ((size_t)2 << O.kh) * (prec == QF_C128 ? 16 : 8) + 64;
+    const size_t vs = prec == QF_C128 ? 16 : 8;
+    return (jit_hpsi_tma(O) ? ((size_t)3 << O.kh) * vs + 64 + 16 : ((size_t)2 << O.kh) * vs + 64);
 }
 
 std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
@@ -1196,12 +1209,30 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
     o("extern \"C\" __global__ void __launch_bounds__(%d, 2) qf_hpsi(const HArgs a) {", T);
     o("  typedef %s V; typedef %s RT;", dbl ? "double2" : "float2", dbl ? "double" : "float");
     o("  extern __shared__ __align__(16) unsigned char smem_raw[];");
+    const bool tma = jit_hpsi_tma(O);
     o("  V* own = reinterpret_cast<V*>(smem_raw); V* part = own + %d; (void)own; (void)part;", TS);
-    o("  double* red = reinterpret_cast<double*>(part + %d);", TS);
+    if (tma) {
+        o("  V* part1 = part + %d;", TS);
+        o("  double* red = reinterpret_cast<double*>(part1 + %d);", TS);
+        o("  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 8);");
+    } else {
+        o("  double* red = reinterpret_cast<double*>(part + %d);", TS);
+    }
     o("  const uint32_t tid = threadIdx.x, tile = blockIdx.x; const int b = blockIdx.y;");
     o("  const V* ps = reinterpret_cast<const V*>(a.psi) + (size_t)b * %zuull;", N);
     o("  const uint32_t base = tile << %d; (void)base;", kh);
     for (int i = 0; i < NA; ++i) o("  const V po%d = ps[(size_t)base + (tid + %uu)];", i, (unsigned)(T * i));
+    std::vector<uint32_t> outer_f;  // outer groups in order (TMA prefetch chain)
+    for (const DevGroup& g : O.groups)
+        if (g.f_out) outer_f.push_back(g.f_out);
+    const unsigned tile_bytes = (unsigned)TS * (dbl ? 16u : 8u);
+    if (tma) {
+        o("  if (tid == 0) { jit_mbar_init(&mbar[0]); jit_mbar_init(&mbar[1]); "
+          "asm volatile(\"fence.mbarrier_init.release.cluster;\\n\" ::: \"memory\"); }");
+        o("  __syncthreads();");
+        o("  if (tid == 0) jit_bulk_load(part, ps + (size_t)(base ^ %uu), %uu, &mbar[0]);", outer_f[0], tile_bytes);
+    }
+    int outer_k = 0;
     bool own_smem = false;
     std::set<uint32_t> dmasks;
     for (const DevGroup& g : O.groups)
@@ -1222,7 +1253,17 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
         bool need_smem = false;
         for (int t = g.term_begin; t < g.term_end; ++t) need_smem |= (O.terms[t].f_in & (uint32_t)(T - 1)) != 0;
         o("  {  // flip group 0x%x", g.f_out);
-        if (outer) {
+        const char* pbuf = (outer_k & 1) ? "part1" : "part";
+        if (outer && tma) {
+            // this group's tile landed (buffer k & 1, phase k >> 1); every thread is done
+            // with the other buffer (previous outer group), which takes the next tile
+            o("    jit_mbar_wait(&mbar[%d], %uu);", outer_k & 1, (unsigned)((outer_k >> 1) & 1));
+            o("    __syncthreads();");
+            if (outer_k + 1 < (int)outer_f.size())
+                o("    if (tid == 0) jit_bulk_load(%s, ps + (size_t)(base ^ %uu), %uu, &mbar[%d]);",
+                  (outer_k & 1) ? "part" : "part1", outer_f[outer_k + 1], tile_bytes, (outer_k + 1) & 1);
+            for (int i = 0; i < NA; ++i) o("    const V q%d = %s[tid + %uu];", i, pbuf, (unsigned)(T * i));
+        } else if (outer) {
             for (int i = 0; i < NA; ++i)
                 o("    const V q%d = ps[(size_t)(base ^ %uu) + (tid + %uu)];", i, g.f_out, (unsigned)(T * i));
             if (need_smem) {
@@ -1233,7 +1274,8 @@ std::string jit_hpsi_source(const ObservablePlan& O, int prec) {
             }
         }
         const char* R = outer ? "q" : "po";
-        const char* S = outer ? "part" : "own";
+        const char* S = outer ? (tma ? pbuf : "part") : "own";
+        if (outer) ++outer_k;
         for (int t = g.term_begin; t < g.term_end; ++t) {
             const DevTerm& d = O.terms[t];
             const uint32_t zt = d.z & (uint32_t)(T - 1), zr = (d.z >> LT) & (uint32_t)(NA - 1);

@@ -165,4 +165,27 @@ __device__ __forceinline__ void tap_flush(const RT* stg, int cnt, int T, double*
     }
 }
 
+// TMA bulk copy (cp.async.bulk) of a contiguous global range into shared memory,
+// completion counted in bytes on an mbarrier (specialised H|psi> partner tiles)
+__device__ __forceinline__ void jit_mbar_init(uint64_t* mb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(mb)) : "memory");
+}
+__device__ __forceinline__ void jit_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+    const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(m), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(m)
+                 : "memory");
+}
+__device__ __forceinline__ void jit_mbar_wait(uint64_t* mb, uint32_t parity) {
+    const unsigned m = (unsigned)__cvta_generic_to_shared(mb);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\n"
+                     : "=r"(done)
+                     : "r"(m), "r"(parity)
+                     : "memory");
+}
+
 }  // namespace qfb
