@@ -226,3 +226,28 @@ def test_invalid_programs_raise_value_error():
         engine.describe_plan(3, [(G["csum"], 0, 1, -1, 1.0, 0.0, -1)], 0)
     with pytest.raises(ValueError, match="not unitary"):
         engine.describe_plan(2, [(G["unitary"], 0, 1, -1, 1.0, 0.0, 0)], 0, mats=[2 * np.eye(4)])
+
+
+def test_searched_schedule_of_the_headline_config():
+    """The C2 template (n = 20, HEA depth 8, complex64) is scheduled by the tile and
+    phase searches into 6 forward + 6 adjoint sweeps with at most 53 phases (the
+    greedy schedule needed 9 + 13 sweeps and 75 phases); every sweep's tile is
+    k bits and every phase's register set R bits."""
+    n, D = 20, 8
+    ops, P = [], 0
+    for _ in range(D):
+        for q in range(n):
+            ops.append((G["ry"], q, -1, P, 1.0, 0.0, -1)); P += 1
+        for q in range(n):
+            ops.append((G["rz"], q, -1, P, 1.0, 0.0, -1)); P += 1
+        for q in range(n - 1):
+            ops.append((G["cx"], q, q + 1, -1, 1.0, 0.0, -1))
+    d = engine.describe_plan(n, ops, P, "c64")["passes"]
+    assert len(d["fwd"]["sweeps"]) == 6 and len(d["bwd"]["sweeps"]) == 6
+    phases = sum(len(s["phases"]) for p in ("fwd", "bwd") for s in d[p]["sweeps"])
+    assert phases <= 53, phases
+    for p in ("fwd", "bwd"):
+        k, R = d[p]["k"], d[p]["R"]
+        for s in d[p]["sweeps"]:
+            assert len(s["tile_bits"]) == k
+            assert all(len(ph["reg_bits"]) == R for ph in s["phases"])
