@@ -186,3 +186,30 @@ def test_hermitian_eigvals_kernel(ctx, m, batch):
         ref = np.linalg.eigvalsh(mats[b])
         scale = max(1.0, np.abs(ref).max())
         assert np.abs(got[b] - ref).max() <= 1e-12 * scale * max(1, m / 64), (b, np.abs(got[b] - ref).max())
+
+
+@pytest.mark.parametrize("prec,tol", [("c128", 1e-10), ("c64", 2e-5)])
+def test_noise_folded_branches_all_arities(ctx, prec, tol):
+    """The last channel's Kraus branch of an op is folded into the next noisy op's
+    pass when their wires are disjoint (apply2_rho): 1q -> 1q, 1q -> 2q, 2q -> 1q
+    and 2q -> 2q hand-overs, plus overlapping ones that are applied alone; states
+    and log-probabilities against the oracle per trajectory."""
+    n = 6
+    ops = []
+    rng = po.Rng(91)
+    for layer in range(3):
+        ops += [(po.GID["cx"], 0, 1, -1, 1.0, 0.0, -1), (po.GID["cx"], 2, 3, -1, 1.0, 0.0, -1),  # 2q -> 2q
+                (po.GID["h"], 4, -1, -1, 1.0, 0.0, -1),                                          # 2q -> 1q
+                (po.GID["cx"], 0, 5, -1, 1.0, 0.0, -1),                                          # 1q -> 2q
+                (po.GID["rx"], 1, -1, -1, 1.0, 3.0 * rng.uniform() - 1.5, -1),                   # 2q -> 1q
+                (po.GID["rx"], 2, -1, -1, 1.0, 3.0 * rng.uniform() - 1.5, -1),                   # 1q -> 1q
+                (po.GID["cx"], 2, 4, -1, 1.0, 0.0, -1)]                                          # overlap
+    op_ch, chans = _channels_for(ops)
+    op_ch = [[0] if op[0] == po.GID["cx"] else ([1, 2] if op[0] == po.GID["h"] else [2]) for op in ops]
+    T = 8
+    n_apps = sum(len(x) for x in op_ch)
+    u = np.array([[rng.uniform() for _ in range(n_apps)] for _ in range(T)])
+    states, logp, _ = engine.noise_trajectories(ctx, n, ops, None, op_ch, chans, u, prec)
+    for t in range(T):
+        ref_s, ref_l = po.mc_trajectory(n, ops, op_ch, chans, u[t])
+        assert np.abs(states[t] - ref_s).max() < tol and abs(logp[t] - ref_l) < tol * 10
