@@ -65,44 +65,80 @@ static bool env_flag_off(const char* name) {
     return e && e[0] == '0';
 }
 
-std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
-                                   const std::vector<std::vector<int>>& preds,
-                                   uint64_t fixed_bits, int budget, int max_items, bool search, int lookahead,
-                                   const std::function<double(const Group&)>* score) {
-    const int n = (int)need.size();
+// Incremental form of the group scheduler (sweeps are chosen one at a time so the
+// caller can hand a sweep's light tail phase back before the next one is chosen).
+class GroupScheduler {
+public:
+    GroupScheduler(const std::vector<uint64_t>& need, const std::vector<std::vector<int>>& preds, uint64_t fixed_bits,
+                   int budget, int max_items, bool search, int lookahead,
+                   const std::function<double(const Group&)>* score)
+        : need_(need), fixed_(fixed_bits), budget_(budget), max_items_(max_items), search_(search),
+          lookahead_(lookahead), score_(score) {
+        const int n = (int)need.size();
+        succ_.resize(n);
+        st_.indeg.assign(n, 0);
+        for (int j = 0; j < n; ++j) {
+            st_.indeg[j] = (int)preds[j].size();
+            for (int p : preds[j]) succ_[p].push_back(j);
+        }
+        for (int j = 0; j < n; ++j)
+            if (st_.indeg[j] == 0) st_.ready.insert(j);
+        st_.remaining = n;
+        uint64_t all_bits = fixed_bits;
+        for (uint64_t m : need) all_bits |= m;
+        nb_ = all_bits ? 64 - __builtin_clzll(all_bits) : 0;
+        win_ = budget - popc(fixed_bits);
+    }
+    int remaining() const { return st_.remaining; }
+    // Give items of the last group back (they were taken last; none of their
+    // successors was taken).
+    void untake(const std::vector<int>& items) {
+        std::set<int> back(items.begin(), items.end());
+        for (int u : items) {
+            ++st_.remaining;
+            for (int sc : succ_[u]) {
+                if (st_.indeg[sc] == 0) st_.ready.erase(sc);
+                ++st_.indeg[sc];
+            }
+        }
+        for (int u : items)
+            if (st_.indeg[u] == 0) st_.ready.insert(u);
+    }
+    // Choose and take the next group; false when nothing fits the budget.
+    bool next(Group& out) {
+        State s_best = st_;
+        Group g = greedy(s_best);
+        if (search_ && win_ > 0) choose(g, s_best);
+        if (g.items.empty()) return false;  // an item needs more bits than the budget
+        st_ = std::move(s_best);
+        out = std::move(g);
+        return true;
+    }
+
+private:
     struct State {
         std::set<int> ready;
         std::vector<int> indeg;
         int remaining = 0;
     };
-    std::vector<std::vector<int>> succ(n);
-    State st;
-    st.indeg.assign(n, 0);
-    for (int j = 0; j < n; ++j) {
-        st.indeg[j] = (int)preds[j].size();
-        for (int p : preds[j]) succ[p].push_back(j);
-    }
-    for (int j = 0; j < n; ++j)
-        if (st.indeg[j] == 0) st.ready.insert(j);
-    st.remaining = n;
-    auto take = [&](State& S, Group& g, int it) {
+    void take(State& S, Group& g, int it) const {
         S.ready.erase(it);
         g.items.push_back(it);
         --S.remaining;
-        for (int s : succ[it])
-            if (--S.indeg[s] == 0) S.ready.insert(s);
-    };
+        for (int sc : succ_[it])
+            if (--S.indeg[sc] == 0) S.ready.insert(sc);
+    }
     // greedy: absorb every ready item that fits, then widen the group's bits by the
     // ready item that needs the fewest extra bits, until the budget is spent
-    auto greedy = [&](State& S) {
+    Group greedy(State& S) const {
         Group g;
-        g.bits = fixed_bits;
+        g.bits = fixed_;
         for (;;) {
             bool progress = true;
-            while (progress && (max_items <= 0 || (int)g.items.size() < max_items)) {
+            while (progress && (max_items_ <= 0 || (int)g.items.size() < max_items_)) {
                 progress = false;
                 for (int it : S.ready) {
-                    if ((need[it] & ~g.bits) == 0) {
+                    if ((need_[it] & ~g.bits) == 0) {
                         take(S, g, it);
                         progress = true;
                         break;
@@ -110,30 +146,30 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
                 }
             }
             int best = -1, best_cost = 1 << 30;
-            if (max_items > 0 && (int)g.items.size() >= max_items) break;
+            if (max_items_ > 0 && (int)g.items.size() >= max_items_) break;
             for (int it : S.ready) {
-                int extra = popc(need[it] & ~g.bits);
-                if (popc(g.bits) + extra <= budget && extra < best_cost) {
+                int extra = popc(need_[it] & ~g.bits);
+                if (popc(g.bits) + extra <= budget_ && extra < best_cost) {
                     best = it;
                     best_cost = extra;
                 }
             }
             if (best < 0) break;
-            g.bits |= need[best];
+            g.bits |= need_[best];
         }
         return g;
-    };
+    }
     // closure of fixed bits: every item reachable through items that fit
-    auto absorb = [&](State& S, uint64_t bits) {
+    Group absorb(State& S, uint64_t bits) const {
         Group g;
         g.bits = bits;
         bool progress = true;
         while (progress) {
             progress = false;
             for (auto itr = S.ready.begin(); itr != S.ready.end();) {
-                if (max_items > 0 && (int)g.items.size() >= max_items) return g;
+                if (max_items_ > 0 && (int)g.items.size() >= max_items_) return g;
                 const int it = *itr;
-                if ((need[it] & ~bits) == 0) {
+                if ((need_[it] & ~bits) == 0) {
                     take(S, g, it);
                     progress = true;
                     itr = S.ready.lower_bound(it);
@@ -143,93 +179,101 @@ std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
             }
         }
         return g;
-    };
-    uint64_t all_bits = fixed_bits;
-    for (uint64_t m : need) all_bits |= m;
-    const int nb = all_bits ? 64 - __builtin_clzll(all_bits) : 0;
-    const int win = budget - popc(fixed_bits);
-    std::vector<Group> out;
-    while (st.remaining > 0) {
-        State s_best = st;
-        Group g = greedy(s_best);
-        if (search && win > 0) {
-            // window search: every run of `win` consecutive bits (above the fixed
-            // ones) is a candidate; the closure with the most items wins, ties keep
-            // the greedy group
-            // candidate bit sets: every win-subset of the free bits when there are few
-            // (C(13, 5) = 1287 at most for phases), else windows of consecutive bits
-            std::vector<uint64_t> cands;
-            const uint64_t freeb = (nb >= 64 ? ~0ull : ((1ull << nb) - 1)) & ~fixed_bits;
-            static const bool exhaustive = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == 'w');
-            if (exhaustive && popc(freeb) <= 14) {
-                std::vector<int> fb;
-                for (int b = 0; b < nb; ++b)
-                    if (freeb >> b & 1) fb.push_back(b);
-                const int m = (int)fb.size();
-                for (uint32_t sel = 0; sel < (1u << m); ++sel) {
-                    if (__builtin_popcount(sel) != win) continue;
-                    uint64_t wbits = 0;
-                    for (int i = 0; i < m; ++i)
-                        if (sel >> i & 1) wbits |= 1ull << fb[i];
-                    cands.push_back(wbits);
-                }
-            } else {
-                for (int s0 = 0; s0 + win <= nb; ++s0) {
-                    const uint64_t wbits = (((win >= 64) ? ~0ull : ((1ull << win) - 1)) << s0);
-                    if (!(wbits & fixed_bits)) cands.push_back(wbits);
-                }
+    }
+    void choose(Group& g, State& s_best) const {
+        // candidate bit sets: every win-subset of the free bits when there are few
+        // (C(13, 5) = 1287 at most for phases), else windows of consecutive bits
+        std::vector<uint64_t> cands;
+        const uint64_t freeb = (nb_ >= 64 ? ~0ull : ((1ull << nb_) - 1)) & ~fixed_;
+        static const bool exhaustive = !(std::getenv("QF_PHASE_SEARCH") && std::getenv("QF_PHASE_SEARCH")[0] == 'w');
+        if (exhaustive && popc(freeb) <= 14) {
+            std::vector<int> fb;
+            for (int b = 0; b < nb_; ++b)
+                if (freeb >> b & 1) fb.push_back(b);
+            const int m = (int)fb.size();
+            for (uint32_t sel = 0; sel < (1u << m); ++sel) {
+                if (__builtin_popcount(sel) != win_) continue;
+                uint64_t wbits = 0;
+                for (int i = 0; i < m; ++i)
+                    if (sel >> i & 1) wbits |= 1ull << fb[i];
+                cands.push_back(wbits);
             }
-            std::vector<std::pair<int, uint64_t>> scored;  // (closure size, bits)
-            for (uint64_t wb : cands) {
-                State s2 = st;
-                scored.push_back({(int)absorb(s2, fixed_bits | wb).items.size(), wb});
-            }
-            if (lookahead > 0 && !scored.empty()) {
-                // two-level: among the best `lookahead` first choices, the one whose
-                // closure plus the best next closure covers the most items
-                std::stable_sort(scored.begin(), scored.end(),
-                                 [](const auto& a, const auto& b) { return a.first > b.first; });
-                int best_total = -1;
-                for (size_t c = 0; c < scored.size() && (int)c < lookahead; ++c) {
-                    State s2 = st;
-                    Group g1 = absorb(s2, fixed_bits | scored[c].second);
-                    int second = 0;
-                    if (s2.remaining > 0)
-                        for (uint64_t wb : cands) {
-                            State s3 = s2;
-                            second = std::max(second, (int)absorb(s3, fixed_bits | wb).items.size());
-                        }
-                    const int total = (int)g1.items.size() + second;
-                    if (total > best_total && g1.items.size() >= g.items.size()) {
-                        best_total = total;
-                        g = std::move(g1);
-                        s_best = std::move(s2);
-                    }
-                }
-            } else if (score) {
-                // caller's cost model (e.g. gates per phase of the resulting sweep)
-                double best = (*score)(g);
-                for (auto& sc : scored) {
-                    State s2 = st;
-                    Group gw = absorb(s2, fixed_bits | sc.second);
-                    const double v = (*score)(gw);
-                    if (v > best) {
-                        best = v;
-                        g = std::move(gw);
-                        s_best = std::move(s2);
-                    }
-                }
-            } else {
-                for (auto& sc : scored)
-                    if (sc.first > (int)g.items.size()) {
-                        State s2 = st;
-                        g = absorb(s2, fixed_bits | sc.second);
-                        s_best = std::move(s2);
-                    }
+        } else {
+            for (int s0 = 0; s0 + win_ <= nb_; ++s0) {
+                const uint64_t wbits = (((win_ >= 64) ? ~0ull : ((1ull << win_) - 1)) << s0);
+                if (!(wbits & fixed_)) cands.push_back(wbits);
             }
         }
-        if (g.items.empty()) return {};  // an item needs more bits than the budget
-        st = std::move(s_best);
+        std::vector<std::pair<int, uint64_t>> scored;  // (closure size, bits)
+        for (uint64_t wb : cands) {
+            State s2 = st_;
+            scored.push_back({(int)absorb(s2, fixed_ | wb).items.size(), wb});
+        }
+        if (lookahead_ > 0 && !scored.empty()) {
+            // two-level: among the best `lookahead` first choices, the one whose
+            // closure plus the best next closure covers the most items
+            std::stable_sort(scored.begin(), scored.end(),
+                             [](const auto& x, const auto& y) { return x.first > y.first; });
+            int best_total = -1;
+            for (size_t c = 0; c < scored.size() && (int)c < lookahead_; ++c) {
+                State s2 = st_;
+                Group g1 = absorb(s2, fixed_ | scored[c].second);
+                int second = 0;
+                if (s2.remaining > 0)
+                    for (uint64_t wb : cands) {
+                        State s3 = s2;
+                        second = std::max(second, (int)absorb(s3, fixed_ | wb).items.size());
+                    }
+                const int total = (int)g1.items.size() + second;
+                if (total > best_total && g1.items.size() >= g.items.size()) {
+                    best_total = total;
+                    g = std::move(g1);
+                    s_best = std::move(s2);
+                }
+            }
+        } else if (score_) {
+            // caller's cost model (e.g. gates per phase of the resulting sweep)
+            double best = (*score_)(g);
+            for (auto& sc : scored) {
+                State s2 = st_;
+                Group gw = absorb(s2, fixed_ | sc.second);
+                const double v = (*score_)(gw);
+                if (v > best) {
+                    best = v;
+                    g = std::move(gw);
+                    s_best = std::move(s2);
+                }
+            }
+        } else {
+            for (auto& sc : scored)
+                if (sc.first > (int)g.items.size()) {
+                    State s2 = st_;
+                    g = absorb(s2, fixed_ | sc.second);
+                    s_best = std::move(s2);
+                }
+        }
+    }
+
+    const std::vector<uint64_t>& need_;
+    std::vector<std::vector<int>> succ_;
+    State st_;
+    uint64_t fixed_;
+    int budget_, max_items_;
+    bool search_;
+    int lookahead_;
+    const std::function<double(const Group&)>* score_;
+    int nb_ = 0, win_ = 0;
+};
+
+std::vector<Group> schedule_groups(const std::vector<uint64_t>& need,
+                                   const std::vector<std::vector<int>>& preds,
+                                   uint64_t fixed_bits, int budget, int max_items, bool search, int lookahead,
+                                   const std::function<double(const Group&)>* score) {
+    GroupScheduler gs(need, preds, fixed_bits, budget, max_items, search, lookahead, score);
+    std::vector<Group> out;
+    while (gs.remaining() > 0) {
+        Group g;
+        if (!gs.next(g)) return {};
         out.push_back(std::move(g));
     }
     return out;
@@ -469,10 +513,21 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
         const auto ph = schedule_groups(ln, lp, 0, R, 0, true);
         return (double)gw.items.size() / std::max(1.5, (double)ph.size());
     };
-    auto sweeps = schedule_groups(need, preds_in_order, fixed, k, max_ops, sweep_search, sweep_look,
-                                  ratio_obj ? &ratio_score : nullptr);
-
-    for (auto& sw : sweeps) {
+    GroupScheduler gsched(need, preds_in_order, fixed, k, max_ops, sweep_search, sweep_look,
+                          ratio_obj ? &ratio_score : nullptr);
+    // A sweep whose last phase is a light tail (at most `tail_max` gates that need
+    // register bits) hands that phase's gates back to the next sweep, saving a
+    // shared-memory exchange (QF_TAIL_MAX, development A/B; -1 = off).
+    static const int tail_max = [] {
+        const char* e = std::getenv("QF_TAIL_MAX");
+        return e ? std::atoi(e) : -1;
+    }();
+    Group sw;
+    while (gsched.remaining() > 0) {
+        if (!gsched.next(sw)) {
+            out.sweeps.clear();  // an item needs more bits than the tile (reported by the caller)
+            return;
+        }
         // pad the tile to exactly k bits with the lowest free positions
         uint64_t bits = sw.bits;
         for (int p = 0; p < n && popc(bits) < k; ++p) bits |= 1ull << p;
@@ -520,6 +575,16 @@ static void lower_pass(const ProgramPlan& P, const std::vector<int>& order,
             return e ? std::atoi(e) : 0;
         }();
         auto phases = schedule_groups(lneed, lpreds, 0, R, 0, phase_search, phase_look);
+        if (tail_max >= 0 && phases.size() > 1) {
+            int nd = 0;
+            for (int li : phases.back().items) nd += lneed[li] != 0;
+            if (nd <= tail_max) {
+                std::vector<int> back;
+                for (int li : phases.back().items) back.push_back(sw.items[li]);
+                gsched.untake(back);
+                phases.pop_back();
+            }
+        }
         // Inside a phase, issue ready non-diagonal gates first and release the
         // diagonal ones (which commute with each other) in batches: long runs of
         // diagonal gates and Z taps are fused by the kernel generator.
